@@ -1,0 +1,372 @@
+"""Benchmark: VGG-16 conv stack, NHWC fp32, batch 32 per GPU (BASELINE.json
+configs[1]; configs[4] when run on 8 GPUs = batch 256 sharded by batch).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--precision tf32|fp32]
+    python bench.py --impl reference ...     # the reference CPU implementation
+
+One step = every conv layer of VGG-16 (13 layers, 9 distinct shapes from
+proj/data/vgg_layers.csv with the canonical multiplicities) on its own
+resident synthetic input, through the C ABI (tk_conv2d_dev).  Metric: total
+conv_flops (conv.hpp:19-23; direct-equivalent, the reference's GFLOP/s
+convention) / device time.  Timing: CUDA events on the launching stream, L2
+flushed (256 MiB write) between steps outside the timed events, max over
+ranks.  `e2e` runs the same layers through the host-buffer C ABI
+(tk_conv2d_ex) with pinned host buffers: H2D of input+filter and D2H of the
+output are inside its timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# (name, H=W, C, K, multiplicity) -- vgg_layers.csv + VGG-16 topology
+VGG16 = [
+    ("vgg_conv1_1", 224, 3, 64, 1), ("vgg_conv1_2", 224, 64, 64, 1),
+    ("vgg_conv2_1", 112, 64, 128, 1), ("vgg_conv2_2", 112, 128, 128, 1),
+    ("vgg_conv3_1", 56, 128, 256, 1), ("vgg_conv3_2", 56, 256, 256, 2),
+    ("vgg_conv4_1", 28, 256, 512, 1), ("vgg_conv4_2", 28, 512, 512, 2),
+    ("vgg_conv5", 14, 512, 512, 3),
+]
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def conv_flops(n, h, c, k):
+    return 2 * n * h * h * k * 9 * c
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--batch", type=int, default=32, help="images per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the unmodified reference on the host cores
+# ---------------------------------------------------------------------------
+def cpu_reference_sample(layers_batch=1, algos=None):
+    """Times the reference's own conv2d (oracle/_ref = ref_shim.cpp over the
+    reference headers; falls back to the C restatement) on every VGG-16
+    layer at batch `layers_batch`, best algorithm per layer.  Returns
+    (gflops, seconds, cores, kind, detail)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("TILEKIT_THREADS", str(cores))
+    kind = "reference" if O.have_ref() else "port"
+    algos = algos or ["im2col", "winograd_t4x4", "winograd_t2x2"]
+    total_flops, total_s, detail = 0, 0.0, []
+    for name, h, c, k, mult in VGG16:
+        s = O.Conv(layers_batch, h, h, c, k, 3, 3, 1, True)
+        x = O.fill_random(int(np.prod(s.in_shape)), 1).reshape(s.in_shape)
+        f = O.fill_random(int(np.prod(s.filt_shape)), 2).reshape(s.filt_shape)
+        best = None
+        for a in algos:
+            t0 = time.perf_counter()
+            if kind == "reference":
+                O.ref_conv2d(s, a, x, f)
+            elif a.startswith("winograd"):
+                O.conv2d_winograd(s, int(a[-1]), x, f)
+            else:
+                O.conv2d_naive(s, x, f)
+            dt = time.perf_counter() - t0
+            if best is None or dt < best[1]:
+                best = (a, dt)
+        total_flops += s.flops() * mult
+        total_s += best[1] * mult
+        detail.append(f"{name}:{best[0]}")
+    return total_flops / total_s / 1e9, total_s, cores, kind, detail
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    O.build()
+    for _ in range(args.warmup):
+        cpu_reference_sample(algos=["winograd_t4x4"])
+    vals = []
+    t_all = 0.0
+    for _ in range(args.steps):
+        g, s, cores, kind, detail = cpu_reference_sample(algos=["winograd_t4x4", "im2col"])
+        vals.append(g)
+        t_all += s
+    value = float(np.median(vals))
+    flops_b1 = sum(conv_flops(1, h, c, k) * m for _, h, c, k, m in VGG16)
+    line = {
+        "impl": "reference", "metric": "VGG16 conv-stack GFLOP/s (conv_flops / time)",
+        "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * t_all / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (fill_random, tuner.hpp:293-297)",
+        "config": {"workload": "VGG16 13 conv layers, NHWC fp32, batch 1 sample per step "
+                               "(bounded CPU sample of the batch-32 workload)",
+                   "algorithms": detail, "step_gflop": flops_b1 / 1e9},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores, "kind": kind,
+                         "sample": "13 VGG16 layers at batch 1, best of reference winograd_t4x4/im2col per layer"},
+        "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1904_05347_b200 as tk
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    N = args.batch
+    prec = args.precision
+
+    # Resident inputs: one independent seeded input + filter per layer
+    # instance (the reference `layers` harness, tilekit_cli.cpp:374-403).
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    layers = []
+    for name, h, c, k, mult in VGG16:
+        for rep in range(mult):
+            shape = tk.ConvShape(N, h, h, c, k, 3, 3, 1, True)
+            algo = tk.parse_conv_params("im2col")
+            x = torch.rand((N, h, h, c), device=dev, generator=gen) * 2 - 1
+            f = torch.rand((3, 3, c, k), device=dev, generator=gen) * 2 - 1
+            y = torch.empty((N, h, h, k), device=dev)
+            ws_n = tk.conv2d_workspace_size(shape, algo, prec)
+            ws = torch.empty(max(ws_n, 4) // 4 + 1, device=dev)
+            layers.append(dict(name=name, shape=shape, algo=algo, x=x, f=f, y=y, ws=ws,
+                               flops=conv_flops(N, h, c, k)))
+    flush = torch.empty(64 * 1024 * 1024, device=dev)  # 256 MiB > 126 MB L2
+    step_flops = sum(L["flops"] for L in layers)
+
+    def step():
+        for L in layers:
+            tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=prec,
+                          workspace=L["ws"], stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # Per-layer device times (same stream, CUDA events), for the roofline.
+    per_layer = []
+    for L in layers:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        flush.zero_()
+        ev[0].record(stream)
+        tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=prec,
+                      workspace=L["ws"], stream=stream)
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        per_layer.append(ev[0].elapsed_time(ev[1]))
+
+    # Timed steps.
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = tk.launch_count()
+    times = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = tk.launch_count() - launches0
+    torch.cuda.synchronize()
+    total_ms = float(sum(times))
+    t = torch.tensor([total_ms], device=dev)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = step_flops * world / (ms_per_step * 1e-3) / 1e9
+
+    # End-to-end through the host-buffer C ABI (pinned host memory).
+    e2e = None
+    if not args.no_e2e:
+        host = []
+        for L in layers:
+            if L["name"] in [h["name"] for h in host]:
+                continue
+            host.append(dict(name=L["name"], shape=L["shape"], algo=L["algo"],
+                             x=L["x"].cpu().pin_memory().numpy(), f=L["f"].cpu().pin_memory().numpy(),
+                             y=torch.empty(tuple(L["y"].shape)).pin_memory().numpy()))
+        by_name = {h["name"]: h for h in host}
+        seq = [by_name[L["name"]] for L in layers]
+        h2d = sum(h["x"].nbytes + h["f"].nbytes for h in seq)
+        d2h = sum(h["y"].nbytes for h in seq)
+        for h in seq:  # warm the pool allocator
+            out = tk.conv2d(h["x"], h["f"], h["shape"], h["algo"], precision=prec)
+        e2e_steps = max(1, min(args.steps, 3))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            for h in seq:
+                lib = tk.lib()
+                rc = lib.tk_conv2d_ex(ctypes.byref(h["shape"].c()), ctypes.byref(h["algo"].c()),
+                                      ctypes.byref(tk.exec_options(prec)),
+                                      h["x"].ctypes.data_as(ctypes.c_void_p),
+                                      h["f"].ctypes.data_as(ctypes.c_void_p),
+                                      h["y"].ctypes.data_as(ctypes.c_void_p))
+                tk._check(rc)
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        te = torch.tensor([e2e_s], device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        e2e = {"value": round(step_flops * world / e2e_s / 1e9, 2), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": round(e2e_s * 1e3, 3), "api": "tk_conv2d_ex (host buffers)"}
+
+    peaks, peaks_kind = load_peaks()
+    # Dominant kernel: the implicit-GEMM conv (tc_gemm_kernel) -- its share
+    # is the whole step except the tiny filter-pack launches.
+    lay_ms = float(sum(per_layer))
+    achieved_tf = step_flops / (lay_ms * 1e-3) / 1e12
+    if prec == "tf32":
+        peak_tf = peaks["bf16_tflops"] / 2.0
+        peak_note = f"TF32 = 1/2 of {peaks_kind} bf16 burst {peaks['bf16_tflops']} TF/s"
+    else:
+        peak_tf = 148 * 128 * 2 * 1.965e9 / 1e12 / 2
+        peak_note = "FP32 exact FMUL+FADD cap = 1/2 of 74.4 TF/s FFMA"
+    roofline = {"bound": "tensor", "achieved": round(achieved_tf, 2), "peak": round(peak_tf, 1),
+                "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4), "traffic": None,
+                "kernel": "tc_gemm_kernel (implicit-GEMM conv)" if prec == "tf32" else "exact_gemm_loc_kernel",
+                "peak_source": peak_note}
+
+    layer_rows = []
+    for L, ms in zip(layers, per_layer):
+        layer_rows.append({"layer": L["name"], "ms": round(ms, 4),
+                           "tflops": round(L["flops"] / (ms * 1e-3) / 1e12, 2)})
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        g, s, cores, kind, detail = cpu_reference_sample()
+        cpu = {"value": round(g, 3), "unit": "GFLOP/s", "cores": cores, "kind": kind,
+               "sample": "13 VGG16 layers at batch 1 (1/32 of a step), best of reference "
+                         "im2col/winograd_t4x4/winograd_t2x2 per layer", "seconds": round(s, 2)}
+
+    if rank == 0:
+        line = {
+            "metric": "VGG16 conv-stack GFLOP/s (conv_flops / time)",
+            "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "tf32" if prec == "tf32" else "f32",
+            "data": "synthetic (uniform[-1,1) via torch, per-layer independent inputs)",
+            "config": {"workload": "VGG16 13 conv layers (3x3/s1/Same, NHWC fp32)",
+                       "batch_per_gpu": N, "global_batch": N * world,
+                       "algorithm": "im2col implicit GEMM",
+                       "precision": prec, "step_gflop": round(step_flops / 1e9, 2),
+                       "l2": "flushed between steps (256 MiB write, outside events)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clocks.summary(), "layers": layer_rows,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,213 @@
+/*
+ * tk_b200.h -- C ABI of the B200-native tilekit kernels (libtilekit_b200.so).
+ *
+ * This is the drop-in boundary.  The reference (tilekit, a header-only C++20
+ * library) has no FFI of its own; its public entry points are the inline
+ * functions listed next to each declaration below.  The C++ headers in
+ * include/tilekit/ keep those signatures verbatim and forward here, so a
+ * caller of the reference recompiles unchanged.  Anything else (Python
+ * ctypes, another language's FFI) binds these symbols directly; see
+ * INTEGRATION.md.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; no C++ or torch types.
+ *  - matrices are column-major (element (i,j) at i + j*rows), 4-D tensors are
+ *    row-major NHWC (inputs/outputs) and HWCK (filters), exactly the
+ *    reference layouts (tensor.hpp:12-111).
+ *  - every function returns TK_OK or an error code; the message is
+ *    available from tk_last_error() (thread-local).  Codes map 1:1 onto the
+ *    reference exception classes (errors.hpp:9-59).
+ *  - "host" entry points take HOST buffers and do the device copies inside;
+ *    "_dev" entry points take caller-owned DEVICE buffers and an explicit
+ *    cudaStream_t (passed as void*), launch asynchronously and allocate
+ *    nothing once their workspace is provided.
+ *  - there is no CPU fallback: without a usable sm_100 GPU every compute
+ *    entry point returns TK_ERR_CUDA.
+ */
+#ifndef TK_B200_H_
+#define TK_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TK_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TK_API __attribute__((visibility("default")))
+#else
+#define TK_API
+#endif
+
+/* Status codes: one per reference exception class (errors.hpp:16-56). */
+enum tk_status {
+  TK_OK = 0,
+  TK_ERR_SHAPE = 1,      /* ShapeError      */
+  TK_ERR_CONFIG = 2,     /* ConfigError     */
+  TK_ERR_PARSE = 3,      /* ParseError      */
+  TK_ERR_CAPABILITY = 4, /* CapabilityError */
+  TK_ERR_CONTRACT = 5,   /* ContractError   */
+  TK_ERR_IO = 6,         /* IoError         */
+  TK_ERR_TUNING = 7,     /* TuningError     */
+  TK_ERR_CUDA = 8        /* device failure / no B200 (no reference twin) */
+};
+
+/* Arithmetic of the contraction.  The reference is FP32 with separate
+ * multiply and add roundings; TK_PREC_FP32_EXACT reproduces it bit for bit
+ * (FMUL+FADD, ascending k, no split-K).  The tensor-core precisions are the
+ * B200 extension and are judged with max_scaled_error (numeric.hpp:39-56). */
+enum tk_precision {
+  TK_PREC_FP32_EXACT = 0, /* SIMT, bit-identical to gemm_naive/conv2d_naive */
+  TK_PREC_TF32 = 1,       /* tcgen05 kind::tf32, fp32 accumulate            */
+  TK_PREC_BF16 = 2,       /* tcgen05 kind::f16 (bf16 operands), fp32 accum. */
+  TK_PREC_3XTF32 = 3      /* split-precision tf32 (hi/lo, three MMAs)       */
+};
+
+/* GemmShape (config.hpp:19-37).  op: 0 = Op::Identity, 1 = Op::Transpose. */
+typedef struct tk_gemm_shape {
+  size_t m, n, k;
+  float alpha, beta;
+  int op_a, op_b;
+} tk_gemm_shape;
+
+/* GemmConfig (config.hpp:42-65): h x w register tile, r x c work-group. */
+typedef struct tk_gemm_config {
+  size_t reg_rows, reg_cols; /* h, w */
+  size_t wg_rows, wg_cols;   /* r, c */
+  int use_local_memory;      /* _loc  */
+  int double_buffer;         /* _db   */
+  size_t k_step;
+} tk_gemm_config;
+
+/* DeviceSpec (device.hpp:20-50).  name may be NULL. */
+typedef struct tk_device_spec {
+  const char* name;
+  size_t cache_line_bytes;
+  size_t local_memory_bytes;
+  size_t compute_units;
+  size_t register_budget;
+  size_t max_workgroup_size;
+} tk_device_spec;
+
+/* ConvShape (config.hpp:137-195).  padding: 0 = Valid, 1 = Same. */
+typedef struct tk_conv_shape {
+  size_t batch, in_rows, in_cols, channels, features;
+  size_t window_rows, window_cols, stride;
+  int padding;
+} tk_conv_shape;
+
+/* ConvAlgoParams (config.hpp:198-241).
+ * algo: 0 = Naive, 1 = Tiled, 2 = Im2col, 3 = Winograd. */
+typedef struct tk_conv_params {
+  int algo;
+  size_t tile_rows, tile_cols;
+  size_t channel_vector, feature_vector;
+} tk_conv_params;
+
+/* B200 execution options (the extension struct of SURVEY.md 8(b); the
+ * reference structs stay untouched).  Zero-initialised = reference
+ * semantics: exact FP32, library-chosen kernel shape. */
+typedef struct tk_exec_options {
+  int precision;     /* enum tk_precision                                  */
+  int tc_tile_n;     /* tensor-core N tile (0 = auto; 64/128/192/256)       */
+  int tc_stages;     /* smem pipeline depth (0 = auto)                      */
+  int reserved[5];
+} tk_exec_options;
+
+/* ---- library --------------------------------------------------------- */
+TK_API const char* tk_last_error(void);
+TK_API int tk_abi_version(void);
+/* Number of usable sm_100 devices (0 when none; never an error). */
+TK_API int tk_device_count(void);
+/* DeviceSpec describing the current B200 (cudaGetDeviceProperties):
+ * 128 B lines, 227 KiB opt-in shared memory, 148 SMs, 255 registers,
+ * 1024 threads.  Kept out of builtin_devices(). */
+TK_API int tk_b200_device_spec(tk_device_spec* out);
+/* Kernels launched by this library since load (all streams); used by the
+ * bench to report gpu_launches. */
+TK_API uint64_t tk_launch_count(void);
+TK_API int tk_synchronize(void);
+
+/* ---- validation (host-only, no GPU needed) ---------------------------- */
+/* validate_config (gemm.hpp:103-146): writes the "; "-joined violation
+ * list (or "valid") into msg and sets *ok. */
+TK_API int tk_validate_gemm_config(const tk_gemm_config* cfg, const tk_device_spec* dev,
+                            int* ok, char* msg, size_t msg_cap);
+/* local_mem_elems (gemm.hpp:71-80). */
+TK_API int tk_local_mem_elems(const tk_gemm_config* cfg, const tk_device_spec* dev,
+                       size_t* elems);
+
+/* ---- GEMM ------------------------------------------------------------- */
+/* gemm_tiled (gemm.hpp:308-445).  a/b are the STORED operands (m x k or
+ * k x m when transposed, etc.), c is m x n, out is m x n.  c is not read
+ * when beta == 0.  Host buffers. */
+TK_API int tk_gemm_tiled(const tk_gemm_shape* shape, const tk_gemm_config* cfg,
+                  const tk_device_spec* dev, const float* a, const float* b,
+                  const float* c, float* out);
+/* gemm_naive (gemm.hpp:194-213): same arithmetic on the GPU. */
+TK_API int tk_gemm_naive(const tk_gemm_shape* shape, const float* a, const float* b,
+                  const float* c, float* out);
+/* gemm_batched_strided (gemm.hpp:451-479); *multiplies gets the count. */
+TK_API int tk_gemm_batched_strided(const float* a, size_t stride_a, const float* b,
+                            size_t stride_b, float* c, size_t stride_c,
+                            size_t batch, size_t m, size_t n, size_t k,
+                            uint64_t* multiplies);
+/* Device-buffer GEMM.  cfg may be NULL (library choice); opts may be NULL
+ * (exact FP32).  Tensor-core precisions ignore cfg. */
+TK_API int tk_gemm_dev(const tk_gemm_shape* shape, const tk_gemm_config* cfg,
+                const tk_exec_options* opts, const float* d_a, const float* d_b,
+                const float* d_c, float* d_out, void* stream);
+TK_API int tk_gemm_batched_strided_dev(const float* d_a, size_t stride_a,
+                                const float* d_b, size_t stride_b, float* d_c,
+                                size_t stride_c, size_t batch, size_t m,
+                                size_t n, size_t k, const tk_exec_options* opts,
+                                void* stream);
+
+/* ---- convolution ------------------------------------------------------ */
+/* conv2d selector (winograd.hpp:304-314) and the per-algorithm entry
+ * points (conv.hpp:74, :136, :320, :353; winograd.hpp:169).  Host buffers:
+ * in NHWC, filt HWCK, out NHWC (batch x out_rows x out_cols x features). */
+TK_API int tk_conv2d(const tk_conv_shape* shape, const tk_conv_params* params,
+              const float* in, const float* filt, float* out);
+TK_API int tk_conv2d_naive(const tk_conv_shape* shape, const float* in,
+                    const float* filt, float* out);
+TK_API int tk_conv2d_tiled(const tk_conv_shape* shape, const tk_conv_params* params,
+                    const float* in, const float* filt, float* out);
+/* conv2d_im2col with an explicit GEMM config + device (conv.hpp:320-351). */
+TK_API int tk_conv2d_im2col(const tk_conv_shape* shape, const tk_gemm_config* cfg,
+                     const tk_device_spec* dev, const float* in,
+                     const float* filt, float* out);
+/* conv2d_winograd (winograd.hpp:169-301); stats may be NULL. */
+TK_API int tk_conv2d_winograd(const tk_conv_shape* shape, const tk_conv_params* params,
+                       const float* in, const float* filt, float* out,
+                       uint64_t* batched_multiplies, size_t* tiles);
+/* im2col (conv.hpp:255-300): column-major (N*OH*OW) x (R*S*C). */
+TK_API int tk_im2col(const tk_conv_shape* shape, const float* in, float* patches);
+/* filter_matrix (conv.hpp:304-317): HWCK -> column-major (R*S*C) x K. */
+TK_API int tk_filter_matrix(size_t r, size_t s, size_t c, size_t k, const float* filt,
+                     float* mat);
+
+/* Device-buffer convolution through the selector.  workspace may be NULL
+ * (library-owned, grown on first use; not allocation-free then). */
+TK_API int tk_conv2d_dev(const tk_conv_shape* shape, const tk_conv_params* params,
+                  const tk_exec_options* opts, const float* d_in,
+                  const float* d_filt, float* d_out, void* d_workspace,
+                  size_t workspace_bytes, void* stream);
+TK_API int tk_conv2d_workspace_size(const tk_conv_shape* shape,
+                             const tk_conv_params* params,
+                             const tk_exec_options* opts, size_t* bytes);
+/* Same as tk_conv2d but with the exec options (host buffers). */
+TK_API int tk_conv2d_ex(const tk_conv_shape* shape, const tk_conv_params* params,
+                 const tk_exec_options* opts, const float* in,
+                 const float* filt, float* out);
+TK_API int tk_im2col_dev(const tk_conv_shape* shape, const float* d_in,
+                  float* d_patches, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TK_B200_H_ */

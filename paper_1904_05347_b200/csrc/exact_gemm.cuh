@@ -1,0 +1,403 @@
+// exact_gemm.cuh -- bit-exact FP32 SIMT tiled GEMM / implicit-GEMM conv.
+//
+// One kernel family implements every exact path of the reference:
+//   gemm_naive / gemm_tiled        (gemm.hpp:194-213, 308-445)
+//   gemm_batched_strided           (gemm.hpp:451-479; gridDim.z = batch)
+//   conv2d_naive / _tiled / _im2col (conv.hpp:74-113, 136-248, 320-362) as an
+//       implicit GEMM whose K index runs over window taps (x, y, c) in the
+//       reference order (x*S + y)*C + c, gathered straight from NHWC input.
+//
+// Parity contract: every output element is one
+// running sum started at +0 and updated acc = fadd_rn(acc, fmul_rn(a, b)) in
+// ascending k; out = alpha*acc (beta == 0, C never read) or
+// alpha*acc + beta*C.  Zero-filled tails and halos add +0 and leave the bits
+// unchanged, so the result equals the reference bit for bit whatever the
+// tiling.  No FFMA, no split-K.
+//
+// Parameterisation follows GemmConfig: each thread owns an H x W register
+// tile (reg_rows x reg_cols), a CTA is wg_rows x wg_cols threads, "loc"
+// stages K-slabs of BK = 32 elements (one 128-byte line, the paper's X)
+// through shared memory with cp.async, "db" deepens that to a multi-stage
+// ring, "noloc" reads operands straight from global memory.
+#pragma once
+
+#include "common.cuh"
+
+namespace tkb {
+
+constexpr int kExactBK = 32;
+
+enum OperandMajor : int { kMN = 0, kK = 1 };
+
+// Element (m, k) of A lives at a[m*a_sm + k*a_sk]; (k, n) of B at
+// b[k*b_sk + n*b_sn]; (m, n) of C/D at d[m*d_sm + n*d_sn].  In conv mode A is
+// the implicit patch matrix of an NHWC input.
+struct ExactArgs {
+  int M, N, K;
+  const float* a;
+  long long a_sm, a_sk, a_batch;
+  const float* b;
+  long long b_sk, b_sn, b_batch;
+  const float* c;
+  float* d;
+  long long d_sm, d_sn, d_batch;
+  float alpha, beta;
+  int read_c;   // beta != 0
+  int tx_on_m;  // lane-fast thread index runs along M (column-major output)
+  // conv geometry (CONV instantiations only)
+  int H, W, C, OH, OW, R, S, stride, pad_t, pad_l;
+};
+
+// Ownership of register-tile rows: MN-major operands hand each thread runs of
+// 4 consecutive indices (16-byte shared loads, conflict-free), K-major
+// operands interleave single indices (row stride 36 words spreads banks).
+template <int T, int LAYOUT>
+__device__ __forceinline__ int own_index(int t, int threads, int u) {
+  if constexpr (LAYOUT == kMN) {
+    if constexpr (T >= 4) {
+      return (u >> 2) * (threads * 4) + t * 4 + (u & 3);
+    } else {
+      return t * T + u;
+    }
+  } else {
+    return u * threads + t;
+  }
+}
+
+// Shared-memory geometry of one operand slab (BK deep, E wide).
+template <int LAYOUT>
+struct SlabGeom {
+  // MN-major: [BK][E+4]; K-major: [E][BK+4]
+  static __device__ __forceinline__ int off(int e, int k, int E) {
+    if constexpr (LAYOUT == kMN) return k * (E + 4) + e;
+    else return e * (kExactBK + 4) + k;
+  }
+  static __host__ __device__ __forceinline__ int words(int E) {
+    return LAYOUT == kMN ? kExactBK * (E + 4) : E * (kExactBK + 4);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Global -> shared staging of one K-slab.
+// ---------------------------------------------------------------------------
+
+// Plain strided operand (GEMM and batched GEMM).  `e` indexes the M (or N)
+// extent, k the depth.  stride_e / stride_k are element strides.
+template <int LAYOUT>
+__device__ __forceinline__ void stage_matrix(float* sm, const float* g, long long stride_e,
+                                             long long stride_k, int e0, int E, int e_lim, int k0,
+                                             int k_lim, int tid, int nthreads) {
+  // Vector chunks of 4 along the contiguous direction of the operand (rows
+  // of an MN-major slab are padded by 4 words, so a ragged last chunk lands
+  // in the padding).
+  const int chunks = LAYOUT == kMN ? ((E + 3) >> 2) * kExactBK : E * (kExactBK >> 2);
+  for (int ch = tid; ch < chunks; ch += nthreads) {
+    int e, k;
+    if constexpr (LAYOUT == kMN) {
+      const int per_row = (E + 3) >> 2;
+      k = ch / per_row;
+      e = (ch - k * per_row) << 2;
+    } else {
+      k = (ch & 7) << 2;  // BK/4 = 8 chunks per row
+      e = ch >> 3;
+    }
+    const int ge = e0 + e, gk = k0 + k;
+    float* dst = sm + SlabGeom<LAYOUT>::off(e, k, E);
+    if constexpr (LAYOUT == kMN) {
+      const float* src = g + (long long)ge * stride_e + (long long)gk * stride_k;
+      const bool full = gk < k_lim && ge + 3 < e_lim && stride_e == 1 &&
+                        ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+      if (full) {
+        cp_async16(dst, src, true);
+      } else {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const bool ok = gk < k_lim && ge + v < e_lim;
+          cp_async4(dst + v, ok ? src + (long long)v * stride_e : g, ok);
+        }
+      }
+    } else {
+      const float* src = g + (long long)ge * stride_e + (long long)gk * stride_k;
+      const bool full = ge < e_lim && gk + 3 < k_lim && stride_k == 1 &&
+                        ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+      if (full) {
+        cp_async16(dst, src, true);
+      } else {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const bool ok = ge < e_lim && gk + v < k_lim;
+          cp_async4(dst + v, ok ? src + (long long)v * stride_k : g, ok);
+        }
+      }
+    }
+  }
+}
+
+// Implicit patch matrix of an NHWC input: row m = (n*OH + oh)*OW + ow,
+// column k = (x*S + y)*C + c.  Taps outside the input stage as zero.
+__device__ __forceinline__ void stage_patches(float* sm, const ExactArgs& p, int m0, int BM,
+                                              int k0, int tid, int nthreads) {
+  const int chunks = BM * (kExactBK >> 2);
+  const bool vec_ok = (p.C & 3) == 0;
+  for (int ch = tid; ch < chunks; ch += nthreads) {
+    const int kq = (ch & 7) << 2;
+    const int e = ch >> 3;
+    const int m = m0 + e;
+    const int k = k0 + kq;
+    float* dst = sm + SlabGeom<kK>::off(e, kq, BM);
+    int n = 0, oh = 0, ow = 0;
+    const bool row_ok = m < p.M;
+    if (row_ok) {
+      ow = m % p.OW;
+      const int t = m / p.OW;
+      oh = t % p.OH;
+      n = t / p.OH;
+    }
+    if (vec_ok && k + 3 < p.K) {
+      // Four consecutive channels of one tap.
+      const int c = k % p.C;
+      const int tap = k / p.C;
+      const int y = tap % p.S, x = tap / p.S;
+      const int ih = oh * p.stride + x - p.pad_t;
+      const int iw = ow * p.stride + y - p.pad_l;
+      const bool ok = row_ok && ih >= 0 && iw >= 0 && ih < p.H && iw < p.W;
+      const float* src = ok ? p.a + (((long long)n * p.H + ih) * p.W + iw) * p.C + c : p.a;
+      if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        cp_async16(dst, src, ok);
+      } else {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) cp_async4(dst + v, ok ? src + v : p.a, ok);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int kk = k + v;
+        bool ok = row_ok && kk < p.K;
+        const float* src = p.a;
+        if (ok) {
+          const int c = kk % p.C;
+          const int tap = kk / p.C;
+          const int y = tap % p.S, x = tap / p.S;
+          const int ih = oh * p.stride + x - p.pad_t;
+          const int iw = ow * p.stride + y - p.pad_l;
+          ok = ih >= 0 && iw >= 0 && ih < p.H && iw < p.W;
+          if (ok) src = p.a + (((long long)n * p.H + ih) * p.W + iw) * p.C + c;
+        }
+        cp_async4(dst + v, src, ok);
+      }
+    }
+  }
+}
+
+// Load the register fragment of one depth step from a staged slab.
+template <int T, int LAYOUT>
+__device__ __forceinline__ void load_frag(float (&f)[T], const float* sm, int t, int threads,
+                                          int E, int k) {
+  if constexpr (LAYOUT == kMN && T >= 4) {
+#pragma unroll
+    for (int q = 0; q < T / 4; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(
+          sm + SlabGeom<kMN>::off(own_index<T, kMN>(t, threads, q * 4), k, E));
+      f[q * 4 + 0] = v.x;
+      f[q * 4 + 1] = v.y;
+      f[q * 4 + 2] = v.z;
+      f[q * 4 + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < T; ++u) f[u] = sm[SlabGeom<LAYOUT>::off(own_index<T, LAYOUT>(t, threads, u), k, E)];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The kernel.  H x W register tile, blockDim.x = r*c threads.
+// ---------------------------------------------------------------------------
+template <int H, int W, int AL, int BL, bool CONV>
+__global__ void exact_gemm_loc_kernel(ExactArgs p, int wg_r, int wg_c, int stages) {
+  extern __shared__ __align__(16) float smem[];
+  const int tid = threadIdx.x;
+  const int nthreads = wg_r * wg_c;
+  const int BM = H * wg_r, BN = W * wg_c;
+  const int tm = p.tx_on_m ? tid % wg_r : tid / wg_c;
+  const int tn = p.tx_on_m ? tid / wg_r : tid % wg_c;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int z = blockIdx.z;
+
+  const float* ga = p.a + (CONV ? 0 : (long long)z * p.a_batch);
+  const float* gb = p.b + (long long)z * p.b_batch;
+
+  const int a_words = SlabGeom<AL>::words(BM), b_words = SlabGeom<BL>::words(BN);
+  const int stage_words = a_words + b_words;
+
+  float acc[H][W];
+#pragma unroll
+  for (int i = 0; i < H; ++i)
+#pragma unroll
+    for (int j = 0; j < W; ++j) acc[i][j] = 0.0f;
+
+  const int nslabs = (p.K + kExactBK - 1) / kExactBK;
+
+  auto issue = [&](int s) {
+    float* sa = smem + (s % stages) * stage_words;
+    float* sb = sa + a_words;
+    const int k0 = s * kExactBK;
+    if constexpr (CONV) {
+      stage_patches(sa, p, m0, BM, k0, tid, nthreads);
+    } else {
+      stage_matrix<AL>(sa, ga, p.a_sm, p.a_sk, m0, BM, p.M, k0, p.K, tid, nthreads);
+    }
+    stage_matrix<BL>(sb, gb, p.b_sn, p.b_sk, n0, BN, p.N, k0, p.K, tid, nthreads);
+  };
+
+  // Prologue: stages-1 slabs in flight.
+  for (int s = 0; s < stages - 1; ++s) {
+    if (s < nslabs) issue(s);
+    cp_async_commit();
+  }
+  for (int s = 0; s < nslabs; ++s) {
+    if (stages == 1) {
+      issue(s);
+      cp_async_commit();
+      cp_async_wait<0>();
+    } else {
+      const int nxt = s + stages - 1;
+      if (nxt < nslabs) issue(nxt);
+      cp_async_commit();
+      cp_async_wait_dyn(stages - 1);
+    }
+    __syncthreads();
+    const float* sa = smem + (s % stages) * stage_words;
+    const float* sb = sa + a_words;
+    const int depth = min(kExactBK, p.K - s * kExactBK);
+#pragma unroll 4
+    for (int k = 0; k < depth; ++k) {
+      float fa[H], fb[W];
+      load_frag<H, AL>(fa, sa, tm, wg_r, BM, k);
+      load_frag<W, BL>(fb, sb, tn, wg_c, BN, k);
+#pragma unroll
+      for (int i = 0; i < H; ++i)
+#pragma unroll
+        for (int j = 0; j < W; ++j) acc[i][j] = mac_exact(acc[i][j], fa[i], fb[j]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: alpha*acc (+ beta*C), clipped to the extent.
+  float* gd = p.d + (long long)z * p.d_batch;
+  const float* gc = p.c ? p.c + (long long)z * p.d_batch : nullptr;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const int m = m0 + own_index<H, AL>(tm, wg_r, i);
+    if (m >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const int n = n0 + own_index<W, BL>(tn, wg_c, j);
+      if (n >= p.N) continue;
+      const long long off = (long long)m * p.d_sm + (long long)n * p.d_sn;
+      float v = __fmul_rn(p.alpha, acc[i][j]);
+      if (p.read_c) v = __fadd_rn(v, __fmul_rn(p.beta, gc[off]));
+      gd[off] = v;
+    }
+  }
+}
+
+// "noloc": same slab walk and accumulation order, operands read straight
+// from global memory (the reference's direct path, gemm.hpp:408-430).
+template <int H, int W, bool CONV>
+__global__ void exact_gemm_noloc_kernel(ExactArgs p, int wg_r, int wg_c) {
+  const int tid = threadIdx.x;
+  const int BM = H * wg_r, BN = W * wg_c;
+  const int tm = p.tx_on_m ? tid % wg_r : tid / wg_c;
+  const int tn = p.tx_on_m ? tid / wg_r : tid % wg_c;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int z = blockIdx.z;
+  const float* ga = p.a + (CONV ? 0 : (long long)z * p.a_batch);
+  const float* gb = p.b + (long long)z * p.b_batch;
+
+  int rows[H], cols[W];
+#pragma unroll
+  for (int i = 0; i < H; ++i) rows[i] = m0 + i * wg_r + tm;
+#pragma unroll
+  for (int j = 0; j < W; ++j) cols[j] = n0 + j * wg_c + tn;
+
+  // Conv row decomposition, once.
+  int pn[H], pih[H], piw[H];
+  if constexpr (CONV) {
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const int m = min(rows[i], p.M - 1);
+      const int ow = m % p.OW, t = m / p.OW;
+      pn[i] = t / p.OH;
+      pih[i] = (t % p.OH) * p.stride - p.pad_t;
+      piw[i] = ow * p.stride - p.pad_l;
+    }
+  }
+
+  float acc[H][W];
+#pragma unroll
+  for (int i = 0; i < H; ++i)
+#pragma unroll
+    for (int j = 0; j < W; ++j) acc[i][j] = 0.0f;
+
+  int c = 0, y = 0, x = 0;  // conv tap walk
+  for (int k = 0; k < p.K; ++k) {
+    float fa[H], fb[W];
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      float v = 0.0f;
+      if (rows[i] < p.M) {
+        if constexpr (CONV) {
+          const int ih = pih[i] + x, iw = piw[i] + y;
+          if (ih >= 0 && iw >= 0 && ih < p.H && iw < p.W)
+            v = __ldg(p.a + (((long long)pn[i] * p.H + ih) * p.W + iw) * p.C + c);
+        } else {
+          v = __ldg(ga + (long long)rows[i] * p.a_sm + (long long)k * p.a_sk);
+        }
+      }
+      fa[i] = v;
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+      fb[j] = cols[j] < p.N ? __ldg(gb + (long long)k * p.b_sk + (long long)cols[j] * p.b_sn) : 0.0f;
+#pragma unroll
+    for (int i = 0; i < H; ++i)
+#pragma unroll
+      for (int j = 0; j < W; ++j) acc[i][j] = mac_exact(acc[i][j], fa[i], fb[j]);
+    if constexpr (CONV) {
+      if (++c == p.C) {
+        c = 0;
+        if (++y == p.S) {
+          y = 0;
+          ++x;
+        }
+      }
+    }
+  }
+
+  float* gd = p.d + (long long)z * p.d_batch;
+  const float* gc = p.c ? p.c + (long long)z * p.d_batch : nullptr;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    if (rows[i] >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      if (cols[j] >= p.N) continue;
+      const long long off = (long long)rows[i] * p.d_sm + (long long)cols[j] * p.d_sn;
+      float v = __fmul_rn(p.alpha, acc[i][j]);
+      if (p.read_c) v = __fadd_rn(v, __fmul_rn(p.beta, gc[off]));
+      gd[off] = v;
+    }
+  }
+}
+
+// Host launcher (exact_gemm.cu).  h/w in {1,2,4,8}; r*c <= 1024.
+struct ExactLaunch {
+  int h, w, r, c;
+  bool loc;
+  int stages;  // 1 (loc), 2..3 (loc_db)
+};
+void launch_exact(const ExactArgs& p, const ExactLaunch& L, bool conv, int batch,
+                  cudaStream_t stream);
+
+}  // namespace tkb

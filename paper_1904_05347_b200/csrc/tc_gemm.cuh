@@ -1,0 +1,45 @@
+// tc_gemm.cuh -- tensor-core (tcgen05 / TMEM / TMA) GEMM and implicit-GEMM
+// convolution launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "layout.cuh"
+
+namespace tkb {
+
+// Row-major batched GEMM on tensor cores:
+//   D(m, n) = alpha * sum_k A[m][k] * B[n][k] (+ beta * C(m, n))
+// A is [M][K], B is [N][K] (both K contiguous, K % 4 == 0), D(m, n) lives at
+// d[z*d_batch + m*d_sm + n*d_sn] (C likewise).  d_sm == 1 gives coalesced
+// stores.
+struct TcGemm {
+  int M = 0, N = 0, K = 0, batch = 1;
+  const float* a = nullptr;
+  long long a_batch = 0;
+  const float* b = nullptr;
+  long long b_batch = 0;
+  float* d = nullptr;
+  const float* c = nullptr;
+  long long d_sm = 1, d_sn = 0, d_batch = 0;
+  float alpha = 1.0f, beta = 0.0f;
+  int precision = 1;
+  int tile_n = 0;  // 0 = auto
+};
+
+void launch_tc_gemm(const TcGemm& g, cudaStream_t st);
+
+// Column-major C = alpha*OPa(A)*OPb(B) + beta*C (the reference GemmShape
+// convention) on tensor cores; transposes operands into K-major scratch
+// where needed.
+void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float beta, bool ta,
+                             bool tb, const float* a, const float* b, const float* c, float* d,
+                             int precision, int tile_n, cudaStream_t st);
+
+// Implicit-GEMM convolution on tensor cores (NHWC in, HWCK filter, NHWC
+// out).  Workspace: packed filter (+ patch matrix on the fallback path).
+size_t tc_conv_workspace(const ConvGeom& g, int precision);
+void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float* out,
+                    int precision, void* ws, cudaStream_t st);
+
+}  // namespace tkb

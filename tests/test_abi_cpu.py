@@ -1,0 +1,100 @@
+"""CPU: the C-ABI library loads, exports exactly what include/tk_b200.h
+declares, enforces the reference's budgets/grammars host-side, and refuses
+to compute without a B200 (there is no CPU fallback)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "tk_b200.h")).read()
+    return sorted(set(re.findall(r"TK_API\s+[\w\s\*]+?\b(tk_\w+)\s*\(", text)))
+
+
+def test_header_and_exports_agree(tk):
+    declared = header_symbols()
+    assert declared == sorted(tk.EXPORTS)
+    lib = tk.lib()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.tk_abi_version() == 1
+
+
+def test_no_cpu_fallback(tk):
+    if tk.device_count() > 0:
+        pytest.skip("a GPU is present")
+    shape = tk.ConvShape(1, 5, 5, 4, 4, 3, 3)
+    x = np.zeros(shape.in_shape, np.float32)
+    w = np.zeros(shape.filt_shape, np.float32)
+    with pytest.raises(tk.DeviceError, match="no CPU"):
+        tk.conv2d(x, w, shape, tk.parse_conv_params("naive"))
+    g = tk.GemmShape(4, 4, 4)
+    with pytest.raises(tk.DeviceError):
+        tk.gemm_tiled(np.zeros(16), np.zeros(16), None, g, tk.parse_gemm_config("4x4_8x8_loc"),
+                      tk.b200_device())
+
+
+def test_validate_config_matches_reference_verdicts(tk):
+    gpu = tk.find_device("Intel Core i7-6700K GPU")
+    ok, msg = tk.validate_config(tk.parse_gemm_config("4x4_8x8_loc"), gpu)
+    assert ok and msg == "valid"
+    # test_gemm.cpp:188-195: three simultaneous violations
+    tiny = tk.DeviceSpec("tiny", 64, 1024, 1, 20, 16)
+    ok, msg = tk.validate_config(tk.parse_gemm_config("8x4_16x16_loc"), tiny)
+    assert not ok and len(msg.split("; ")) == 3
+    ok, msg = tk.validate_config(tk.parse_gemm_config("4x4_8x8_loc"), tk.find_device("mali"))
+    assert not ok and "local-memory budget" in msg
+
+
+def test_gemm_tiled_rejects_before_touching_the_gpu(tk):
+    g = tk.GemmShape(8, 8, 8)
+    z = np.zeros(64, np.float32)
+    with pytest.raises(tk.ConfigError, match="local-memory budget"):
+        tk.gemm_tiled(z, z, z, g, tk.parse_gemm_config("4x4_8x8_loc"), tk.find_device("mali"))
+    cfg = tk.parse_gemm_config("4x4_8x8_noloc")
+    cfg.k_step = 0
+    with pytest.raises(tk.ConfigError, match="k_step"):
+        tk.gemm_tiled(z, z, z, g, cfg, tk.find_device("mali"))
+
+
+def test_conv_capability_errors(tk):
+    x = np.zeros((1, 8, 8, 4), np.float32)
+    w = np.zeros((3, 3, 4, 2), np.float32)
+    s3 = tk.ConvShape(1, 8, 8, 4, 2, 3, 3, 3, True)
+    with pytest.raises(tk.CapabilityError, match="stride 3"):
+        tk.conv2d(x, w, s3, tk.parse_conv_params("tiled_t2x2_v4x4"))
+    s2 = tk.ConvShape(1, 8, 8, 4, 2, 3, 3, 2, True)
+    with pytest.raises(tk.CapabilityError, match="stride 2"):
+        tk.conv2d(x, w, s2, tk.parse_conv_params("winograd_t2x2"))
+    s1 = tk.ConvShape(1, 8, 8, 4, 2, 3, 3, 1, True)
+    with pytest.raises(tk.CapabilityError, match="3x3 output tile"):
+        tk.conv2d(x, w, s1, tk.parse_conv_params("winograd_t3x3"))
+    bad = tk.ConvShape(1, 2, 2, 4, 2, 3, 3, 1, False)
+    with pytest.raises(tk.ShapeError, match="does not fit"):
+        tk.conv2d(np.zeros((1, 2, 2, 4), np.float32), w, bad, tk.parse_conv_params("naive"))
+
+
+def test_grammars(tk):
+    for name in ["4x4_8x8_loc", "8x4_8x16_loc_db", "8x2_4x16_noloc"]:
+        assert tk.parse_gemm_config(name).name() == name
+    for bad in ["4x4_8x8", "4x4_8x8_noloc_db", "0x4_8x8_loc", "4X4_8x8_loc"]:
+        with pytest.raises(tk.ParseError):
+            tk.parse_gemm_config(bad)
+    for name in ["naive", "im2col", "tiled_t4x5_v4x2", "winograd_t2x2"]:
+        assert tk.parse_conv_params(name).name() == name
+    with pytest.raises(tk.ParseError):
+        tk.parse_conv_params("tiled_t4x5_v3x2")
+
+
+def test_b200_device_spec(tk):
+    d = tk.b200_device()
+    assert d.cache_line_bytes == 128 and d.register_budget == 255
+    assert d.local_memory_bytes >= 227 * 1024 and d.max_workgroup_size == 1024
+    assert d.compute_units in (148, 132, 160) or d.compute_units > 0
+    ok, _ = tk.validate_config(tk.parse_gemm_config("8x8_16x16_loc_db"), d)
+    assert ok

@@ -1,0 +1,103 @@
+"""GPU parity of the tensor-core (tcgen05 TF32) paths.
+
+Tolerance (stated here): TF32 operands are truncated to a
+10-bit mantissa, so results are judged with the reference's scale-normalised
+metric max_scaled_error (numeric.hpp:39-56) at <= 1e-3 for GEMM / implicit
+GEMM / Winograd F(2x2) and <= 1e-2 for Winograd F(4x4).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_TF32 = 1e-3
+TOL_TF32_F4 = 1e-2
+
+
+def dev_conv(tk, x, f, shape, algo, precision="tf32"):
+    import torch
+    dx, df = torch.from_numpy(x).cuda(), torch.from_numpy(f).cuda()
+    dy = torch.full(shape.out_shape, float("nan"), device="cuda")
+    tk.conv2d_dev(dx, df, dy, shape, tk.parse_conv_params(algo), precision=precision)
+    torch.cuda.synchronize()
+    return dy.cpu().numpy()
+
+
+@pytest.mark.parametrize("m,n,k,ta,tb", [(128, 128, 32, 1, 0), (256, 512, 128, 1, 0),
+                                         (1024, 1024, 1024, 0, 0), (33, 29, 21, 0, 1),
+                                         (300, 200, 100, 1, 1), (1000, 70, 64, 0, 0)])
+def test_tc_gemm_colmajor(tk, oracle, m, n, k, ta, tb):
+    import torch
+    a = oracle.fill_random(m * k, 1)
+    b = oracle.fill_random(k * n, 2)
+    c = oracle.fill_random(m * n, 3)
+    want = oracle.gemm_naive(m, n, k, 1.5, -0.5, ta, tb, a, b, c)
+    da, db, dc = (torch.from_numpy(v).cuda() for v in (a, b, c))
+    out = torch.full((m * n,), float("nan"), device="cuda")
+    shape = tk.GemmShape(m, n, k, 1.5, -0.5, "t" if ta else "n", "t" if tb else "n")
+    tk.gemm_dev(da, db, dc, out, shape, precision="tf32")
+    torch.cuda.synchronize()
+    err = oracle.max_scaled_error(out.cpu().numpy(), want)
+    assert err <= TOL_TF32, err
+
+
+@pytest.mark.parametrize("shape", [
+    (2, 14, 14, 32, 128), (1, 28, 28, 64, 64), (2, 56, 56, 64, 128), (1, 28, 28, 256, 512),
+    (3, 17, 23, 32, 96), (1, 112, 112, 64, 128), (2, 7, 7, 512, 512), (1, 9, 9, 3, 16),
+])
+def test_tc_conv_im2col(tk, oracle, shape):
+    N, H, W, C, K = shape
+    s = tk.ConvShape(N, H, W, C, K, 3, 3, 1, True)
+    conv = oracle.Conv(N, H, W, C, K, 3, 3, 1, True)
+    x = oracle.fill_random(int(np.prod(conv.in_shape)), 5).reshape(conv.in_shape)
+    f = oracle.fill_random(int(np.prod(conv.filt_shape)), 6).reshape(conv.filt_shape)
+    want = oracle.conv2d_naive(conv, x, f)
+    got = dev_conv(tk, x, f, s, "im2col")
+    assert not np.isnan(got).any()
+    err = oracle.max_scaled_error(got, want)
+    assert err <= TOL_TF32, err
+
+
+@pytest.mark.parametrize("window,stride,same", [(1, 1, True), (1, 2, True), (7, 2, True),
+                                                (3, 2, False), (3, 1, False)])
+def test_tc_conv_general_windows(tk, oracle, window, stride, same):
+    s = tk.ConvShape(2, 20, 18, 32, 64, window, window, stride, same)
+    conv = oracle.Conv(2, 20, 18, 32, 64, window, window, stride, same)
+    x = oracle.fill_random(int(np.prod(conv.in_shape)), 5).reshape(conv.in_shape)
+    f = oracle.fill_random(int(np.prod(conv.filt_shape)), 6).reshape(conv.filt_shape)
+    want = oracle.conv2d_naive(conv, x, f)
+    got = dev_conv(tk, x, f, s, "im2col")
+    assert oracle.max_scaled_error(got, want) <= TOL_TF32
+
+
+@pytest.mark.parametrize("m", [2, 4])
+def test_tc_winograd(tk, oracle, m):
+    s = tk.ConvShape(2, 28, 28, 64, 64, 3, 3, 1, True)
+    conv = oracle.Conv(2, 28, 28, 64, 64, 3, 3, 1, True)
+    x = oracle.fill_random(int(np.prod(conv.in_shape)), 5).reshape(conv.in_shape)
+    f = oracle.fill_random(int(np.prod(conv.filt_shape)), 6).reshape(conv.filt_shape)
+    want = oracle.conv2d_naive(conv, x, f)
+    got = dev_conv(tk, x, f, s, f"winograd_t{m}x{m}")
+    err = oracle.max_scaled_error(got, want)
+    assert err <= (TOL_TF32 if m == 2 else TOL_TF32_F4), err
+
+
+def test_tc_vgg_batch32_full_size_property(tk, oracle):
+    """BASELINE config 2 at full size (vgg_conv3_2, batch 32): the oracle
+    cannot run the whole batch in seconds, so check images 0 and 31 against
+    single-image oracle runs (batch independence, test_conv.cpp:268-293)."""
+    import torch
+    N, H, C, K = 32, 56, 256, 256
+    s = tk.ConvShape(N, H, H, C, K, 3, 3, 1, True)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    dx = torch.rand((N, H, H, C), device="cuda", generator=gen) * 2 - 1
+    df = torch.rand((3, 3, C, K), device="cuda", generator=gen) * 2 - 1
+    dy = torch.empty((N, H, H, K), device="cuda")
+    tk.conv2d_dev(dx, df, dy, s, tk.parse_conv_params("im2col"), precision="tf32")
+    torch.cuda.synchronize()
+    f = df.cpu().numpy()
+    for img in (0, N - 1):
+        conv = oracle.Conv(1, H, H, C, K, 3, 3, 1, True)
+        want = oracle.conv2d_naive(conv, dx[img:img + 1].cpu().numpy(), f)
+        err = oracle.max_scaled_error(dy[img:img + 1].cpu().numpy(), want)
+        assert err <= TOL_TF32, (img, err)
