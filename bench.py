@@ -58,10 +58,10 @@ def conv_flops(n, h, c, k):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16", "fp32"])
     ap.add_argument("--batch", type=int, default=32, help="images per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -84,9 +84,13 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0:  # sampler is live
+                time.sleep(0.01)
+            self.lines.clear()
         except FileNotFoundError:
             self.proc = None
         return self
@@ -324,7 +328,10 @@ def main():
     # is the whole step except the tiny filter-pack launches.
     lay_ms = float(sum(per_layer))
     achieved_tf = step_flops / (lay_ms * 1e-3) / 1e12
-    if prec == "tf32":
+    if prec == "bf16":
+        peak_tf = peaks["bf16_tflops"]
+        peak_note = f"{peaks_kind} bf16 burst {peaks['bf16_tflops']} TF/s"
+    elif prec == "tf32":
         peak_tf = peaks["bf16_tflops"] / 2.0
         peak_note = f"TF32 = 1/2 of {peaks_kind} bf16 burst {peaks['bf16_tflops']} TF/s"
     else:
@@ -332,7 +339,7 @@ def main():
         peak_note = "FP32 exact FMUL+FADD cap = 1/2 of 74.4 TF/s FFMA"
     roofline = {"bound": "tensor", "achieved": round(achieved_tf, 2), "peak": round(peak_tf, 1),
                 "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4), "traffic": None,
-                "kernel": "tc_gemm_kernel (implicit-GEMM conv)" if prec == "tf32" else "exact_gemm_loc_kernel",
+                "kernel": "exact_gemm_loc_kernel" if prec == "fp32" else "tc_gemm_kernel (implicit-GEMM conv)",
                 "peak_source": peak_note}
 
     layer_rows = []
@@ -353,7 +360,7 @@ def main():
             "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "tf32" if prec == "tf32" else "f32",
+            "dtype": {"tf32": "tf32", "bf16": "bf16", "fp32": "f32"}[prec],
             "data": "synthetic (uniform[-1,1) via torch, per-layer independent inputs)",
             "config": {"workload": "VGG16 13 conv layers (3x3/s1/Same, NHWC fp32)",
                        "batch_per_gpu": N, "global_batch": N * world,

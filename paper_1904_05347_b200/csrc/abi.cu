@@ -417,7 +417,9 @@ void winograd_dev(const ConvGeom& g, int m, int precision, const float* in, cons
     t.d_sm = 1;
     t.d_sn = w.K;
     t.d_batch = (long long)w.tiles * w.K;
-    t.precision = precision;
+    // The transform-domain operands are fp32 scratch: the batched GEMM runs
+    // kind::tf32 for every tensor-core precision request.
+    t.precision = TK_PREC_TF32;
     launch_tc_gemm(t, st);
   }
   wino_output_transform(w, prod, out, st);

@@ -1,26 +1,37 @@
 // tc_gemm.cu -- tcgen05 tensor-core GEMM and implicit-GEMM convolution.
 //
-// One persistent, warp-specialised kernel (192 threads, one CTA per SM):
-//   warp 0      TMA producer: fills a STAGES-deep ring of 128-byte-swizzled
-//               K-slabs (A: 128 rows, B: BN rows; 128 B = 32 fp32 of K each)
-//   warp 1      MMA issuer: one elected thread issues 4 x tcgen05.mma
-//               (kind::tf32, M=128, N=BN, K=8) per slab into a TMEM
-//               accumulator; tcgen05.commit frees the slab / publishes the
-//               accumulator
-//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> global, while the
-//               MMA warp already accumulates the next tile into the second
-//               TMEM buffer (2 x 256 columns)
+// One persistent, warp-specialised kernel family (192 threads per CTA, one
+// CTA per SM), templated on
+//   MODE  operand sources (plain GEMM / conv with pixels on N / on M)
+//   CG    CTA group: 1 = one SM, UMMA M = 128; 2 = an SM pair (cluster of 2)
+//         issuing tcgen05.mma.cta_group::2 with UMMA M = 256 -- each SM
+//         stages half of A (128 rows) and half of B (BN/2 rows), which halves
+//         the per-SM shared-memory operand traffic per MAC
+//   TF32  kind::tf32 on fp32 operands (32 elements per 128-byte K-slab) or
+//         kind::f16 on bf16 operands (64 elements per slab)
+// Roles:
+//   warp 0      TMA producer (both CTAs): STAGES-deep ring of 128-byte-
+//               swizzled K-slabs; completion is signalled on the leader CTA's
+//               `full` barrier (cp.async.bulk.tensor.cta_group::2)
+//   warp 1      MMA issuer (leader CTA only): 4 x tcgen05.mma per slab into a
+//               TMEM accumulator; tcgen05.commit (multicast to the pair)
+//               frees the slab in both CTAs / publishes the accumulator
+//   warps 2..5  epilogue (both CTAs): tcgen05.ld 32x32b -> registers ->
+//               global; two TMEM accumulators (2 x 256 columns) let the MMA
+//               run the next tile while the epilogue drains this one
 // Operand sources:
 //   plain GEMM : A [M][K], B [N][K] via 3-D TMA (K, rows, batch)
-//   conv       : the filter, repacked once per call to [Kout][R*S*C], via 2-D
-//                TMA; the activations via a 4-D TMA box {32 ch, Wb, Hb, 1}
-//                of the NHWC input per (tap, channel chunk), shifted by the
-//                tap offset.  Out-of-range rows/cols of the box are zero-
-//                filled by the TMA unit, which is exactly Same padding.
-// K order of the conv slabs is (x, y, c) like the reference's im2col
+//   conv       : the filter repacked to [Kout][R*S*C] via 2-D TMA; the
+//                activations via a 4-D TMA box {slab, Wb, Hb, 1} of the NHWC
+//                input per (tap, channel chunk) shifted by the tap offset.
+//                Rows/cols of the box outside the input are zero-filled by
+//                the TMA unit, which is exactly Same padding.
+// K order of the conv slabs is (x, y, c), the reference's im2col column order
 // (conv.hpp:286-292).
 #include <cuda.h>
+#include <cuda_bf16.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -32,7 +43,7 @@ namespace tkb {
 
 namespace {
 
-constexpr int kBM = 128;
+constexpr int kRows = 128;       // A rows staged per CTA (UMMA M per SM)
 constexpr int kSlabBytes = 128;  // bytes of K per operand row per stage
 constexpr int kThreads = 192;
 constexpr int kAccCols = 256;
@@ -42,15 +53,18 @@ enum TcMode : int { kPlain = 0, kConvPixN = 1, kConvPixM = 2 };
 
 struct TcArgs {
   int M, N, K;
-  int BN;
+  int BN;                      // UMMA N (columns of the tile)
   int num_m, num_n, batch, num_kb, stages;
+  int ek;                      // K elements per slab (32 tf32 / 64 bf16)
   float* d;
   const float* c;
   long long d_sm, d_sn, d_batch;
   float alpha, beta;
   int read_c;
+  int store_tma;               // epilogue via swizzled smem tile + TMA store
+  int epi_bufs;                // staging buffers for the TMA-store epilogue
   // conv geometry
-  int OH, OW, Kout, Wb, Hb, tiles_w, tiles_h, pad_t, pad_l, cchunks, S;
+  int OH, OW, Kout, Wb, tileH, boxH, tiles_w, tiles_h, pad_t, pad_l, cchunks, S;
 };
 
 struct PixTile {
@@ -62,20 +76,72 @@ __device__ __forceinline__ PixTile pix_tile(const TcArgs& p, int t) {
   const int per_img = p.tiles_w * p.tiles_h;
   r.img = t / per_img;
   const int rem = t - r.img * per_img;
-  r.oh0 = (rem / p.tiles_w) * p.Hb;
+  r.oh0 = (rem / p.tiles_w) * p.tileH;
   r.ow0 = (rem % p.tiles_w) * p.Wb;
   return r;
 }
 
-template <int MODE>
+// Epilogue through shared memory + TMA store: each of the 128 epilogue
+// threads owns one accumulator row (TMEM lane); it writes the row into a
+// 128-byte-swizzled [128 rows][32 fp32] staging tile per 32-column chunk
+// (conflict-free: 16-byte chunk c of row r lands at c ^ (r % 8)), then one
+// thread issues the bulk tensor store(s).  Rows/columns outside the output
+// tensor are clipped by the TMA unit.  Two staging buffers alternate, so the
+// store of tile i overlaps the TMEM drain of tile i+1.
+template <int CG>
+__device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t taddr, uint8_t* stage,
+                                                   int local, uint32_t warp, uint32_t lane, int row,
+                                                   uint32_t empty_cluster_addr, uint64_t* empty_local,
+                                                   const CUtensorMap* map_d, int c0, int c1, int c2,
+                                                   int c3, int rank_dims) {
+  const int nchunks = (p.BN + 31) / 32;
+  const int buf_bytes = nchunks * kRows * kSlabBytes;
+  uint8_t* sbuf = stage + (p.epi_bufs > 1 ? (local & 1) : 0) * buf_bytes;
+  const bool issuer = warp == 2 && lane == 0;
+  if (issuer) {
+    if (p.epi_bufs > 1) ptx::bulk_wait_read<1>();
+    else ptx::bulk_wait_read<0>();
+  }
+  ptx::named_sync(1, 128);
+  for (int j = 0; j < nchunks; ++j) {
+    float v[32];
+    ptx::tmem_ld32(taddr + j * 32, v);
+    uint8_t* rowp = sbuf + j * kRows * kSlabBytes + row * kSlabBytes;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      *reinterpret_cast<float4*>(rowp + ((c ^ (row & 7)) << 4)) =
+          make_float4(p.alpha * v[4 * c], p.alpha * v[4 * c + 1], p.alpha * v[4 * c + 2],
+                      p.alpha * v[4 * c + 3]);
+    }
+  }
+  // Accumulator fully read: hand TMEM back to the MMA warp.
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::mbar_arrive_cluster(empty_cluster_addr);
+  else ptx::mbar_arrive(empty_local);
+  ptx::fence_proxy_async();
+  ptx::named_sync(1, 128);
+  if (issuer) {
+    for (int j = 0; j < nchunks; ++j) {
+      const uint8_t* src = sbuf + j * kRows * kSlabBytes;
+      if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + 32 * j, c1, c2, c3);
+      else ptx::tma_store_3d(map_d, src, c0 + 32 * j, c1, c2);
+    }
+    ptx::bulk_commit();
+  }
+}
+
+template <int MODE, int CG, bool TF32>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b, TcArgs p) {
+                   const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_d, TcArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  const int a_bytes = kBM * kSlabBytes;
-  const int b_bytes = p.BN * kSlabBytes;
+  constexpr int BM = kRows * CG;
+  const int a_bytes = kRows * kSlabBytes;
+  const int b_rows = p.BN / CG;
+  const int b_bytes = b_rows * kSlabBytes;
   const int stage_bytes = a_bytes + b_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + p.stages * stage_bytes);
   uint64_t* full = bars;
@@ -83,11 +149,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tmem_full = bars + 2 * kMaxStages;
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  // TMA-store staging: epi_bufs x (BN/32) swizzled 128-row x 128-byte tiles
+  uint8_t* epi_stage = base + p.stages * stage_bytes + 1024;
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const uint32_t rank = CG == 2 ? ptx::cluster_rank() : 0;
+  const bool leader = rank == 0;
+
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&map_a);
     ptx::prefetch_tmap(&map_b);
+    if (p.store_tma) ptx::prefetch_tmap(&map_d);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -96,24 +168,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tmem_full[a], 1);
-      ptx::mbar_init(&tmem_empty[a], 128);
+      ptx::mbar_init(&tmem_empty[a], 128 * CG);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc<2 * kAccCols>(tmem_slot);
+  if (warp == 2) ptx::tmem_alloc_cg<CG, 2 * kAccCols>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int total = p.num_m * p.num_n * p.batch;
+  const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA producer (every CTA) ----------------
     if (ptx::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = unit; t < total; t += nunits) {
         const int m_blk = t % p.num_m;
         const int rest = t / p.num_m;
         const int n_blk = rest % p.num_n;
@@ -125,24 +199,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = base + stage * stage_bytes;
           uint8_t* sb = sa + a_bytes;
-          ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
-          const int k0 = kb * 32;
+          uint32_t fb = ptx::smem(&full[stage]);
+          if constexpr (CG == 2) fb = ptx::map_to_rank(fb, 0);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], CG * stage_bytes);
+          const int k0 = kb * p.ek;
           int c0 = 0, dy = 0, dx = 0;
           if constexpr (MODE != kPlain) {
             const int tap = kb / p.cchunks;
-            c0 = (kb - tap * p.cchunks) * 32;
+            c0 = (kb - tap * p.cchunks) * p.ek;
             dy = tap % p.S - p.pad_l;
             dx = tap / p.S - p.pad_t;
           }
           if constexpr (MODE == kPlain) {
-            ptx::tma_load_3d(sa, &map_a, &full[stage], k0, m_blk * kBM, z);
-            ptx::tma_load_3d(sb, &map_b, &full[stage], k0, n_blk * p.BN, z);
+            ptx::tma3<CG>(sa, &map_a, fb, k0, m_blk * BM + rank * kRows, z);
+            ptx::tma3<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows, z);
           } else if constexpr (MODE == kConvPixN) {
-            ptx::tma_load_2d(sa, &map_a, &full[stage], k0, m_blk * kBM);
-            ptx::tma_load_4d(sb, &map_b, &full[stage], c0, pt.ow0 + dy, pt.oh0 + dx, pt.img);
+            ptx::tma2<CG>(sa, &map_a, fb, k0, m_blk * BM + rank * kRows);
+            ptx::tma4<CG>(sb, &map_b, fb, c0, pt.ow0 + dy, pt.oh0 + rank * p.boxH + dx, pt.img);
           } else {
-            ptx::tma_load_4d(sa, &map_a, &full[stage], c0, pt.ow0 + dy, pt.oh0 + dx, pt.img);
-            ptx::tma_load_2d(sb, &map_b, &full[stage], k0, n_blk * p.BN);
+            ptx::tma4<CG>(sa, &map_a, fb, c0, pt.ow0 + dy, pt.oh0 + rank * p.boxH + dx, pt.img);
+            ptx::tma2<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows);
           }
           if (++stage == p.stages) {
             stage = 0;
@@ -152,44 +228,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    const uint32_t idesc = ptx::idesc(kBM, p.BN, true);
-    int stage = 0;
-    uint32_t phase = 0;
-    int local = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
-      ptx::tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * kAccCols;
-      for (int kb = 0; kb < p.num_kb; ++kb) {
-        ptx::mbar_wait(&full[stage], phase);
+    // ---------------- MMA issuer (leader CTA) ----------------
+    if (leader) {
+      const uint32_t idesc = ptx::idesc(BM, p.BN, TF32);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = unit; t < total; t += nunits, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          const uint32_t sa = ptx::smem(base + stage * stage_bytes);
-          const uint32_t sb = sa + a_bytes;
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            const uint32_t sa = ptx::smem(base + stage * stage_bytes);
+            const uint32_t sb = sa + a_bytes;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            ptx::mma<true>(d_tmem, ptx::desc_sw128(sa + kk * 32), ptx::desc_sw128(sb + kk * 32),
-                           idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < 4; ++kk) {
+              ptx::mma_cg<CG, TF32>(d_tmem, ptx::desc_sw128(sa + kk * 32),
+                                    ptx::desc_sw128(sb + kk * 32), idesc, (kb | kk) != 0);
+            }
+            ptx::commit_cg<CG>(&empty[stage]);
+            if (kb == p.num_kb - 1) ptx::commit_cg<CG>(&tmem_full[acc]);
           }
-          ptx::mma_commit(&empty[stage]);
-          if (kb == p.num_kb - 1) ptx::mma_commit(&tmem_full[acc]);
-        }
-        __syncwarp();
-        if (++stage == p.stages) {
-          stage = 0;
-          phase ^= 1;
+          __syncwarp();
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5) ----------------
+    // ---------------- epilogue (warps 2..5, every CTA) ----------------
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
+    uint32_t empty_addr[2] = {ptx::smem(&tmem_empty[0]), ptx::smem(&tmem_empty[1])};
+    if constexpr (CG == 2) {
+      empty_addr[0] = ptx::map_to_rank(empty_addr[0], 0);
+      empty_addr[1] = ptx::map_to_rank(empty_addr[1], 0);
+    }
     int local = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+    for (int t = unit; t < total; t += nunits, ++local) {
       const int m_blk = t % p.num_m;
       const int rest = t / p.num_m;
       const int n_blk = rest % p.num_n;
@@ -201,16 +284,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
 
       if constexpr (MODE == kPlain) {
-        const int m = m_blk * kBM + row;
+        const int m = m_blk * BM + rank * kRows + row;
         float* dz = p.d + (long long)z * p.d_batch;
         const float* cz = p.read_c ? p.c + (long long)z * p.d_batch : nullptr;
+        if (p.store_tma) {
+          tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, empty_addr[acc],
+                                 &tmem_empty[acc], &map_d, n_blk * p.BN,
+                                 m_blk * BM + rank * kRows, z, 0, 3);
+          continue;
+        }
         for (int col = 0; col < p.BN; col += 32) {
           float v[32];
           ptx::tmem_ld32(taddr + col, v);
+          const int n0 = n_blk * p.BN + col;
           if (m < p.M) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const int n = n_blk * p.BN + col + j;
+              const int n = n0 + j;
               if (col + j < p.BN && n < p.N) {
                 const long long off = (long long)m * p.d_sm + (long long)n * p.d_sn;
                 float r = p.alpha * v[j];
@@ -222,53 +312,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else if constexpr (MODE == kConvPixN) {
         const PixTile pt = pix_tile(p, n_blk);
-        const int m = m_blk * kBM + row;  // output feature
+        const int m = m_blk * BM + rank * kRows + row;  // output feature
         const long long img_base = (long long)pt.img * p.OH;
         for (int col = 0; col < p.BN; col += 32) {
           float v[32];
           ptx::tmem_ld32(taddr + col, v);
+          if (m < p.Kout) {
+            // Column -> pixel walk without per-column division.
+            int h = col / p.Wb, w = col - (col / p.Wb) * p.Wb;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int n = col + j;
-            const int oh = pt.oh0 + n / p.Wb, ow = pt.ow0 + n % p.Wb;
-            if (n < p.BN && oh < p.OH && ow < p.OW && m < p.Kout)
-              p.d[((img_base + oh) * p.OW + ow) * p.Kout + m] = v[j];
-          }
-        }
-      } else {
-        const PixTile pt = pix_tile(p, m_blk);
-        const int oh = pt.oh0 + row / p.Wb, ow = pt.ow0 + row % p.Wb;
-        const bool valid = oh < p.OH && ow < p.OW;
-        float* dst = p.d + (((long long)pt.img * p.OH + oh) * p.OW + ow) * p.Kout;
-        for (int col = 0; col < p.BN; col += 32) {
-          float v[32];
-          ptx::tmem_ld32(taddr + col, v);
-          if (valid) {
-            const int f0 = n_blk * p.BN + col;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const int f = f0 + j;
-              if (col + j + 3 < p.BN && f + 3 < p.Kout) {
-                *reinterpret_cast<float4*>(dst + f) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-              } else {
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                  if (col + j + u < p.BN && f + u < p.Kout) dst[f + u] = v[j + u];
+            for (int j = 0; j < 32; ++j) {
+              const int oh = pt.oh0 + h, ow = pt.ow0 + w;
+              if (col + j < p.BN && oh < p.OH && ow < p.OW)
+                p.d[((img_base + oh) * p.OW + ow) * p.Kout + m] = v[j];
+              if (++w == p.Wb) {
+                w = 0;
+                ++h;
               }
             }
           }
         }
+      } else {
+        const PixTile pt = pix_tile(p, m_blk);
+        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, empty_addr[acc],
+                               &tmem_empty[acc], &map_d, n_blk * p.BN, pt.ow0,
+                               pt.oh0 + rank * p.boxH, pt.img, 4);
+        continue;
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&tmem_empty[acc]);
+      if constexpr (CG == 2) ptx::mbar_arrive_cluster(empty_addr[acc]);
+      else ptx::mbar_arrive(&tmem_empty[acc]);
     }
   }
 
+  if (warp == 2 && lane == 0 && p.store_tma) ptx::bulk_wait<0>();
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<2 * kAccCols>(tmem_base);
+    ptx::tmem_dealloc_cg<CG, 2 * kAccCols>(tmem_base);
   }
 }
 
@@ -295,42 +378,45 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-CUtensorMap make_map(const float* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
-                     const cuuint32_t* box) {
+// esize: 4 (fp32 / tf32) or 2 (bf16).  dims[0] is the contiguous K axis.
+CUtensorMap make_map(const void* base, int esize, int rank, const cuuint64_t* dims,
+                     const cuuint64_t* strides, const cuuint32_t* box) {
   CUtensorMap m;
   cuuint32_t elem_strides[5] = {1, 1, 1, 1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank,
-                                 const_cast<float*>(base), dims, strides, box, elem_strides,
-                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  const CUresult r = encode_fn()(
+      &m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+      (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, elem_strides,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   return m;
 }
 
-// [batch][rows][K] K-major operand, box {32, box_rows, 1}.
-CUtensorMap map_rows(const float* base, long long K, long long rows, long long batch,
+// [batch][rows][K] K-major operand, box {slab, box_rows, 1}.
+CUtensorMap map_rows(const void* base, int esize, long long K, long long rows, long long batch,
                      long long batch_stride, int box_rows) {
   cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
-  cuuint64_t strides[2] = {(cuuint64_t)K * 4, (cuuint64_t)(batch_stride ? batch_stride : K * rows) * 4};
-  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
-  return make_map(base, 3, dims, strides, box);
+  cuuint64_t strides[2] = {(cuuint64_t)K * esize,
+                           (cuuint64_t)(batch_stride ? batch_stride : K * rows) * esize};
+  cuuint32_t box[3] = {(cuuint32_t)(kSlabBytes / esize), (cuuint32_t)box_rows, 1};
+  return make_map(base, esize, 3, dims, strides, box);
 }
 
-CUtensorMap map_rows2d(const float* base, long long K, long long rows, int box_rows) {
+CUtensorMap map_rows2d(const void* base, int esize, long long K, long long rows, int box_rows) {
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)K * 4};
-  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
-  return make_map(base, 2, dims, strides, box);
+  cuuint64_t strides[1] = {(cuuint64_t)K * esize};
+  cuuint32_t box[2] = {(cuuint32_t)(kSlabBytes / esize), (cuuint32_t)box_rows};
+  return make_map(base, esize, 2, dims, strides, box);
 }
 
-// NHWC activations, box {32 channels, Wb, Hb, 1}.
-CUtensorMap map_nhwc(const float* base, const ConvGeom& g, int wb, int hb) {
+// NHWC activations, box {slab channels, Wb, Hb, 1}.
+CUtensorMap map_nhwc(const void* base, int esize, const ConvGeom& g, int wb, int hb) {
   cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
-  cuuint64_t strides[3] = {(cuuint64_t)g.C * 4, (cuuint64_t)g.W * g.C * 4,
-                           (cuuint64_t)g.H * g.W * g.C * 4};
-  cuuint32_t box[4] = {32, (cuuint32_t)wb, (cuuint32_t)hb, 1};
-  return make_map(base, 4, dims, strides, box);
+  cuuint64_t strides[3] = {(cuuint64_t)g.C * esize, (cuuint64_t)g.W * g.C * esize,
+                           (cuuint64_t)g.H * g.W * g.C * esize};
+  cuuint32_t box[4] = {(cuuint32_t)(kSlabBytes / esize), (cuuint32_t)wb, (cuuint32_t)hb, 1};
+  return make_map(base, esize, 4, dims, strides, box);
 }
 
 int sm_count() {
@@ -345,40 +431,84 @@ int sm_count() {
   return n;
 }
 
-template <int MODE>
-void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, TcArgs p, int stages_req,
-                cudaStream_t st) {
-  const int stage_bytes = kBM * kSlabBytes + p.BN * kSlabBytes;
-  const int budget = 232448 - 1024 - 256;
+template <int MODE, int CG, bool TF32>
+void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, TcArgs p,
+                int stages_req, cudaStream_t st) {
+  const int stage_bytes = kRows * kSlabBytes + (p.BN / CG) * kSlabBytes;
+  const int epi_bytes =
+      p.store_tma ? p.epi_bufs * ((p.BN + 31) / 32) * kRows * kSlabBytes : 0;
+  const int budget = 232448 - 1024 - 1024 - epi_bytes;
   int stages = budget / stage_bytes;
   if (stages > kMaxStages) stages = kMaxStages;
   if (stages_req > 0 && stages_req < stages) stages = stages_req;
   if (stages < 2) fail(TK_ERR_CAPABILITY, "tc_gemm: tile too large for shared memory");
   p.stages = stages;
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + 256;
-  auto fn = tc_gemm_kernel<MODE>;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + 1024 + epi_bytes;
+  auto fn = tc_gemm_kernel<MODE, CG, TF32>;
   TKB_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   const long long total = (long long)p.num_m * p.num_n * p.batch;
-  const int grid = (int)(total < sm_count() ? total : sm_count());
+  const int units = sm_count() / CG;
+  const int grid = (int)(total < units ? total : units) * CG;
   if (grid <= 0) return;
-  fn<<<grid, kThreads, smem, st>>>(ma, mb, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TKB_CUDA(cudaLaunchKernelEx(&cfg, fn, ma, mb, md, p));
   note_launch();
-  TKB_CUDA(cudaGetLastError());
 }
 
-void require_tf32(int precision) {
-  if (precision != TK_PREC_TF32)
-    fail(TK_ERR_CAPABILITY, "tensor-core path: only TF32 is built in this version");
+template <int MODE>
+void dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
+              const TcArgs& p, int cg, bool tf32, cudaStream_t st) {
+  if (cg == 2) {
+    if (tf32) run_kernel<MODE, 2, true>(ma, mb, md, p, 0, st);
+    else run_kernel<MODE, 2, false>(ma, mb, md, p, 0, st);
+  } else {
+    if (tf32) run_kernel<MODE, 1, true>(ma, mb, md, p, 0, st);
+    else run_kernel<MODE, 1, false>(ma, mb, md, p, 0, st);
+  }
 }
 
-// ---- packing kernels ---------------------------------------------------------
+void require_tc(int precision) {
+  if (precision != TK_PREC_TF32 && precision != TK_PREC_BF16)
+    fail(TK_ERR_CAPABILITY, "tensor-core path: precision must be TF32 or BF16 in this version");
+}
+
+// ---- packing / conversion kernels -------------------------------------------
+
+__device__ __forceinline__ float round_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+template <typename T>
+__device__ __forceinline__ T cvt_out(float v, int tf32_round);
+template <>
+__device__ __forceinline__ float cvt_out<float>(float v, int tf32_round) {
+  return tf32_round ? round_tf32(v) : v;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v, int) {
+  return __float2bfloat16_rn(v);
+}
 
 // dst[r][kk] (row length kp, zero for kk >= k) = src[r*rs + kk*ks].
+template <typename T>
 __global__ void __launch_bounds__(256) pack_kmajor_kernel(const float* __restrict__ src,
                                                           long long rs, long long ks, long long rows,
                                                           long long k, long long kp,
-                                                          float* __restrict__ dst) {
+                                                          T* __restrict__ dst, int tf32_round) {
   __shared__ float tile[32][33];
   const long long r0 = (long long)blockIdx.y * 32, k0 = (long long)blockIdx.x * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -396,63 +526,108 @@ __global__ void __launch_bounds__(256) pack_kmajor_kernel(const float* __restric
   __syncthreads();
   for (int i = ty; i < 32; i += 8) {
     const long long r = r0 + i, kk = k0 + tx;
-    if (r < rows && kk < kp) dst[r * kp + kk] = tile[i][tx];
+    if (r < rows && kk < kp) dst[r * kp + kk] = cvt_out<T>(tile[i][tx], tf32_round);
   }
 }
 
+template <typename T>
 void pack_kmajor(const float* src, long long rs, long long ks, long long rows, long long k,
-                 long long kp, float* dst, cudaStream_t st) {
+                 long long kp, T* dst, bool tf32_round, cudaStream_t st) {
   dim3 grid((unsigned)((kp + 31) / 32), (unsigned)((rows + 31) / 32));
   if (grid.y > 65535) fail(TK_ERR_CAPABILITY, "pack: too many rows");
-  pack_kmajor_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rs, ks, rows, k, kp, dst);
+  pack_kmajor_kernel<T><<<grid, dim3(32, 8), 0, st>>>(src, rs, ks, rows, k, kp, dst, tf32_round);
   note_launch();
   TKB_CUDA(cudaGetLastError());
 }
 
-// Row-major patch matrix [pixel][kp] (K-major, zero padded to kp), the
-// explicit fallback for channel counts TMA cannot box (C % 32 != 0) and
-// strides != 1.
-__global__ void __launch_bounds__(256) patches_rm_kernel(ConvGeom g, const float* __restrict__ in,
-                                                         long long kp, float* __restrict__ out) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long pixels = (long long)g.N * g.OH * g.OW;
-  if (idx >= pixels * kp) return;
-  const long long pix = idx / kp;
-  const int kk = (int)(idx - pix * kp);
-  const int K = g.R * g.S * g.C;
-  float v = 0.0f;
-  if (kk < K) {
-    const int c = kk % g.C, tap = kk / g.C;
-    const int y = tap % g.S, x = tap / g.S;
-    const int ow = (int)(pix % g.OW);
-    const long long t = pix / g.OW;
-    const int oh = (int)(t % g.OH);
-    const long long n = t / g.OH;
-    const int ih = oh * g.stride + x - g.pad_t, iw = ow * g.stride + y - g.pad_l;
-    if (ih >= 0 && iw >= 0 && ih < g.H && iw < g.W) v = __ldg(in + ((n * g.H + ih) * g.W + iw) * g.C + c);
+// fp32 -> bf16, 8 elements per thread (n % 8 == 0 fast path).
+__global__ void __launch_bounds__(256) to_bf16_kernel(const float4* __restrict__ src,
+                                                      __nv_bfloat162* __restrict__ dst,
+                                                      long long n4) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = src[i];
+    dst[2 * i] = __floats2bfloat162_rn(v.x, v.y);
+    dst[2 * i + 1] = __floats2bfloat162_rn(v.z, v.w);
   }
-  out[idx] = v;
 }
 
-// Pixel-tile shape for the conv box: Wb * Hb pixels.
+void to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st) {
+  if (n % 4 != 0) fail(TK_ERR_CAPABILITY, "bf16 conversion needs a multiple of 4 elements");
+  const long long n4 = n / 4;
+  const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)sm_count() * 8);
+  to_bf16_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(src),
+                                         reinterpret_cast<__nv_bfloat162*>(dst), n4);
+  note_launch();
+  TKB_CUDA(cudaGetLastError());
+}
+
+// Row-major patch matrix [pixel][kp] (K-major, zero padded to kp): one
+// thread per 4-element chunk, consecutive threads write consecutive 16-byte
+// chunks.  The explicit fallback for channel counts TMA cannot box and for
+// strides != 1.
+__global__ void __launch_bounds__(256) patches_rm_kernel(ConvGeom g, const float* __restrict__ in,
+                                                         int kp, float* __restrict__ out,
+                                                         long long chunks) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= chunks) return;
+  const int per_pix = kp >> 2;
+  const int pix = (int)(idx / per_pix);
+  const int k0 = (int)(idx - (long long)pix * per_pix) * 4;
+  const int ow = pix % g.OW;
+  const int t = pix / g.OW;
+  const int oh = t % g.OH;
+  const int n = t / g.OH;
+  const int K = g.R * g.S * g.C;
+  float v[4];
+  int c = k0 % g.C, tap = k0 / g.C;
+  int y = tap % g.S, x = tap / g.S;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    float val = 0.0f;
+    if (k0 + u < K) {
+      const int ih = oh * g.stride + x - g.pad_t, iw = ow * g.stride + y - g.pad_l;
+      if (ih >= 0 && iw >= 0 && ih < g.H && iw < g.W)
+        val = __ldg(in + (((long long)n * g.H + ih) * g.W + iw) * g.C + c);
+      if (++c == g.C) {
+        c = 0;
+        if (++y == g.S) {
+          y = 0;
+          ++x;
+        }
+      }
+    }
+    v[u] = val;
+  }
+  reinterpret_cast<float4*>(out)[idx] = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// Pixel-tile shape for the conv box: Wb x tileH pixels per tile, loaded as
+// CG boxes of Wb x boxH.
 struct BoxShape {
-  int wb, hb, tiles_w, tiles_h;
+  int wb, tileH, boxH, tiles_w, tiles_h;
 };
 
-BoxShape pick_box(const ConvGeom& g, bool pix_on_n) {
-  BoxShape best{0, 0, 0, 0};
+// pix_on_n: the tile is the MMA N side (P = BN, multiple of 16*CG, <= 256);
+// otherwise it is the M side (P = 128*CG, each CTA boxes 128 pixels).
+BoxShape pick_box(const ConvGeom& g, bool pix_on_n, int cg) {
+  BoxShape best{0, 0, 0, 0, 0};
   double best_score = 1e30;
   for (int wb = 1; wb <= 256; ++wb) {
-    for (int hb = 1; wb * hb <= 256; ++hb) {
-      const int P = wb * hb;
-      if (pix_on_n ? (P % 16 != 0 || P < 64) : (P != kBM)) continue;
-      if (wb > 2 * g.OW + 16 || hb > 2 * g.OH + 16) continue;
-      const int tw = (g.OW + wb - 1) / wb, th = (g.OH + hb - 1) / hb;
-      const double waste = (double)tw * wb * th * hb / ((double)g.OW * g.OH);
+    for (int th = 1; wb * th <= 256 * cg; ++th) {
+      const int P = wb * th;
+      if (pix_on_n) {
+        if (P > 256 || P % (16 * cg) != 0 || P < 64 || th % cg != 0) continue;
+      } else {
+        if (P != kRows * cg || th % cg != 0) continue;
+      }
+      if (wb > 2 * g.OW + 16 || th > 2 * g.OH + 16) continue;
+      const int tw = (g.OW + wb - 1) / wb, tt = (g.OH + th - 1) / th;
+      const double waste = (double)tw * wb * tt * th / ((double)g.OW * g.OH);
       const double score = waste * (1.0 + 24.0 / P);
       if (score < best_score - 1e-9) {
         best_score = score;
-        best = BoxShape{wb, hb, tw, th};
+        best = BoxShape{wb, th, th / cg, tw, tt};
       }
     }
   }
@@ -462,21 +637,27 @@ BoxShape pick_box(const ConvGeom& g, bool pix_on_n) {
 }  // namespace
 
 void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
-  require_tf32(g.precision);
-  if (g.K % 4 != 0) fail(TK_ERR_CAPABILITY, "tc_gemm: K must be a multiple of 4 (pack first)");
+  require_tc(g.precision);
+  const bool tf32 = g.precision == TK_PREC_TF32;
+  const int esize = tf32 ? 4 : 2;
+  const int ek = kSlabBytes / esize;
+  if ((g.K * esize) % 16 != 0) fail(TK_ERR_CAPABILITY, "tc_gemm: rows must be 16-byte multiples");
+  const int cg = g.M > kRows ? 2 : 1;
   int bn = g.tile_n > 0 ? g.tile_n : (g.N >= 256 ? 256 : ((g.N + 15) / 16) * 16);
   if (bn > 256) bn = 256;
-  if (bn < 16) bn = 16;
-  bn = (bn + 15) / 16 * 16;
+  const int step = 16 * cg;
+  bn = (bn + step - 1) / step * step;
+  if (bn < step) bn = step;
   TcArgs p{};
   p.M = g.M;
   p.N = g.N;
   p.K = g.K;
   p.BN = bn;
-  p.num_m = (g.M + kBM - 1) / kBM;
+  p.ek = ek;
+  p.num_m = (g.M + kRows * cg - 1) / (kRows * cg);
   p.num_n = (g.N + bn - 1) / bn;
   p.batch = g.batch;
-  p.num_kb = (g.K + 31) / 32;
+  p.num_kb = (g.K + ek - 1) / ek;
   p.d = g.d;
   p.c = g.c;
   p.d_sm = g.d_sm;
@@ -485,37 +666,57 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
   p.alpha = g.alpha;
   p.beta = g.beta;
   p.read_c = g.c != nullptr && g.beta != 0.0f;
-  const CUtensorMap ma = map_rows(g.a, g.K, g.M, g.batch, g.a_batch, kBM);
-  const CUtensorMap mb = map_rows(g.b, g.K, g.N, g.batch, g.b_batch, bn);
-  run_kernel<kPlain>(ma, mb, p, 0, st);
+  const CUtensorMap ma = map_rows(g.a, esize, g.K, g.M, g.batch, g.a_batch, kRows);
+  const CUtensorMap mb = map_rows(g.b, esize, g.K, g.N, g.batch, g.b_batch, bn / cg);
+  // Row-major output (d_sn == 1): stage through smem and TMA-store it.
+  CUtensorMap md = ma;
+  if (g.d_sn == 1 && !p.read_c && (g.d_sm * 4) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(g.d) & 15) == 0 && (bn % 32 == 0 || p.num_n == 1) &&
+      (g.batch == 1 || (g.d_batch * 4) % 16 == 0)) {
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)g.batch};
+    cuuint64_t strides[2] = {(cuuint64_t)g.d_sm * 4,
+                             (cuuint64_t)(g.d_batch ? g.d_batch : g.d_sm * g.M) * 4};
+    cuuint32_t box[3] = {32, (cuuint32_t)kRows, 1};
+    md = make_map(g.d, 4, 3, dims, strides, box);
+    p.store_tma = 1;
+    p.epi_bufs = 2;
+  }
+  dispatch<kPlain>(ma, mb, md, p, cg, tf32, st);
 }
 
 void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float beta, bool ta,
                              bool tb, const float* a, const float* b, const float* c, float* d,
                              int precision, int tile_n, cudaStream_t st) {
-  require_tf32(precision);
-  const long long kp = (long long)((k + 3) / 4 * 4);
-  // A as [m][k]: stored k x m (transposed) is already K-major.
-  const bool a_ok = ta && kp == (long long)k;
-  const bool b_ok = !tb && kp == (long long)k;
-  float* pa = nullptr;
-  float* pb = nullptr;
-  if (!a_ok) TKB_CUDA(cudaMallocAsync(&pa, (size_t)m * kp * 4, st));
-  if (!b_ok) TKB_CUDA(cudaMallocAsync(&pb, (size_t)n * kp * 4, st));
+  require_tc(precision);
+  const bool tf32 = precision == TK_PREC_TF32;
+  const long long kp = tf32 ? (long long)((k + 3) / 4 * 4) : (long long)((k + 7) / 8 * 8);
+  // TF32 operands already K-major with 16-byte rows are used in place;
+  // everything else is packed (and converted for BF16).
+  const bool a_ok = tf32 && ta && kp == (long long)k;
+  const bool b_ok = tf32 && !tb && kp == (long long)k;
+  const size_t esz = tf32 ? 4 : 2;
+  void* pa = nullptr;
+  void* pb = nullptr;
+  if (!a_ok) TKB_CUDA(cudaMallocAsync(&pa, (size_t)m * kp * esz, st));
+  if (!b_ok) TKB_CUDA(cudaMallocAsync(&pb, (size_t)n * kp * esz, st));
+  auto pack = [&](const float* src, long long rs, long long ks, long long rows, void* dst) {
+    if (tf32) pack_kmajor<float>(src, rs, ks, rows, (long long)k, kp, (float*)dst, false, st);
+    else pack_kmajor<__nv_bfloat16>(src, rs, ks, rows, (long long)k, kp, (__nv_bfloat16*)dst, false, st);
+  };
   if (!a_ok) {
-    if (ta) pack_kmajor(a, (long long)k, 1, (long long)m, (long long)k, kp, pa, st);
-    else pack_kmajor(a, 1, (long long)m, (long long)m, (long long)k, kp, pa, st);
+    if (ta) pack(a, (long long)k, 1, (long long)m, pa);
+    else pack(a, 1, (long long)m, (long long)m, pa);
   }
   if (!b_ok) {
-    if (tb) pack_kmajor(b, 1, (long long)n, (long long)n, (long long)k, kp, pb, st);
-    else pack_kmajor(b, (long long)k, 1, (long long)n, (long long)k, kp, pb, st);
+    if (tb) pack(b, 1, (long long)n, (long long)n, pb);
+    else pack(b, (long long)k, 1, (long long)n, pb);
   }
   TcGemm g;
   g.M = (int)m;
   g.N = (int)n;
   g.K = (int)kp;
-  g.a = a_ok ? a : pa;
-  g.b = b_ok ? b : pb;
+  g.a = a_ok ? a : (const float*)pa;
+  g.b = b_ok ? b : (const float*)pb;
   g.d = d;
   g.c = c;
   g.d_sm = 1;
@@ -531,94 +732,147 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
 
 namespace {
 
-bool conv_boxable(const ConvGeom& g) { return g.C % 32 == 0 && g.stride == 1; }
+// Slab width in elements for the precision.
+int slab_elems(int precision) { return precision == TK_PREC_TF32 ? 32 : 64; }
 
-long long conv_kp(const ConvGeom& g) {
-  const long long K = (long long)g.R * g.S * g.C;
-  return conv_boxable(g) ? K : (K + 31) / 32 * 32;
+bool conv_boxable(const ConvGeom& g, int precision) {
+  return g.C % slab_elems(precision) == 0 && g.stride == 1;
 }
+
+long long conv_kp(const ConvGeom& g, int precision) {
+  const long long K = (long long)g.R * g.S * g.C;
+  if (conv_boxable(g, precision)) return K;
+  return (K + 31) / 32 * 32;  // fallback path is always TF32 on fp32 patches
+}
+
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
 }  // namespace
 
 size_t tc_conv_workspace(const ConvGeom& g, int precision) {
-  (void)precision;
-  const long long kp = conv_kp(g);
-  size_t bytes = ((size_t)g.K * kp * 4 + 255) / 256 * 256;
-  if (!conv_boxable(g)) bytes += (size_t)g.N * g.OH * g.OW * kp * 4;
+  const long long kp = conv_kp(g, precision);
+  const bool box = conv_boxable(g, precision);
+  const size_t esz = (box && precision == TK_PREC_BF16) ? 2 : 4;
+  size_t bytes = align256((size_t)g.K * kp * esz);
+  if (!box) bytes += align256((size_t)g.N * g.OH * g.OW * kp * 4);
+  else if (precision == TK_PREC_BF16) bytes += align256((size_t)g.N * g.H * g.W * g.C * 2);
   return bytes;
 }
 
 void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float* out,
                     int precision, void* ws, cudaStream_t st) {
-  require_tf32(precision);
+  require_tc(precision);
   const long long K = (long long)g.R * g.S * g.C;
-  const long long kp = conv_kp(g);
-  float* ft = static_cast<float*>(ws);
-  // Filter HWCK = [K][Kout] -> [Kout][kp] (K-major, zero padded).
-  pack_kmajor(filt, 1, g.K, g.K, K, kp, ft, st);
+  const bool box = conv_boxable(g, precision);
+  const long long kp = conv_kp(g, precision);
+  char* cursor = static_cast<char*>(ws);
 
-  if (!conv_boxable(g)) {
-    // Explicit patch matrix + plain GEMM: D(feature, pixel) -> NHWC.
-    float* patches = reinterpret_cast<float*>(static_cast<char*>(ws) +
-                                              ((size_t)g.K * kp * 4 + 255) / 256 * 256);
-    const long long pixels = (long long)g.N * g.OH * g.OW;
-    const long long n = pixels * kp;
-    patches_rm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, in, kp, patches);
+  if (!box) {
+    // Explicit patch matrix (fp32, TF32 math) + plain GEMM.
+    float* ft = reinterpret_cast<float*>(cursor);
+    cursor += align256((size_t)g.K * kp * 4);
+    float* patches = reinterpret_cast<float*>(cursor);
+    pack_kmajor<float>(filt, 1, g.K, g.K, K, kp, ft, true, st);
+    const int pixels = g.N * g.OH * g.OW;
+    const long long chunks = (long long)pixels * (kp / 4);
+    patches_rm_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, st>>>(g, in, (int)kp, patches,
+                                                                        chunks);
     note_launch();
     TKB_CUDA(cudaGetLastError());
     TcGemm t;
-    t.M = g.K;
-    t.N = (int)pixels;
     t.K = (int)kp;
-    t.a = ft;
-    t.b = patches;
+    t.precision = TK_PREC_TF32;
+    if (g.K >= kRows) {
+      // features on M: D(feature, pixel) -> out[pixel*K + feature]
+      t.M = g.K;
+      t.N = pixels;
+      t.a = ft;
+      t.b = patches;
+      t.d_sm = 1;
+      t.d_sn = g.K;
+    } else {
+      // pixels on M: each thread writes its pixel's contiguous features
+      t.M = pixels;
+      t.N = g.K;
+      t.a = patches;
+      t.b = ft;
+      t.d_sm = g.K;
+      t.d_sn = 1;
+    }
     t.d = out;
-    t.d_sm = 1;
-    t.d_sn = g.K;
-    t.precision = precision;
     launch_tc_gemm(t, st);
     return;
   }
 
-  const bool pix_on_n = g.K >= kBM;
-  const BoxShape box = pick_box(g, pix_on_n);
-  if (box.wb == 0) fail(TK_ERR_CAPABILITY, "tc_conv: no pixel box fits this output plane");
+  const bool tf32 = precision == TK_PREC_TF32;
+  const int esize = tf32 ? 4 : 2;
+  const int ek = kSlabBytes / esize;
+  const void* fa = nullptr;
+  const void* xin = in;
+  if (tf32) {
+    float* ft = reinterpret_cast<float*>(cursor);
+    pack_kmajor<float>(filt, 1, g.K, g.K, K, kp, ft, true, st);
+    fa = ft;
+  } else {
+    __nv_bfloat16* ft = reinterpret_cast<__nv_bfloat16*>(cursor);
+    cursor += align256((size_t)g.K * kp * 2);
+    pack_kmajor<__nv_bfloat16>(filt, 1, g.K, g.K, K, kp, ft, false, st);
+    __nv_bfloat16* xb = reinterpret_cast<__nv_bfloat16*>(cursor);
+    to_bf16(in, xb, (long long)g.N * g.H * g.W * g.C, st);
+    fa = ft;
+    xin = xb;
+  }
+
+  const bool pix_on_n = g.K >= kRows;
+  const int cg = pix_on_n ? (g.K >= 2 * kRows ? 2 : 1) : 2;
+  const BoxShape bx = pick_box(g, pix_on_n, cg);
+  if (bx.wb == 0) fail(TK_ERR_CAPABILITY, "tc_conv: no pixel box fits this output plane");
   TcArgs p{};
   p.K = (int)K;
-  p.num_kb = (int)(K / 32);
+  p.ek = ek;
+  p.num_kb = (int)(K / ek);
   p.batch = 1;
   p.d = out;
   p.alpha = 1.0f;
   p.OH = g.OH;
   p.OW = g.OW;
   p.Kout = g.K;
-  p.Wb = box.wb;
-  p.Hb = box.hb;
-  p.tiles_w = box.tiles_w;
-  p.tiles_h = box.tiles_h;
+  p.Wb = bx.wb;
+  p.tileH = bx.tileH;
+  p.boxH = bx.boxH;
+  p.tiles_w = bx.tiles_w;
+  p.tiles_h = bx.tiles_h;
   p.pad_t = g.pad_t;
   p.pad_l = g.pad_l;
-  p.cchunks = g.C / 32;
+  p.cchunks = g.C / ek;
   p.S = g.S;
-  const int pix_tiles = g.N * box.tiles_w * box.tiles_h;
+  const int pix_tiles = g.N * bx.tiles_w * bx.tiles_h;
   if (pix_on_n) {
-    p.BN = box.wb * box.hb;
+    p.BN = bx.wb * bx.tileH;
     p.M = g.K;
     p.N = p.BN * pix_tiles;
-    p.num_m = (g.K + kBM - 1) / kBM;
+    p.num_m = (g.K + kRows * cg - 1) / (kRows * cg);
     p.num_n = pix_tiles;
-    const CUtensorMap ma = map_rows2d(ft, kp, g.K, kBM);
-    const CUtensorMap mb = map_nhwc(in, g, box.wb, box.hb);
-    run_kernel<kConvPixN>(ma, mb, p, 0, st);
+    const CUtensorMap ma = map_rows2d(fa, esize, kp, g.K, kRows);
+    const CUtensorMap mb = map_nhwc(xin, esize, g, bx.wb, bx.boxH);
+    dispatch<kConvPixN>(ma, mb, ma, p, cg, tf32, st);
   } else {
-    p.BN = (g.K + 15) / 16 * 16;
-    p.M = kBM * pix_tiles;
+    p.BN = (g.K + 16 * cg - 1) / (16 * cg) * (16 * cg);
+    p.M = kRows * cg * pix_tiles;
     p.N = g.K;
     p.num_m = pix_tiles;
     p.num_n = 1;
-    const CUtensorMap ma = map_nhwc(in, g, box.wb, box.hb);
-    const CUtensorMap mb = map_rows2d(ft, kp, g.K, p.BN);
-    run_kernel<kConvPixM>(ma, mb, p, 0, st);
+    const CUtensorMap ma = map_nhwc(xin, esize, g, bx.wb, bx.boxH);
+    const CUtensorMap mb = map_rows2d(fa, esize, kp, g.K, p.BN / cg);
+    if (g.K % 4 != 0) fail(TK_ERR_CAPABILITY, "tc_conv: output features must be a multiple of 4");
+    cuuint64_t dims[4] = {(cuuint64_t)g.K, (cuuint64_t)g.OW, (cuuint64_t)g.OH, (cuuint64_t)g.N};
+    cuuint64_t strides[3] = {(cuuint64_t)g.K * 4, (cuuint64_t)g.OW * g.K * 4,
+                             (cuuint64_t)g.OH * g.OW * g.K * 4};
+    cuuint32_t box[4] = {32, (cuuint32_t)bx.wb, (cuuint32_t)bx.boxH, 1};
+    const CUtensorMap md = make_map(out, 4, 4, dims, strides, box);
+    p.store_tma = 1;
+    p.epi_bufs = 2;
+    dispatch<kConvPixM>(ma, mb, md, p, cg, tf32, st);
   }
 }
 

@@ -1,9 +1,10 @@
 """GPU parity of the tensor-core (tcgen05 TF32) paths.
 
-Tolerance (stated here): TF32 operands are truncated to a
-10-bit mantissa, so results are judged with the reference's scale-normalised
-metric max_scaled_error (numeric.hpp:39-56) at <= 1e-3 for GEMM / implicit
-GEMM / Winograd F(2x2) and <= 1e-2 for Winograd F(4x4).
+Tolerances (stated here), judged with the reference's
+scale-normalised metric max_scaled_error (numeric.hpp:39-56):
+  TF32 (10-bit mantissa operands)     <= 1e-3 GEMM / implicit GEMM / Winograd
+                                       F(2x2); <= 1e-2 Winograd F(4x4)
+  BF16 (7-bit mantissa operands)      <= 5e-3
 """
 import numpy as np
 import pytest
@@ -12,6 +13,8 @@ pytestmark = pytest.mark.gpu
 
 TOL_TF32 = 1e-3
 TOL_TF32_F4 = 1e-2
+TOL_BF16 = 5e-3
+TOL = {'tf32': TOL_TF32, 'bf16': TOL_BF16}
 
 
 def dev_conv(tk, x, f, shape, algo, precision="tf32"):
@@ -23,10 +26,11 @@ def dev_conv(tk, x, f, shape, algo, precision="tf32"):
     return dy.cpu().numpy()
 
 
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
 @pytest.mark.parametrize("m,n,k,ta,tb", [(128, 128, 32, 1, 0), (256, 512, 128, 1, 0),
                                          (1024, 1024, 1024, 0, 0), (33, 29, 21, 0, 1),
                                          (300, 200, 100, 1, 1), (1000, 70, 64, 0, 0)])
-def test_tc_gemm_colmajor(tk, oracle, m, n, k, ta, tb):
+def test_tc_gemm_colmajor(tk, oracle, m, n, k, ta, tb, prec):
     import torch
     a = oracle.fill_random(m * k, 1)
     b = oracle.fill_random(k * n, 2)
@@ -35,27 +39,28 @@ def test_tc_gemm_colmajor(tk, oracle, m, n, k, ta, tb):
     da, db, dc = (torch.from_numpy(v).cuda() for v in (a, b, c))
     out = torch.full((m * n,), float("nan"), device="cuda")
     shape = tk.GemmShape(m, n, k, 1.5, -0.5, "t" if ta else "n", "t" if tb else "n")
-    tk.gemm_dev(da, db, dc, out, shape, precision="tf32")
+    tk.gemm_dev(da, db, dc, out, shape, precision=prec)
     torch.cuda.synchronize()
     err = oracle.max_scaled_error(out.cpu().numpy(), want)
-    assert err <= TOL_TF32, err
+    assert err <= TOL[prec], err
 
 
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
 @pytest.mark.parametrize("shape", [
-    (2, 14, 14, 32, 128), (1, 28, 28, 64, 64), (2, 56, 56, 64, 128), (1, 28, 28, 256, 512),
+    (2, 14, 14, 32, 128), (2, 14, 14, 64, 256), (2, 30, 30, 128, 64), (1, 56, 56, 64, 64), (1, 28, 28, 64, 64), (2, 56, 56, 64, 128), (1, 28, 28, 256, 512),
     (3, 17, 23, 32, 96), (1, 112, 112, 64, 128), (2, 7, 7, 512, 512), (1, 9, 9, 3, 16),
 ])
-def test_tc_conv_im2col(tk, oracle, shape):
+def test_tc_conv_im2col(tk, oracle, shape, prec):
     N, H, W, C, K = shape
     s = tk.ConvShape(N, H, W, C, K, 3, 3, 1, True)
     conv = oracle.Conv(N, H, W, C, K, 3, 3, 1, True)
     x = oracle.fill_random(int(np.prod(conv.in_shape)), 5).reshape(conv.in_shape)
     f = oracle.fill_random(int(np.prod(conv.filt_shape)), 6).reshape(conv.filt_shape)
     want = oracle.conv2d_naive(conv, x, f)
-    got = dev_conv(tk, x, f, s, "im2col")
+    got = dev_conv(tk, x, f, s, "im2col", precision=prec)
     assert not np.isnan(got).any()
     err = oracle.max_scaled_error(got, want)
-    assert err <= TOL_TF32, err
+    assert err <= TOL[prec], err
 
 
 @pytest.mark.parametrize("window,stride,same", [(1, 1, True), (1, 2, True), (7, 2, True),
@@ -82,7 +87,8 @@ def test_tc_winograd(tk, oracle, m):
     assert err <= (TOL_TF32 if m == 2 else TOL_TF32_F4), err
 
 
-def test_tc_vgg_batch32_full_size_property(tk, oracle):
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+def test_tc_vgg_batch32_full_size_property(tk, oracle, prec):
     """BASELINE config 2 at full size (vgg_conv3_2, batch 32): the oracle
     cannot run the whole batch in seconds, so check images 0 and 31 against
     single-image oracle runs (batch independence, test_conv.cpp:268-293)."""
@@ -93,11 +99,11 @@ def test_tc_vgg_batch32_full_size_property(tk, oracle):
     dx = torch.rand((N, H, H, C), device="cuda", generator=gen) * 2 - 1
     df = torch.rand((3, 3, C, K), device="cuda", generator=gen) * 2 - 1
     dy = torch.empty((N, H, H, K), device="cuda")
-    tk.conv2d_dev(dx, df, dy, s, tk.parse_conv_params("im2col"), precision="tf32")
+    tk.conv2d_dev(dx, df, dy, s, tk.parse_conv_params("im2col"), precision=prec)
     torch.cuda.synchronize()
     f = df.cpu().numpy()
     for img in (0, N - 1):
         conv = oracle.Conv(1, H, H, C, K, 3, 3, 1, True)
         want = oracle.conv2d_naive(conv, dx[img:img + 1].cpu().numpy(), f)
         err = oracle.max_scaled_error(dy[img:img + 1].cpu().numpy(), want)
-        assert err <= TOL_TF32, (img, err)
+        assert err <= TOL[prec], (img, err)
