@@ -49,7 +49,16 @@ constexpr int kThreads = 192;
 constexpr int kAccCols = 256;
 constexpr int kMaxStages = 8;
 
-enum TcMode : int { kPlain = 0, kConvPixN = 1, kConvPixM = 2 };
+enum TcMode : int { kPlain = 0, kConvPixN = 1, kConvPixM = 2, kConvGather = 3 };
+
+// Gather mode adds kGatherGroups x 4 producer warps (6..) that build the
+// pixel operand; groups take alternate K-slabs so their load latencies
+// overlap.
+constexpr int kGatherGroups = 2;
+template <int MODE>
+constexpr int threads_of() {
+  return MODE == kConvGather ? kThreads + 128 * kGatherGroups : kThreads;
+}
 
 struct TcArgs {
   int M, N, K;
@@ -62,9 +71,13 @@ struct TcArgs {
   float alpha, beta;
   int read_c;
   int store_tma;               // epilogue via swizzled smem tile + TMA store
+  int epi_bytes;               // bytes of epilogue staging
   int epi_bufs;                // staging buffers for the TMA-store epilogue
   // conv geometry
   int OH, OW, Kout, Wb, tileH, boxH, tiles_w, tiles_h, pad_t, pad_l, cchunks, S;
+  // gather mode: input geometry
+  const float* in;
+  int H, W, C, R, stride, Kreal;
 };
 
 struct PixTile {
@@ -106,21 +119,22 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
   for (int j = 0; j < nchunks; ++j) {
     float v[32];
     ptx::tmem_ld32(taddr + j * 32, v);
-    uint8_t* rowp = sbuf + j * kRows * kSlabBytes + row * kSlabBytes;
+    const uint32_t rowp = ptx::smem(sbuf + j * kRows * kSlabBytes + row * kSlabBytes);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      *reinterpret_cast<float4*>(rowp + ((c ^ (row & 7)) << 4)) =
-          make_float4(p.alpha * v[4 * c], p.alpha * v[4 * c + 1], p.alpha * v[4 * c + 2],
-                      p.alpha * v[4 * c + 3]);
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(rowp + ((c ^ (row & 7)) << 4)),
+                   "f"(p.alpha * v[4 * c]), "f"(p.alpha * v[4 * c + 1]),
+                   "f"(p.alpha * v[4 * c + 2]), "f"(p.alpha * v[4 * c + 3])
+                   : "memory");
     }
   }
-  // Accumulator fully read: hand TMEM back to the MMA warp.
   ptx::tc_fence_before();
-  if constexpr (CG == 2) ptx::mbar_arrive_cluster(empty_cluster_addr);
-  else ptx::mbar_arrive(empty_local);
   ptx::fence_proxy_async();
   ptx::named_sync(1, 128);
   if (issuer) {
+    // Accumulator fully read by all 128 threads: hand TMEM back to the MMA.
+    if constexpr (CG == 2) ptx::mbar_arrive_cluster(empty_cluster_addr);
+    else ptx::mbar_arrive(empty_local);
     for (int j = 0; j < nchunks; ++j) {
       const uint8_t* src = sbuf + j * kRows * kSlabBytes;
       if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + 32 * j, c1, c2, c3);
@@ -130,8 +144,98 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
   }
 }
 
+// Gather producer (conv fallback for channel counts / strides the TMA box
+// cannot express): 128 threads build the 128-pixel x 32-element fp32 K-slab
+// of the implicit patch matrix directly in the 128-byte-swizzled layout the
+// UMMA descriptor expects, reading the NHWC input through the read-only
+// cache (neighbouring pixels share most taps, so it is served from L1/L2).
+// K order is the reference's (x, y, c) (conv.hpp:286-292); K is zero-padded
+// to whole slabs.  Thread t owns 16-byte chunk q = t % 8 of rows
+// t / 8 + 16 i; completion is an mbarrier arrival (count 128 per CTA) on the
+// leader's `full` barrier after a proxy fence.
+template <int CG>
+__device__ __forceinline__ void gather_producer(const TcArgs& p, uint8_t* base, int stage_bytes,
+                                                uint64_t* full, uint64_t* empty,
+                                                const int2* ktab, uint32_t warp, uint32_t lane,
+                                                uint32_t rank, int unit, int nunits, int total) {
+  const int group = (int)(warp - 6) / 4;
+  const int t = (int)((warp - 6) & 3) * 32 + (int)lane;
+  const int q = t & 7;
+  const int r0 = t >> 3;
+  const uint32_t sbase = ptx::smem(base);
+  int local = 0;
+  for (int tt = unit; tt < total; tt += nunits, ++local) {
+    if ((local % kGatherGroups) != group) continue;  // groups own alternate tiles
+    const int m_blk = tt % p.num_m;
+    // Pixel geometry of this thread's 8 rows (rows r0 + 16 i), walked
+    // incrementally from the first row: no per-row division.
+    const float* rowp[8];
+    int ih0[8], iw0[8];
+    {
+      int m = m_blk * kRows * CG + (int)rank * kRows + r0;
+      int ow = m % p.OW;
+      int rest = m / p.OW;
+      int oh = rest % p.OH;
+      int n = rest / p.OH;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool ok = m < p.M;
+        ih0[i] = ok ? oh * p.stride - p.pad_t : -(1 << 28);
+        iw0[i] = ow * p.stride - p.pad_l;
+        rowp[i] = p.in + (((long long)n * p.H + ih0[i]) * p.W + iw0[i]) * p.C;
+        m += 16;
+        ow += 16;
+        while (ow >= p.OW) {
+          ow -= p.OW;
+          if (++oh == p.OH) {
+            oh = 0;
+            ++n;
+          }
+        }
+      }
+    }
+    for (int kb = 0; kb < p.num_kb; ++kb) {
+      const int seq = local * p.num_kb + kb;  // slab sequence of this CTA
+      const int stage = seq % p.stages;
+      const uint32_t phase = (uint32_t)(seq / p.stages) & 1u;
+      int2 kd[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) kd[u] = ktab[kb * 32 + q * 4 + u];
+      // Loads first (they do not touch the stage), then wait for the slot.
+      float v[8][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int x = kd[u].y >> 16, y = (kd[u].y << 16) >> 16;
+          const int ih = ih0[i] + x, iw = iw0[i] + y;
+          v[i][u] = ((unsigned)ih < (unsigned)p.H && (unsigned)iw < (unsigned)p.W)
+                        ? __ldg(rowp[i] + kd[u].x)
+                        : 0.0f;
+        }
+      }
+      ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
+      const uint32_t sa = sbase + stage * stage_bytes;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = r0 + 16 * i;
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(
+                         sa + r * kSlabBytes + ((q ^ (r & 7)) << 4)),
+                     "f"(v[i][0]), "f"(v[i][1]), "f"(v[i][2]), "f"(v[i][3])
+                     : "memory");
+      }
+      ptx::fence_proxy_async();
+      ptx::named_sync(2 + group, 128);
+      if (t == 0) {
+        if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::map_to_rank(ptx::smem(&full[stage]), 0));
+        else ptx::mbar_arrive(&full[stage]);
+      }
+    }
+  }
+}
+
 template <int MODE, int CG, bool TF32>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(threads_of<MODE>(), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_d, TcArgs p) {
@@ -151,6 +255,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   // TMA-store staging: epi_bufs x (BN/32) swizzled 128-row x 128-byte tiles
   uint8_t* epi_stage = base + p.stages * stage_bytes + 1024;
+  // gather mode: K -> {element offset (x*W + y)*C + c, (x << 16) | y} table,
+  // K padded to whole slabs with out-of-window markers.
+  int2* ktab = reinterpret_cast<int2*>(epi_stage + p.epi_bytes);
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   const uint32_t rank = CG == 2 ? ptx::cluster_rank() : 0;
@@ -163,12 +270,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&full[s], MODE == kConvGather ? 1 + CG : 1);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tmem_full[a], 1);
-      ptx::mbar_init(&tmem_empty[a], 128 * CG);
+      ptx::mbar_init(&tmem_empty[a], CG);
     }
     ptx::fence_mbar_init();
   }
@@ -196,12 +303,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (MODE == kConvPixN) pt = pix_tile(p, n_blk);
         if constexpr (MODE == kConvPixM) pt = pix_tile(p, m_blk);
         for (int kb = 0; kb < p.num_kb; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
           uint8_t* sa = base + stage * stage_bytes;
           uint8_t* sb = sa + a_bytes;
           uint32_t fb = ptx::smem(&full[stage]);
           if constexpr (CG == 2) fb = ptx::map_to_rank(fb, 0);
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], CG * stage_bytes);
+          if (leader)
+            ptx::mbar_arrive_expect_tx(&full[stage],
+                                       CG * (MODE == kConvGather ? b_bytes : stage_bytes));
           const int k0 = kb * p.ek;
           int c0 = 0, dy = 0, dx = 0;
           if constexpr (MODE != kPlain) {
@@ -216,8 +325,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else if constexpr (MODE == kConvPixN) {
             ptx::tma2<CG>(sa, &map_a, fb, k0, m_blk * BM + rank * kRows);
             ptx::tma4<CG>(sb, &map_b, fb, c0, pt.ow0 + dy, pt.oh0 + rank * p.boxH + dx, pt.img);
-          } else {
+          } else if constexpr (MODE == kConvPixM) {
             ptx::tma4<CG>(sa, &map_a, fb, c0, pt.ow0 + dy, pt.oh0 + rank * p.boxH + dx, pt.img);
+            ptx::tma2<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows);
+          } else {
             ptx::tma2<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows);
           }
           if (++stage == p.stages) {
@@ -237,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = unit; t < total; t += nunits, ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
-        ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        ptx::mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
         for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -262,15 +373,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+  } else if (MODE == kConvGather && warp >= 6) {
+    // ---------------- pixel gather (warps 6.., every CTA) ----------------
+    {
+      const int tid = (int)(warp - 6) * 32 + (int)lane;
+      for (int k = tid; k < p.num_kb * 32; k += 128 * kGatherGroups) {
+        int2 e;
+        if (k < p.Kreal) {
+          const int c = k % p.C, tap = k / p.C;
+          const int y = tap % p.S, x = tap / p.S;
+          e.x = (x * p.W + y) * p.C + c;
+          e.y = (x << 16) | (y & 0xFFFF);
+        } else {
+          e.x = 0;
+          e.y = (1 << 30);  // x huge: always outside the input
+        }
+        ktab[k] = e;
+      }
+      ptx::named_sync(4, 128 * kGatherGroups);
+    }
+    gather_producer<CG>(p, base, stage_bytes, full, empty, ktab, warp, lane, rank, unit, nunits,
+                        total);
   } else {
     // ---------------- epilogue (warps 2..5, every CTA) ----------------
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
-    uint32_t empty_addr[2] = {ptx::smem(&tmem_empty[0]), ptx::smem(&tmem_empty[1])};
-    if constexpr (CG == 2) {
-      empty_addr[0] = ptx::map_to_rank(empty_addr[0], 0);
-      empty_addr[1] = ptx::map_to_rank(empty_addr[1], 0);
-    }
+    uint32_t empty_base = ptx::smem(&tmem_empty[0]);
+    if constexpr (CG == 2) empty_base = ptx::map_to_rank(empty_base, 0);
     int local = 0;
     for (int t = unit; t < total; t += nunits, ++local) {
       const int m_blk = t % p.num_m;
@@ -279,16 +408,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int z = rest / p.num_n;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      ptx::mbar_wait(&tmem_full[acc], acc_phase);
+      ptx::mbar_wait_sleep(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
 
-      if constexpr (MODE == kPlain) {
+      if constexpr (MODE == kConvGather) {
+        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, empty_base + 8u * acc,
+                               &tmem_empty[acc], &map_d, n_blk * p.BN, m_blk * BM + rank * kRows,
+                               0, 0, 3);
+        continue;
+      } else if constexpr (MODE == kPlain) {
         const int m = m_blk * BM + rank * kRows + row;
         float* dz = p.d + (long long)z * p.d_batch;
         const float* cz = p.read_c ? p.c + (long long)z * p.d_batch : nullptr;
         if (p.store_tma) {
-          tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, empty_addr[acc],
+          tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, empty_base + 8u * acc,
                                  &tmem_empty[acc], &map_d, n_blk * p.BN,
                                  m_blk * BM + rank * kRows, z, 0, 3);
           continue;
@@ -334,14 +468,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         const PixTile pt = pix_tile(p, m_blk);
-        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, empty_addr[acc],
+        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, empty_base + 8u * acc,
                                &tmem_empty[acc], &map_d, n_blk * p.BN, pt.ow0,
                                pt.oh0 + rank * p.boxH, pt.img, 4);
         continue;
       }
       ptx::tc_fence_before();
-      if constexpr (CG == 2) ptx::mbar_arrive_cluster(empty_addr[acc]);
-      else ptx::mbar_arrive(&tmem_empty[acc]);
+      ptx::named_sync(1, 128);
+      if (warp == 2 && lane == 0) {
+        if constexpr (CG == 2) ptx::mbar_arrive_cluster(empty_base + 8u * acc);
+        else ptx::mbar_arrive(&tmem_empty[acc]);
+      }
     }
   }
 
@@ -437,13 +574,15 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   const int stage_bytes = kRows * kSlabBytes + (p.BN / CG) * kSlabBytes;
   const int epi_bytes =
       p.store_tma ? p.epi_bufs * ((p.BN + 31) / 32) * kRows * kSlabBytes : 0;
-  const int budget = 232448 - 1024 - 1024 - epi_bytes;
+  p.epi_bytes = epi_bytes;
+  const int ktab_bytes = MODE == kConvGather ? p.num_kb * 32 * 8 : 0;
+  const int budget = 232448 - 1024 - 1024 - epi_bytes - ktab_bytes;
   int stages = budget / stage_bytes;
   if (stages > kMaxStages) stages = kMaxStages;
   if (stages_req > 0 && stages_req < stages) stages = stages_req;
   if (stages < 2) fail(TK_ERR_CAPABILITY, "tc_gemm: tile too large for shared memory");
   p.stages = stages;
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + 1024 + epi_bytes;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + 1024 + epi_bytes + ktab_bytes;
   auto fn = tc_gemm_kernel<MODE, CG, TF32>;
   TKB_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
@@ -453,7 +592,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   if (grid <= 0) return;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads_of<MODE>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -754,8 +893,7 @@ size_t tc_conv_workspace(const ConvGeom& g, int precision) {
   const bool box = conv_boxable(g, precision);
   const size_t esz = (box && precision == TK_PREC_BF16) ? 2 : 4;
   size_t bytes = align256((size_t)g.K * kp * esz);
-  if (!box) bytes += align256((size_t)g.N * g.OH * g.OW * kp * 4);
-  else if (precision == TK_PREC_BF16) bytes += align256((size_t)g.N * g.H * g.W * g.C * 2);
+  if (box && precision == TK_PREC_BF16) bytes += align256((size_t)g.N * g.H * g.W * g.C * 2);
   return bytes;
 }
 
@@ -768,39 +906,48 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   char* cursor = static_cast<char*>(ws);
 
   if (!box) {
-    // Explicit patch matrix (fp32, TF32 math) + plain GEMM.
+    // Gather mode: the pixel operand is built in shared memory by producer
+    // warps (any channel count / stride), the filter streams by TMA, the
+    // output leaves through a TMA store.  fp32 operands, kind::tf32.
     float* ft = reinterpret_cast<float*>(cursor);
-    cursor += align256((size_t)g.K * kp * 4);
-    float* patches = reinterpret_cast<float*>(cursor);
     pack_kmajor<float>(filt, 1, g.K, g.K, K, kp, ft, true, st);
     const int pixels = g.N * g.OH * g.OW;
-    const long long chunks = (long long)pixels * (kp / 4);
-    patches_rm_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, st>>>(g, in, (int)kp, patches,
-                                                                        chunks);
-    note_launch();
-    TKB_CUDA(cudaGetLastError());
-    TcGemm t;
-    t.K = (int)kp;
-    t.precision = TK_PREC_TF32;
-    if (g.K >= kRows) {
-      // features on M: D(feature, pixel) -> out[pixel*K + feature]
-      t.M = g.K;
-      t.N = pixels;
-      t.a = ft;
-      t.b = patches;
-      t.d_sm = 1;
-      t.d_sn = g.K;
-    } else {
-      // pixels on M: each thread writes its pixel's contiguous features
-      t.M = pixels;
-      t.N = g.K;
-      t.a = patches;
-      t.b = ft;
-      t.d_sm = g.K;
-      t.d_sn = 1;
-    }
-    t.d = out;
-    launch_tc_gemm(t, st);
+    const int cg = 2;
+    TcArgs p{};
+    p.M = pixels;
+    p.N = g.K;
+    p.K = (int)kp;
+    p.Kreal = (int)K;
+    p.ek = 32;
+    p.BN = std::min(256, (g.K + 16 * cg - 1) / (16 * cg) * (16 * cg));
+    p.num_m = (pixels + kRows * cg - 1) / (kRows * cg);
+    p.num_n = (g.K + p.BN - 1) / p.BN;
+    p.batch = 1;
+    p.num_kb = (int)(kp / 32);
+    p.d = out;
+    p.alpha = 1.0f;
+    p.OH = g.OH;
+    p.OW = g.OW;
+    p.Kout = g.K;
+    p.pad_t = g.pad_t;
+    p.pad_l = g.pad_l;
+    p.cchunks = 1;
+    p.S = g.S;
+    p.in = in;
+    p.H = g.H;
+    p.W = g.W;
+    p.C = g.C;
+    p.R = g.R;
+    p.stride = g.stride;
+    if (g.K % 4 != 0) fail(TK_ERR_CAPABILITY, "tc_conv: output features must be a multiple of 4");
+    const CUtensorMap mb = map_rows2d(ft, 4, kp, g.K, p.BN / cg);
+    cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)pixels, 1};
+    cuuint64_t strides[2] = {(cuuint64_t)g.K * 4, (cuuint64_t)g.K * pixels * 4};
+    cuuint32_t boxd[3] = {32, (cuuint32_t)kRows, 1};
+    const CUtensorMap md = make_map(out, 4, 3, dims, strides, boxd);
+    p.store_tma = 1;
+    p.epi_bufs = 2;
+    dispatch<kConvGather>(mb, mb, md, p, cg, true, st);
     return;
   }
 
