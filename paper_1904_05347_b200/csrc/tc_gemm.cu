@@ -32,6 +32,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -49,7 +50,7 @@ constexpr int kThreads = 192;
 constexpr int kAccCols = 256;
 constexpr int kMaxStages = 8;
 
-enum TcMode : int { kPlain = 0, kConvPixN = 1, kConvPixM = 2, kConvGather = 3 };
+enum TcMode : int { kPlain = 0, kConvPixN = 1, kConvPixM = 2, kConvGather = 3, kConvHalo = 4 };
 
 // Gather mode adds kGatherGroups x 4 producer warps (6..) that build the
 // pixel operand; groups take alternate K-slabs so their load latencies
@@ -75,6 +76,9 @@ struct TcArgs {
   int epi_bufs;                // staging buffers for the TMA-store epilogue
   // conv geometry
   int OH, OW, Kout, Wb, tileH, boxH, tiles_w, tiles_h, pad_t, pad_l, cchunks, S;
+  // halo mode: virtual pitch P, TH rows per CTA, TW useful columns, R*S taps
+  int P, TH, TW, taps, halo_bytes;
+  int resident;                // halo mode: this CTA's filter slice lives in smem
   // gather mode: input geometry
   const float* in;
   int H, W, C, R, stride, Kreal;
@@ -104,6 +108,7 @@ __device__ __forceinline__ PixTile pix_tile(const TcArgs& p, int t) {
 template <int CG>
 __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t taddr, uint8_t* stage,
                                                    int local, uint32_t warp, uint32_t lane, int row,
+                                                   int srow,
                                                    uint32_t empty_cluster_addr, uint64_t* empty_local,
                                                    const CUtensorMap* map_d, int c0, int c1, int c2,
                                                    int c3, int rank_dims) {
@@ -119,10 +124,11 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
   for (int j = 0; j < nchunks; ++j) {
     float v[32];
     ptx::tmem_ld32(taddr + j * 32, v);
-    const uint32_t rowp = ptx::smem(sbuf + j * kRows * kSlabBytes + row * kSlabBytes);
+    if (srow < 0) continue;  // virtual row without an output pixel
+    const uint32_t rowp = ptx::smem(sbuf + j * kRows * kSlabBytes + srow * kSlabBytes);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(rowp + ((c ^ (row & 7)) << 4)),
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(rowp + ((c ^ (srow & 7)) << 4)),
                    "f"(p.alpha * v[4 * c]), "f"(p.alpha * v[4 * c + 1]),
                    "f"(p.alpha * v[4 * c + 2]), "f"(p.alpha * v[4 * c + 3])
                    : "memory");
@@ -243,18 +249,23 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   constexpr int BM = kRows * CG;
-  const int a_bytes = kRows * kSlabBytes;
+  const int a_bytes = MODE == kConvHalo ? p.halo_bytes : kRows * kSlabBytes;
   const int b_rows = p.BN / CG;
   const int b_bytes = b_rows * kSlabBytes;
-  const int stage_bytes = a_bytes + b_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + p.stages * stage_bytes);
+  const int stage_bytes =
+      a_bytes + (MODE == kConvHalo ? (p.resident ? 0 : p.taps) : 1) * b_bytes;
+  // resident filter (halo mode): taps x cchunks slabs after the stages
+  uint8_t* fres = base + p.stages * stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      base + p.stages * stage_bytes + (p.resident ? p.taps * p.cchunks * b_bytes : 0));
   uint64_t* full = bars;
   uint64_t* empty = bars + kMaxStages;
   uint64_t* tmem_full = bars + 2 * kMaxStages;
   uint64_t* tmem_empty = tmem_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* fbar = tmem_empty + 2;  // resident-filter barrier
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fbar + 1);
   // TMA-store staging: epi_bufs x (BN/32) swizzled 128-row x 128-byte tiles
-  uint8_t* epi_stage = base + p.stages * stage_bytes + 1024;
+  uint8_t* epi_stage = reinterpret_cast<uint8_t*>(bars) + 1024;
   // gather mode: K -> {element offset (x*W + y)*C + c, (x << 16) | y} table,
   // K padded to whole slabs with out-of-window markers.
   int2* ktab = reinterpret_cast<int2*>(epi_stage + p.epi_bytes);
@@ -277,6 +288,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       ptx::mbar_init(&tmem_full[a], 1);
       ptx::mbar_init(&tmem_empty[a], CG);
     }
+    ptx::mbar_init(fbar, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc_cg<CG, 2 * kAccCols>(tmem_slot);
@@ -289,7 +301,107 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   const int total = p.num_m * p.num_n * p.batch;
   const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
 
-  if (warp == 0) {
+  if (MODE == kConvHalo && warp == 0) {
+    // ---------------- TMA producer, halo mode ----------------
+    // One super-stage per (tile, channel chunk): the (TH+R) x P halo box of
+    // this CTA's output rows plus the R*S filter slabs of the chunk.
+    if (ptx::elect_one()) {
+      if (p.resident) {
+        // Every tile of this CTA has the same feature block (host ensures
+        // nunits % num_n == 0): stage its filter slice once.
+        uint32_t fb = ptx::smem(fbar);
+        if constexpr (CG == 2) fb = ptx::map_to_rank(fb, 0);
+        if (leader) ptx::mbar_arrive_expect_tx(fbar, CG * p.taps * p.cchunks * b_bytes);
+        const int n_blk = unit % p.num_n;
+        for (int tap = 0; tap < p.taps; ++tap)
+          for (int ch = 0; ch < p.cchunks; ++ch)
+            ptx::tma2<CG>(fres + (tap * p.cchunks + ch) * b_bytes, &map_b, fb,
+                          tap * p.cchunks * p.ek + ch * p.ek, n_blk * p.BN + rank * b_rows);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = unit; t < total; t += nunits) {
+        const int n_blk = t % p.num_n;
+        const int m_blk = t / p.num_n;
+        const PixTile pt = pix_tile(p, m_blk);
+        for (int ch = 0; ch < p.cchunks; ++ch) {
+          ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
+          uint8_t* sa = base + stage * stage_bytes;
+          uint32_t fb = ptx::smem(&full[stage]);
+          if constexpr (CG == 2) fb = ptx::map_to_rank(fb, 0);
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], CG * stage_bytes);
+          const int c0 = ch * p.ek;
+          ptx::tma4<CG>(sa, &map_a, fb, c0, pt.ow0 - p.pad_l, pt.oh0 + rank * p.TH - p.pad_t, pt.img);
+          if (!p.resident)
+            for (int tap = 0; tap < p.taps; ++tap)
+              ptx::tma2<CG>(sa + a_bytes + tap * b_bytes, &map_b, fb, tap * p.cchunks * p.ek + c0,
+                            n_blk * p.BN + rank * b_rows);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (MODE == kConvHalo && warp == 1) {
+    // ---------------- MMA issuer, halo mode (leader CTA) ----------------
+    // Tap (x, y) reads the halo from row x*P + y on: output row v = h*P + w
+    // needs halo pixel (h + x, w + y), a constant shift in the virtual
+    // pitch-P layout.
+    if (leader) {
+      const uint32_t idesc = ptx::idesc(BM, p.BN, TF32);
+      if (p.resident) ptx::mbar_wait(fbar, 0);
+      const uint32_t fres_s = ptx::smem(fres);
+      const uint64_t kdesc = ptx::desc_sw128(0);
+      uint64_t tap_off[9];  // halo row shift of tap (x, y), in 16-byte units
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) {
+        const int x = tap / p.S, y = tap - (tap / p.S) * p.S;
+        tap_off[tap] = (uint64_t)((x * p.P + y) * (kSlabBytes / 16));
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = unit; t < total; t += nunits, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        ptx::mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        for (int ch = 0; ch < p.cchunks; ++ch) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            // Descriptors are linear in the 16-byte address field: build
+            // the stage bases once, then every MMA is two 64-bit adds.
+            const uint32_t sa = ptx::smem(base + stage * stage_bytes);
+            const uint64_t ad0 = kdesc + (sa >> 4);
+            const uint64_t bd0 = kdesc + ((p.resident ? fres_s + (uint32_t)(ch * b_bytes)
+                                                      : sa + (uint32_t)a_bytes) >> 4);
+            const uint64_t b_tap = (uint64_t)((p.resident ? p.cchunks : 1) * b_bytes) >> 4;
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) {
+              if (tap < p.taps) {
+                const uint64_t ad = ad0 + tap_off[tap];
+                const uint64_t bd = bd0 + b_tap * tap;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  ptx::mma_cg<CG, TF32>(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc,
+                                        (ch | tap | kk) != 0);
+              }
+            }
+            ptx::commit_cg<CG>(&empty[stage]);
+            if (ch == p.cchunks - 1) ptx::commit_cg<CG>(&tmem_full[acc]);
+          }
+          __syncwarp();
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 0) {
     // ---------------- TMA producer (every CTA) ----------------
     if (ptx::elect_one()) {
       int stage = 0;
@@ -342,6 +454,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
     // ---------------- MMA issuer (leader CTA) ----------------
     if (leader) {
       const uint32_t idesc = ptx::idesc(BM, p.BN, TF32);
+      const uint64_t kdesc = ptx::desc_sw128(0);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -356,12 +469,11 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
             const uint32_t sa = ptx::smem(base + stage * stage_bytes);
-            const uint32_t sb = sa + a_bytes;
+            const uint64_t ad = kdesc + (sa >> 4);
+            const uint64_t bd = kdesc + ((sa + (uint32_t)a_bytes) >> 4);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              ptx::mma_cg<CG, TF32>(d_tmem, ptx::desc_sw128(sa + kk * 32),
-                                    ptx::desc_sw128(sb + kk * 32), idesc, (kb | kk) != 0);
-            }
+            for (int kk = 0; kk < 4; ++kk)
+              ptx::mma_cg<CG, TF32>(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
             ptx::commit_cg<CG>(&empty[stage]);
             if (kb == p.num_kb - 1) ptx::commit_cg<CG>(&tmem_full[acc]);
           }
@@ -412,8 +524,17 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       ptx::tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
 
-      if constexpr (MODE == kConvGather) {
-        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, empty_base + 8u * acc,
+      if constexpr (MODE == kConvHalo) {
+        const int hn = t % p.num_n, hm = t / p.num_n;
+        const PixTile pt = pix_tile(p, hm);
+        const int h = row / p.P, w = row - (row / p.P) * p.P;
+        const int srow = w < p.TW ? h * p.TW + w : -1;
+        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, srow,
+                               empty_base + 8u * acc, &tmem_empty[acc], &map_d, hn * p.BN, pt.ow0,
+                               pt.oh0 + rank * p.TH, pt.img, 4);
+        continue;
+      } else if constexpr (MODE == kConvGather) {
+        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, row, empty_base + 8u * acc,
                                &tmem_empty[acc], &map_d, n_blk * p.BN, m_blk * BM + rank * kRows,
                                0, 0, 3);
         continue;
@@ -422,7 +543,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         float* dz = p.d + (long long)z * p.d_batch;
         const float* cz = p.read_c ? p.c + (long long)z * p.d_batch : nullptr;
         if (p.store_tma) {
-          tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, empty_base + 8u * acc,
+          tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, row, empty_base + 8u * acc,
                                  &tmem_empty[acc], &map_d, n_blk * p.BN,
                                  m_blk * BM + rank * kRows, z, 0, 3);
           continue;
@@ -468,7 +589,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         }
       } else {
         const PixTile pt = pix_tile(p, m_blk);
-        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, empty_base + 8u * acc,
+        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, row, empty_base + 8u * acc,
                                &tmem_empty[acc], &map_d, n_blk * p.BN, pt.ow0,
                                pt.oh0 + rank * p.boxH, pt.img, 4);
         continue;
@@ -571,24 +692,32 @@ int sm_count() {
 template <int MODE, int CG, bool TF32>
 void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, TcArgs p,
                 int stages_req, cudaStream_t st) {
-  const int stage_bytes = kRows * kSlabBytes + (p.BN / CG) * kSlabBytes;
+  const int b_bytes_h = (p.BN / CG) * kSlabBytes;
+  const int stage_bytes = MODE == kConvHalo
+                              ? p.halo_bytes + (p.resident ? 0 : p.taps) * b_bytes_h
+                              : kRows * kSlabBytes + b_bytes_h;
+  const int fres_bytes = (MODE == kConvHalo && p.resident) ? p.taps * p.cchunks * b_bytes_h : 0;
   const int epi_bytes =
       p.store_tma ? p.epi_bufs * ((p.BN + 31) / 32) * kRows * kSlabBytes : 0;
   p.epi_bytes = epi_bytes;
   const int ktab_bytes = MODE == kConvGather ? p.num_kb * 32 * 8 : 0;
-  const int budget = 232448 - 1024 - 1024 - epi_bytes - ktab_bytes;
+  const int budget = 232448 - 1024 - 1024 - epi_bytes - ktab_bytes - fres_bytes;
   int stages = budget / stage_bytes;
   if (stages > kMaxStages) stages = kMaxStages;
   if (stages_req > 0 && stages_req < stages) stages = stages_req;
   if (stages < 2) fail(TK_ERR_CAPABILITY, "tc_gemm: tile too large for shared memory");
   p.stages = stages;
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + 1024 + epi_bytes + ktab_bytes;
+  const size_t smem =
+      1024 + (size_t)stages * stage_bytes + fres_bytes + 1024 + epi_bytes + ktab_bytes;
   auto fn = tc_gemm_kernel<MODE, CG, TF32>;
   TKB_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   const long long total = (long long)p.num_m * p.num_n * p.batch;
   const int units = sm_count() / CG;
-  const int grid = (int)(total < units ? total : units) * CG;
+  int used = (int)(total < units ? total : units);
+  // Halo mode with a resident filter: every CTA must keep one feature block.
+  if (MODE == kConvHalo && p.resident) used -= used % p.num_n;
+  const int grid = used * CG;
   if (grid <= 0) return;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -968,6 +1097,65 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     to_bf16(in, xb, (long long)g.N * g.H * g.W * g.C, st);
     fa = ft;
     xin = xb;
+  }
+
+  // Halo mode: small-feature stride-1 layers whose tap re-reads of the
+  // input would otherwise dominate the L2->SM traffic.
+  const char* force = getenv("TK_CONV_MODE");
+  const bool halo_ok = g.stride == 1 && g.R * g.S <= 9 && g.S <= 3 && g.K % 32 == 0 &&
+                       ((g.K <= 128 && (g.C <= 64 || g.K <= 64)) ||
+                        (force && std::string(force) == "halo"));
+  const bool use_halo = halo_ok && !(force && std::string(force) != "halo");
+  if (use_halo) {
+    const int cg = 2;
+    TcArgs p{};
+    p.P = 16;
+    p.TH = kRows / p.P;
+    p.TW = p.P - (g.S - 1);
+    p.taps = g.R * g.S;
+    p.halo_bytes = (p.TH + g.R) * p.P * kSlabBytes;
+    p.K = (int)K;
+    p.ek = ek;
+    p.cchunks = g.C / ek;
+    p.num_kb = p.cchunks;
+    p.BN = g.K <= 32 ? 32 : 64;
+    p.Wb = p.TW;
+    p.tileH = cg * p.TH;
+    p.tiles_w = (g.OW + p.TW - 1) / p.TW;
+    p.tiles_h = (g.OH + p.tileH - 1) / p.tileH;
+    p.num_m = g.N * p.tiles_w * p.tiles_h;
+    p.num_n = (g.K + p.BN - 1) / p.BN;
+    p.M = p.num_m * kRows * cg;
+    p.N = g.K;
+    p.batch = 1;
+    p.d = out;
+    p.alpha = 1.0f;
+    p.OH = g.OH;
+    p.OW = g.OW;
+    p.Kout = g.K;
+    p.pad_t = g.pad_t;
+    p.pad_l = g.pad_l;
+    p.S = g.S;
+    const CUtensorMap ma = map_nhwc(xin, esize, g, p.P, p.TH + g.R);
+    const CUtensorMap mb = map_rows2d(fa, esize, kp, g.K, p.BN / cg);
+    cuuint64_t dims[4] = {(cuuint64_t)g.K, (cuuint64_t)g.OW, (cuuint64_t)g.OH, (cuuint64_t)g.N};
+    cuuint64_t strides[3] = {(cuuint64_t)g.K * 4, (cuuint64_t)g.OW * g.K * 4,
+                             (cuuint64_t)g.OH * g.OW * g.K * 4};
+    cuuint32_t box[4] = {32, (cuuint32_t)p.TW, (cuuint32_t)p.TH, 1};
+    const CUtensorMap md = make_map(out, 4, 4, dims, strides, box);
+    p.store_tma = 1;
+    p.epi_bufs = 1;
+    {
+      const int b_bytes_h = (p.BN / cg) * kSlabBytes;
+      const int fres = p.taps * p.cchunks * b_bytes_h;
+      const int epi = ((p.BN + 31) / 32) * kRows * kSlabBytes;
+      const int left = 232448 - 2048 - epi - fres;
+      const int units = sm_count() / cg;
+      p.resident = (left >= 3 * p.halo_bytes && units % p.num_n == 0) ? 1 : 0;
+      if (force && std::string(force) == "halo_stream") p.resident = 0;
+    }
+    dispatch<kConvHalo>(ma, mb, md, p, cg, tf32, st);
+    return;
   }
 
   const bool pix_on_n = g.K >= kRows;
