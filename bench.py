@@ -65,6 +65,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=32, help="images per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     return ap.parse_args()
 
 
@@ -128,68 +129,96 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # reference arm / CPU baseline: the unmodified reference on the host cores
 # ---------------------------------------------------------------------------
-def cpu_reference_sample(layers_batch=1, algos=None):
-    """Times the reference's own conv2d (oracle/_ref = ref_shim.cpp over the
-    reference headers; falls back to the C restatement) on every VGG-16
-    layer at batch `layers_batch`, best algorithm per layer.  Returns
-    (gflops, seconds, cores, kind, detail)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle as O
-    cores = os.cpu_count() or 1
-    os.environ.setdefault("TILEKIT_THREADS", str(cores))
-    kind = "reference" if O.have_ref() else "port"
-    algos = algos or ["im2col", "winograd_t4x4", "winograd_t2x2"]
-    total_flops, total_s, detail = 0, 0.0, []
+# The reference's fastest CPU algorithm per VGG-16 layer (its own conv2d
+# selector), from timing all of naive/tiled/im2col/winograd on the host.
+REF_ALGO = {
+    "vgg_conv1_1": "tiled_t4x5_v4x2", "vgg_conv1_2": "winograd_t4x4",
+    "vgg_conv2_1": "winograd_t4x4", "vgg_conv2_2": "winograd_t4x4",
+    "vgg_conv3_1": "winograd_t4x4", "vgg_conv3_2": "winograd_t2x2",
+    "vgg_conv4_1": "winograd_t4x4", "vgg_conv4_2": "winograd_t2x2",
+    "vgg_conv5": "winograd_t2x2",
+}
+
+
+def vgg_instances():
+    out = []
     for name, h, c, k, mult in VGG16:
-        s = O.Conv(layers_batch, h, h, c, k, 3, 3, 1, True)
-        x = O.fill_random(int(np.prod(s.in_shape)), 1).reshape(s.in_shape)
-        f = O.fill_random(int(np.prod(s.filt_shape)), 2).reshape(s.filt_shape)
-        best = None
-        for a in algos:
-            t0 = time.perf_counter()
-            if kind == "reference":
-                O.ref_conv2d(s, a, x, f)
-            elif a.startswith("winograd"):
-                O.conv2d_winograd(s, int(a[-1]), x, f)
-            else:
-                O.conv2d_naive(s, x, f)
-            dt = time.perf_counter() - t0
-            if best is None or dt < best[1]:
-                best = (a, dt)
-        total_flops += s.flops() * mult
-        total_s += best[1] * mult
-        detail.append(f"{name}:{best[0]}")
-    return total_flops / total_s / 1e9, total_s, cores, kind, detail
+        out += [(name, h, c, k)] * mult
+    return out
+
+
+class CpuReference:
+    """Times the reference's own conv2d on host cores: oracle/_ref (the
+    unmodified reference headers behind ref_shim.cpp) when it was built in
+    this tree, else the C restatement (kind "port").  A sample is one VGG-16
+    layer instance at batch 1 (1/32 of that layer's per-GPU work)."""
+
+    def __init__(self):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle as O
+        O.build()
+        self.O = O
+        self.cores = os.cpu_count() or 1
+        os.environ["TILEKIT_THREADS"] = str(self.cores)
+        self.kind = "reference" if O.have_ref() else "port"
+        self.cache = {}
+
+    def layer(self, name, h, c, k):
+        O = self.O
+        if name not in self.cache:
+            s = O.Conv(1, h, h, c, k, 3, 3, 1, True)
+            x = O.fill_random(int(np.prod(s.in_shape)), 1).reshape(s.in_shape)
+            f = O.fill_random(int(np.prod(s.filt_shape)), 2).reshape(s.filt_shape)
+            self.cache[name] = (s, x, f)
+        s, x, f = self.cache[name]
+        algo = REF_ALGO[name]
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            O.ref_conv2d(s, algo, x, f)
+        elif algo.startswith("winograd"):
+            O.conv2d_winograd(s, int(algo[-1]), x, f)
+        else:
+            O.conv2d_naive(s, x, f)
+        return s.flops(), time.perf_counter() - t0
+
+    def full_pass(self):
+        fl, sec = 0, 0.0
+        for inst in vgg_instances():
+            a, b = self.layer(*inst)
+            fl += a
+            sec += b
+        return fl, sec
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle as O
-    O.build()
-    for _ in range(args.warmup):
-        cpu_reference_sample(algos=["winograd_t4x4"])
-    vals = []
-    t_all = 0.0
-    for _ in range(args.steps):
-        g, s, cores, kind, detail = cpu_reference_sample(algos=["winograd_t4x4", "im2col"])
-        vals.append(g)
-        t_all += s
-    value = float(np.median(vals))
-    flops_b1 = sum(conv_flops(1, h, c, k) * m for _, h, c, k, m in VGG16)
+    ref = CpuReference()
+    insts = vgg_instances()
+    for i in range(args.warmup):
+        ref.layer(*insts[i % len(insts)])
+    fl, sec, times = 0, 0.0, []
+    for i in range(args.steps):
+        a, b = ref.layer(*insts[i % len(insts)])
+        fl += a
+        sec += b
+        times.append(b)
+    value = fl / sec / 1e9
     line = {
         "impl": "reference", "metric": "VGG16 conv-stack GFLOP/s (conv_flops / time)",
         "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(1e3 * t_all / args.steps, 3),
+        "warmup": args.warmup, "ms_per_step": round(1e3 * sec / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (fill_random, tuner.hpp:293-297)",
-        "config": {"workload": "VGG16 13 conv layers, NHWC fp32, batch 1 sample per step "
-                               "(bounded CPU sample of the batch-32 workload)",
-                   "algorithms": detail, "step_gflop": flops_b1 / 1e9},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores, "kind": kind,
-                         "sample": "13 VGG16 layers at batch 1, best of reference winograd_t4x4/im2col per layer"},
+        "config": {"workload": "VGG16 13 conv layers (3x3/s1/Same, NHWC fp32); each step one "
+                               "layer instance at batch 1, rotating through the 13 (bounded "
+                               "CPU sample of the batch-32 GPU workload)",
+                   "algorithms": REF_ALGO},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": ref.cores,
+                         "kind": ref.kind,
+                         "sample": f"{args.steps} rotating VGG16 layer instances at batch 1, "
+                                   "reference conv2d with its fastest CPU algorithm per layer"},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -208,6 +237,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1904_05347_b200 as tk
+    from paper_1904_05347_b200 import shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -276,12 +306,7 @@ def main():
             times.append(e0.elapsed_time(e1))
     launches = tk.launch_count() - launches0
     torch.cuda.synchronize()
-    total_ms = float(sum(times))
-    t = torch.tensor([total_ms], device=dev)
-    if world > 1:
-        dist.barrier()
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = shard.max_over_ranks(float(sum(times)), device=dev)
     ms_per_step = total_ms / args.steps
     value = step_flops * world / (ms_per_step * 1e-3) / 1e9
 
@@ -314,11 +339,7 @@ def main():
                                       h["f"].ctypes.data_as(ctypes.c_void_p),
                                       h["y"].ctypes.data_as(ctypes.c_void_p))
                 tk._check(rc)
-        e2e_s = (time.perf_counter() - t0) / e2e_steps
-        te = torch.tensor([e2e_s], device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_s = float(te.item())
+        e2e_s = shard.max_over_ranks((time.perf_counter() - t0) / e2e_steps, device=dev)
         e2e = {"value": round(step_flops * world / e2e_s / 1e9, 2), "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": round(e2e_s * 1e3, 3), "api": "tk_conv2d_ex (host buffers)"}
@@ -347,12 +368,62 @@ def main():
         layer_rows.append({"layer": L["name"], "ms": round(ms, 4),
                            "tflops": round(L["flops"] / (ms * 1e-3) / 1e12, 2)})
 
+    # Secondary lines (same run, same resident inputs): the other precisions
+    # of the stack and BASELINE configs[0], SGEMM 1024^3 (row-major C = A B as
+    # the column-major nn call with operands swapped).
+    secondary = {}
+    if not args.no_secondary:
+        def stack_ms(p_, reps):
+            ts = []
+            for _ in range(reps):
+                flush.zero_()
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                for L in layers:
+                    tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=p_,
+                                  workspace=None, stream=stream)
+                b_.record(stream)
+                b_.synchronize()
+                ts.append(a_.elapsed_time(b_))
+            return float(np.median(ts))
+        for p_ in [q for q in ("tf32", "bf16", "fp32") if q != prec]:
+            stack_ms(p_, 1)
+            ms = stack_ms(p_, 3 if p_ != "fp32" else 1)
+            secondary[f"vgg16_{p_}"] = {"value": round(step_flops / (ms * 1e-3) / 1e9, 1),
+                                         "unit": "GFLOP/s", "ms_per_step": round(ms, 3),
+                                         "bit_exact": p_ == "fp32"}
+        n = 1024
+        ga = torch.rand(n * n, device=dev) * 2 - 1
+        gb = torch.rand(n * n, device=dev) * 2 - 1
+        gc = torch.empty(n * n, device=dev)
+        gshape = tk.GemmShape(n, n, n)
+        for p_ in ("fp32", "tf32", "bf16"):
+            cfg = tk.parse_gemm_config("8x8_16x16_loc_db") if p_ == "fp32" else None
+            for _ in range(3):
+                tk.gemm_dev(gb, ga, None, gc, gshape, cfg, precision=p_, stream=stream)
+            ts = []
+            for _ in range(20):
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                tk.gemm_dev(gb, ga, None, gc, gshape, cfg, precision=p_, stream=stream)
+                b_.record(stream)
+                b_.synchronize()
+                ts.append(a_.elapsed_time(b_))
+            ms = float(np.median(ts))
+            secondary[f"sgemm1024_{p_}"] = {"value": round(2 * n ** 3 / (ms * 1e-3) / 1e9, 1),
+                                             "unit": "GFLOP/s", "ms": round(ms, 4),
+                                             "note": "L2-resident operands (12.6 MB)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        g, s, cores, kind, detail = cpu_reference_sample()
-        cpu = {"value": round(g, 3), "unit": "GFLOP/s", "cores": cores, "kind": kind,
-               "sample": "13 VGG16 layers at batch 1 (1/32 of a step), best of reference "
-                         "im2col/winograd_t4x4/winograd_t2x2 per layer", "seconds": round(s, 2)}
+        ref = CpuReference()
+        ref.full_pass()  # warm caches / thread pools
+        fl, sec = ref.full_pass()
+        cpu = {"value": round(fl / sec / 1e9, 3), "unit": "GFLOP/s", "cores": ref.cores,
+               "kind": ref.kind,
+               "sample": "one full VGG16 conv stack at batch 1 (1/32 of a GPU step), reference "
+                         "conv2d with its fastest CPU algorithm per layer",
+               "seconds": round(sec, 3)}
 
     if rank == 0:
         line = {
@@ -369,6 +440,7 @@ def main():
                        "l2": "flushed between steps (256 MiB write, outside events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks.summary(), "layers": layer_rows,
+            "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -1,0 +1,76 @@
+"""Multi-GPU decomposition of the tilekit hot path.
+
+The reference has no distributed code: every output element is owned by one
+logical thread and computed from its own ordered sum, so ANY disjoint
+partition of the outputs is exact.  The B200 build therefore shards with no
+data-path collective (one process per GPU, launched by torchrun):
+
+* convolution: by batch -- NHWC is batch-outermost, so rank r owns images
+  [lo, hi) as one contiguous slice of input and output.  Filters are
+  replicated once, outside any timed region.
+* GEMM (column-major C = A B): by column panels of C -- a panel needs only
+  the matching column block of B; A is replicated.  Panels are rounded to a
+  multiple of the tile width so no tile straddles two ranks.
+
+Collectives appear only in the plumbing: a barrier + MAX all-reduce of the
+device time (every multi-GPU number is the slowest rank), and an optional
+gather of the shards to rank 0 for verification.
+"""
+from __future__ import annotations
+
+from typing import List, Tuple
+
+
+def shard_range(total: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous [lo, hi) slice of `total` units owned by `rank` (the first
+    total % world ranks get one extra unit)."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    base, extra = divmod(total, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def panel_range(n: int, world: int, rank: int, align: int = 256) -> Tuple[int, int]:
+    """Column-panel slice of an n-column output, panel edges on multiples of
+    `align` (the tensor-core N tile) except at the end."""
+    blocks = (n + align - 1) // align
+    lo_b, hi_b = shard_range(blocks, world, rank)
+    return min(n, lo_b * align), min(n, hi_b * align)
+
+
+def all_shards(total: int, world: int) -> List[Tuple[int, int]]:
+    return [shard_range(total, world, r) for r in range(world)]
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """MAX of a per-rank scalar (device time) over the process group; the
+    identity without an initialised group."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_batch_shards(local, total_batch: int, dst: int = 0):
+    """Verification-only gather of per-rank batch shards (tensors of shape
+    [hi-lo, ...]) into a full batch on rank `dst` (None elsewhere)."""
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    shapes = all_shards(total_batch, world)
+    if rank == dst:
+        parts = [torch.empty((hi - lo,) + tuple(local.shape[1:]), dtype=local.dtype,
+                             device=local.device) for lo, hi in shapes]
+        parts[rank].copy_(local)
+        for r, buf in enumerate(parts):
+            if r != rank and buf.shape[0] > 0:
+                dist.recv(buf, src=r)
+        return torch.cat(parts, dim=0)
+    if local.shape[0] > 0:
+        dist.send(local.contiguous(), dst=dst)
+    return None
