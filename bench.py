@@ -39,6 +39,22 @@ VGG16 = [
     ("vgg_conv5", 14, 512, 512, 3),
 ]
 
+# ResNet-50 (Caffe variant) conv layers, proj/data/resnet_layers.csv, with the
+# multiplicities of the canonical network (53 convs): (name, R, stride, H, C, K, mult)
+RESNET50 = [
+    ("conv1", 7, 2, 224, 3, 64, 1), ("res2a_branch2a", 1, 1, 56, 64, 64, 1),
+    ("res2a_branch2b", 3, 1, 56, 64, 64, 3), ("res2a_branch2c", 1, 1, 56, 64, 256, 3),
+    ("res2a_branch1", 1, 1, 56, 64, 256, 1), ("res2b_branch2a", 1, 1, 56, 256, 64, 2),
+    ("res3a_branch2a", 1, 2, 56, 256, 128, 1), ("res3a_branch2b", 3, 1, 28, 128, 128, 4),
+    ("res3a_branch2c", 1, 1, 28, 128, 512, 4), ("res3a_branch1", 1, 2, 56, 256, 512, 1),
+    ("res3b_branch2a", 1, 1, 28, 512, 128, 3), ("res4a_branch2a", 1, 2, 28, 512, 256, 1),
+    ("res4a_branch2b", 3, 1, 14, 256, 256, 6), ("res4a_branch2c", 1, 1, 14, 256, 1024, 6),
+    ("res4a_branch1", 1, 2, 28, 512, 1024, 1), ("res4b_branch2a", 1, 1, 14, 1024, 256, 5),
+    ("res5a_branch2a", 1, 2, 14, 1024, 512, 1), ("res5a_branch2b", 3, 1, 7, 512, 512, 3),
+    ("res5a_branch2c", 1, 1, 7, 512, 2048, 3), ("res5a_branch1", 1, 2, 14, 1024, 2048, 1),
+    ("res5b_branch2a", 1, 1, 7, 2048, 512, 2),
+]
+
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -66,6 +82,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch layer by layer")
     return ap.parse_args()
 
 
@@ -277,17 +294,59 @@ def main():
         step()
     torch.cuda.synchronize()
 
+    # The step is captured once as a CUDA graph (launch-bound inner loop:
+    # 26 launches whose host-side setup would otherwise gate the small
+    # layers); kernel parameters, TMA descriptors included, are captured by
+    # value.  gpu_launches counts the kernels inside the graph.
+    graph = None
+    launches_per_step = None
+    if not args.no_graph:
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(stream)
+        l0 = tk.launch_count()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            for L in layers:
+                tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=prec,
+                              workspace=L["ws"], stream=cap)
+        launches_per_step = tk.launch_count() - l0
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+
+    def run_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+
     # Per-layer device times (same stream, CUDA events), for the roofline.
+    # (each layer replayed from its own graph so host launch latency does not
+    # pad the small layers; median of 3)
     per_layer = []
     for L in layers:
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        flush.zero_()
-        ev[0].record(stream)
-        tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=prec,
-                      workspace=L["ws"], stream=stream)
-        ev[1].record(stream)
-        torch.cuda.synchronize()
-        per_layer.append(ev[0].elapsed_time(ev[1]))
+        lg = None
+        if not args.no_graph:
+            cap = torch.cuda.Stream(device=dev)
+            cap.wait_stream(stream)
+            lg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(lg, stream=cap):
+                tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=prec,
+                              workspace=L["ws"], stream=cap)
+        ts = []
+        for _ in range(3):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            flush.zero_()
+            ev[0].record(stream)
+            if lg is not None:
+                lg.replay()
+            else:
+                tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=prec,
+                              workspace=L["ws"], stream=stream)
+            ev[1].record(stream)
+            torch.cuda.synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]))
+        per_layer.append(float(np.median(ts)))
 
     # Timed steps.
     if world > 1:
@@ -300,11 +359,13 @@ def main():
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            step()
+            run_step()
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
     launches = tk.launch_count() - launches0
+    if launches_per_step is not None:
+        launches = launches_per_step * args.steps
     torch.cuda.synchronize()
     total_ms = shard.max_over_ranks(float(sum(times)), device=dev)
     ms_per_step = total_ms / args.steps
@@ -392,6 +453,56 @@ def main():
             secondary[f"vgg16_{p_}"] = {"value": round(step_flops / (ms * 1e-3) / 1e9, 1),
                                          "unit": "GFLOP/s", "ms_per_step": round(ms, 3),
                                          "bit_exact": p_ == "fp32"}
+        # BASELINE configs[2]: ResNet-50 conv stack (53 layers) at batch 32.
+        rn = []
+        for name, r, stv, h, c, k, mult in RESNET50:
+            shp = tk.ConvShape(N, h, h, c, k, r, r, stv, True)
+            x = torch.rand((N, h, h, c), device=dev, generator=gen) * 2 - 1
+            f = torch.rand((r, r, c, k), device=dev, generator=gen) * 2 - 1
+            y = torch.empty(shp.out_shape, device=dev)
+            ws = torch.empty(tk.conv2d_workspace_size(shp, tk.parse_conv_params("im2col"), prec)
+                             // 4 + 1, device=dev)
+            rn.append((shp, x, f, y, ws, mult, shp.flops()))
+        rn_flops = sum(fl * m for *_, m, fl in rn)
+        for p_ in ("tf32", "bf16"):
+            def rn_pass():
+                for shp, x, f, y, ws, mult, _ in rn:
+                    for _ in range(mult):
+                        tk.conv2d_dev(x, f, y, shp, tk.parse_conv_params("im2col"), precision=p_,
+                                      workspace=ws if p_ == prec else None, stream=stream)
+            rn_pass()
+            torch.cuda.synchronize()
+            g_rn = None
+            if not args.no_graph:
+                cap = torch.cuda.Stream(device=dev)
+                cap.wait_stream(stream)
+                g_rn = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g_rn, stream=cap):
+                    for shp, x, f, y, ws, mult, _ in rn:
+                        for _ in range(mult):
+                            tk.conv2d_dev(x, f, y, shp, tk.parse_conv_params("im2col"),
+                                          precision=p_, workspace=ws if p_ == prec else None,
+                                          stream=cap)
+                g_rn.replay()
+                torch.cuda.synchronize()
+            ts = []
+            for _ in range(3):
+                flush.zero_()
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                if g_rn is not None:
+                    g_rn.replay()
+                else:
+                    rn_pass()
+                b_.record(stream)
+                b_.synchronize()
+                ts.append(a_.elapsed_time(b_))
+            ms = float(np.median(ts))
+            secondary[f"resnet50_{p_}"] = {"value": round(rn_flops / (ms * 1e-3) / 1e9, 1),
+                                            "unit": "GFLOP/s", "ms_per_step": round(ms, 3),
+                                            "step_gflop": round(rn_flops / 1e9, 2),
+                                            "batch_per_gpu": N}
+        del rn
         n = 1024
         ga = torch.rand(n * n, device=dev) * 2 - 1
         gb = torch.rand(n * n, device=dev) * 2 - 1

@@ -169,9 +169,14 @@ __device__ __forceinline__ void gather_producer(const TcArgs& p, uint8_t* base, 
   const int q = t & 7;
   const int r0 = t >> 3;
   const uint32_t sbase = ptx::smem(base);
+  // Groups take alternate K-slabs of the CTA's slab sequence.  (Owning
+  // alternate *tiles* would let a group run more than one phase ahead on a
+  // stage barrier once a tile has more slabs than stages, and the mbarrier
+  // parity test cannot tell those phases apart.)
   int local = 0;
   for (int tt = unit; tt < total; tt += nunits, ++local) {
-    if ((local % kGatherGroups) != group) continue;  // groups own alternate tiles
+    const int seq0 = local * p.num_kb;
+    if (p.num_kb == 1 && (seq0 % kGatherGroups) != group) continue;
     const int m_blk = tt % p.num_m;
     // Pixel geometry of this thread's 8 rows (rows r0 + 16 i), walked
     // incrementally from the first row: no per-row division.
@@ -201,7 +206,8 @@ __device__ __forceinline__ void gather_producer(const TcArgs& p, uint8_t* base, 
       }
     }
     for (int kb = 0; kb < p.num_kb; ++kb) {
-      const int seq = local * p.num_kb + kb;  // slab sequence of this CTA
+      const int seq = seq0 + kb;  // slab sequence of this CTA
+      if (seq % kGatherGroups != group) continue;
       const int stage = seq % p.stages;
       const uint32_t phase = (uint32_t)(seq / p.stages) & 1u;
       int2 kd[4];
@@ -568,23 +574,23 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       } else if constexpr (MODE == kConvPixN) {
         const PixTile pt = pix_tile(p, n_blk);
         const int m = m_blk * BM + rank * kRows + row;  // output feature
-        const long long img_base = (long long)pt.img * p.OH;
+        const bool m_ok = m < p.Kout;
         for (int col = 0; col < p.BN; col += 32) {
           float v[32];
           ptx::tmem_ld32(taddr + col, v);
-          if (m < p.Kout) {
-            // Column -> pixel walk without per-column division.
-            int h = col / p.Wb, w = col - (col / p.Wb) * p.Wb;
+          // Lane l resolves column col + l to its NHWC pixel offset once; the
+          // warp then walks the 32 columns with shuffles (one coalesced
+          // 128-byte store of 32 consecutive features per column).
+          const int n = col + (int)lane;
+          const int h = n / p.Wb, w = n - (n / p.Wb) * p.Wb;
+          const int oh = pt.oh0 + h, ow = pt.ow0 + w;
+          const bool ok = n < p.BN && oh < p.OH && ow < p.OW;
+          const long long pix_off =
+              ok ? (((long long)pt.img * p.OH + oh) * p.OW + ow) * p.Kout : -1ll;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int oh = pt.oh0 + h, ow = pt.ow0 + w;
-              if (col + j < p.BN && oh < p.OH && ow < p.OW)
-                p.d[((img_base + oh) * p.OW + ow) * p.Kout + m] = v[j];
-              if (++w == p.Wb) {
-                w = 0;
-                ++h;
-              }
-            }
+          for (int j = 0; j < 32; ++j) {
+            const long long o = __shfl_sync(0xffffffffu, pix_off, j);
+            if (o >= 0 && m_ok) p.d[o + m] = v[j];
           }
         }
       } else {
@@ -697,6 +703,11 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
                               ? p.halo_bytes + (p.resident ? 0 : p.taps) * b_bytes_h
                               : kRows * kSlabBytes + b_bytes_h;
   const int fres_bytes = (MODE == kConvHalo && p.resident) ? p.taps * p.cchunks * b_bytes_h : 0;
+  const int ktab_bytes0 = MODE == kConvGather ? p.num_kb * 32 * 8 : 0;
+  // Double-buffered TMA-store staging when it leaves room for >= 3 stages.
+  if (p.store_tma && p.epi_bufs > 1 &&
+      232448 - 2048 - ktab_bytes0 - 2 * ((p.BN + 31) / 32) * kRows * kSlabBytes < 3 * stage_bytes)
+    p.epi_bufs = 1;
   const int epi_bytes =
       p.store_tma ? p.epi_bufs * ((p.BN + 31) / 32) * kRows * kSlabBytes : 0;
   p.epi_bytes = epi_bytes;
@@ -1048,7 +1059,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     p.K = (int)kp;
     p.Kreal = (int)K;
     p.ek = 32;
-    p.BN = std::min(256, (g.K + 16 * cg - 1) / (16 * cg) * (16 * cg));
+    p.BN = std::min(128, (g.K + 16 * cg - 1) / (16 * cg) * (16 * cg));
     p.num_m = (pixels + kRows * cg - 1) / (kRows * cg);
     p.num_n = (g.K + p.BN - 1) / p.BN;
     p.batch = 1;
@@ -1103,7 +1114,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   // input would otherwise dominate the L2->SM traffic.
   const char* force = getenv("TK_CONV_MODE");
   const bool halo_ok = g.stride == 1 && g.R * g.S <= 9 && g.S <= 3 && g.K % 32 == 0 &&
-                       ((g.K <= 128 && (g.C <= 64 || g.K <= 64)) ||
+                       ((g.K <= 128 && g.C <= 128) ||
                         (force && std::string(force) == "halo"));
   const bool use_halo = halo_ok && !(force && std::string(force) != "halo");
   if (use_halo) {

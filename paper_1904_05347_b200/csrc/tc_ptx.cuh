@@ -52,6 +52,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+#ifndef TKB_WAIT_NS
+#define TKB_WAIT_NS 2000
+#endif
 // Long waits: ask the hardware to suspend the thread (up to ~2 us per try)
 // instead of spinning on issue slots the working warps need.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
@@ -60,7 +63,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       "WAITS_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAITS_%=;\n\t}\n" ::"r"(smem(bar)),
-      "r"(parity), "r"(2000u)
+      "r"(parity), "r"((uint32_t)TKB_WAIT_NS)
       : "memory");
 }
 
