@@ -429,6 +429,7 @@ def main():
         layer_rows.append({"layer": L["name"], "ms": round(ms, 4),
                            "tflops": round(L["flops"] / (ms * 1e-3) / 1e12, 2)})
 
+    peaks, peaks_kind = load_peaks()
     # Secondary lines (same run, same resident inputs): the other precisions
     # of the stack and BASELINE configs[0], SGEMM 1024^3 (row-major C = A B as
     # the column-major nn call with operands swapped).
@@ -503,6 +504,30 @@ def main():
                                             "step_gflop": round(rn_flops / 1e9, 2),
                                             "batch_per_gpu": N}
         del rn
+        # BASELINE configs[3]: large square GEMMs on the tensor cores
+        # (column-major nn through tk_gemm_dev; operands in HBM, > L2 from 4096).
+        for n in (2048, 4096, 8192):
+            ga = torch.rand(n * n, device=dev) * 2 - 1
+            gb = torch.rand(n * n, device=dev) * 2 - 1
+            gc = torch.empty(n * n, device=dev)
+            gshape = tk.GemmShape(n, n, n)
+            for p_ in ("tf32", "bf16"):
+                for _ in range(2):
+                    tk.gemm_dev(ga, gb, None, gc, gshape, None, precision=p_, stream=stream)
+                ts = []
+                for _ in range(5):
+                    a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a_.record(stream)
+                    tk.gemm_dev(ga, gb, None, gc, gshape, None, precision=p_, stream=stream)
+                    b_.record(stream)
+                    b_.synchronize()
+                    ts.append(a_.elapsed_time(b_))
+                ms = float(np.median(ts))
+                tf = 2 * n ** 3 / (ms * 1e-3) / 1e12
+                pk = peaks["bf16_tflops"] / (2.0 if p_ == "tf32" else 1.0)
+                secondary[f"gemm{n}_{p_}"] = {"value": round(tf * 1e3, 1), "unit": "GFLOP/s",
+                                              "ms": round(ms, 4), "frac_of_peak": round(tf / pk, 4)}
+            del ga, gb, gc
         n = 1024
         ga = torch.rand(n * n, device=dev) * 2 - 1
         gb = torch.rand(n * n, device=dev) * 2 - 1

@@ -8,6 +8,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <string>
 
 #include "tilekit/config.hpp"
 #include "tilekit/device.hpp"
@@ -37,6 +38,16 @@ struct ExecOptions {
     return o;
   }
 };
+
+inline std::string precision_name(Precision p) {
+  switch (p) {
+    case Precision::Fp32Exact: return "fp32";
+    case Precision::Tf32: return "tf32";
+    case Precision::Bf16: return "bf16";
+    case Precision::Tf32x3: return "3xtf32";
+  }
+  return "unknown";
+}
 
 // Number of usable B200 (sm_100) devices.
 inline int device_count() { return tk_device_count(); }

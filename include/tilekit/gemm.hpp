@@ -179,4 +179,20 @@ inline std::uint64_t gemm_batched_strided(const float* a, std::size_t stride_a, 
   return count;
 }
 
+namespace b200 {
+
+// gemm with B200 execution options (precision, tensor-core tile) on host
+// matrices; same operand conventions and checks as gemm_naive.
+inline Matrix gemm(const Matrix& a, const Matrix& b, const Matrix& c, const GemmShape& shape,
+                   const ExecOptions& opts) {
+  tilekit::detail::check_gemm_operands(a, b, c, shape);
+  Matrix out(shape.m, shape.n);
+  const tk_gemm_shape s = tilekit::detail::to_c(shape);
+  const tk_exec_options o = opts.c();
+  tilekit::detail::check_status(
+      tk_gemm_ex(&s, &o, a.data.data(), b.data.data(), c.data.data(), out.data.data()));
+  return out;
+}
+
+}  // namespace b200
 }  // namespace tilekit

@@ -160,6 +160,9 @@ TK_API int tk_gemm_batched_strided(const float* a, size_t stride_a, const float*
 TK_API int tk_gemm_dev(const tk_gemm_shape* shape, const tk_gemm_config* cfg,
                 const tk_exec_options* opts, const float* d_a, const float* d_b,
                 const float* d_c, float* d_out, void* stream);
+/* gemm with B200 execution options on HOST buffers (precision etc.). */
+TK_API int tk_gemm_ex(const tk_gemm_shape* shape, const tk_exec_options* opts, const float* a,
+                      const float* b, const float* c, float* out);
 TK_API int tk_gemm_batched_strided_dev(const float* d_a, size_t stride_a,
                                 const float* d_b, size_t stride_b, float* d_c,
                                 size_t stride_c, size_t batch, size_t m,
@@ -205,6 +208,19 @@ TK_API int tk_conv2d_ex(const tk_conv_shape* shape, const tk_conv_params* params
                  const float* filt, float* out);
 TK_API int tk_im2col_dev(const tk_conv_shape* shape, const float* d_in,
                   float* d_patches, void* stream);
+
+/* ---- benchmarking (the tuner's device clock) --------------------------- */
+/* Upload the given HOST inputs once, run `warmup` untimed and `samples`
+ * timed launches of the device path (CUDA events on a private stream) and
+ * write each sample's duration in nanoseconds to ns[samples].  cfg may be
+ * NULL (library default); opts may be NULL (exact FP32).  c may be NULL
+ * when beta == 0.  Used by tilekit::benchmark_config (tuner.hpp). */
+TK_API int tk_bench_gemm(const tk_gemm_shape* shape, const tk_gemm_config* cfg,
+                         const tk_exec_options* opts, const float* a, const float* b,
+                         const float* c, int warmup, int samples, int64_t* ns);
+TK_API int tk_bench_conv2d(const tk_conv_shape* shape, const tk_conv_params* params,
+                           const tk_exec_options* opts, const float* in, const float* filt,
+                           int warmup, int samples, int64_t* ns);
 
 #ifdef __cplusplus
 }

@@ -117,6 +117,7 @@ EXPORTS = [
     "tk_gemm_batched_strided_dev", "tk_conv2d", "tk_conv2d_naive", "tk_conv2d_tiled",
     "tk_conv2d_im2col", "tk_conv2d_winograd", "tk_im2col", "tk_filter_matrix",
     "tk_conv2d_dev", "tk_conv2d_workspace_size", "tk_conv2d_ex", "tk_im2col_dev",
+    "tk_bench_gemm", "tk_bench_conv2d", "tk_gemm_ex",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -169,6 +170,12 @@ def lib() -> C.CDLL:
                           C.POINTER(ExecOptionsC), _vp, _vp, _vp, _vp, C.c_size_t, _vp],
         "tk_conv2d_workspace_size": [C.POINTER(ConvShapeC), C.POINTER(ConvParamsC),
                                      C.POINTER(ExecOptionsC), C.POINTER(C.c_size_t)],
+        "tk_gemm_ex": [C.POINTER(GemmShapeC), C.POINTER(ExecOptionsC), _vp, _vp, _vp, _vp],
+        "tk_bench_gemm": [C.POINTER(GemmShapeC), C.POINTER(GemmConfigC), C.POINTER(ExecOptionsC),
+                          _vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(C.c_int64)],
+        "tk_bench_conv2d": [C.POINTER(ConvShapeC), C.POINTER(ConvParamsC),
+                            C.POINTER(ExecOptionsC), _vp, _vp, C.c_int, C.c_int,
+                            C.POINTER(C.c_int64)],
     }
     for name, args in sig.items():
         getattr(L, name).argtypes = args

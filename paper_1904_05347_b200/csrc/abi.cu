@@ -490,6 +490,42 @@ void note_launch(int n) { g_launches += (uint64_t)n; }
 
 }  // namespace tkb
 
+
+namespace tkb {
+namespace {
+
+struct EventTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  EventTimer() {
+    TKB_CUDA(cudaEventCreate(&a));
+    TKB_CUDA(cudaEventCreate(&b));
+  }
+  ~EventTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+template <typename Run>
+void time_samples(Run&& run, int warmup, int samples, int64_t* ns, cudaStream_t st) {
+  if (samples < 1 || !ns) fail(TK_ERR_CONTRACT, "bench: samples must be >= 1 with an output array");
+  for (int i = 0; i < warmup; ++i) run();
+  TKB_CUDA(cudaStreamSynchronize(st));
+  EventTimer t;
+  for (int i = 0; i < samples; ++i) {
+    TKB_CUDA(cudaEventRecord(t.a, st));
+    run();
+    TKB_CUDA(cudaEventRecord(t.b, st));
+    TKB_CUDA(cudaEventSynchronize(t.b));
+    float ms = 0.0f;
+    TKB_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
+    ns[i] = (int64_t)((double)ms * 1.0e6);
+  }
+}
+
+}  // namespace
+}  // namespace tkb
+
 using namespace tkb;
 
 extern "C" {
@@ -598,6 +634,29 @@ int tk_gemm_dev(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const tk_
                               g.op_b == tilekit::Op::Transpose, d_a, d_b, d_c, d_out, prec,
                               opts ? opts->tc_tile_n : 0, st);
     }
+  });
+}
+
+int tk_gemm_ex(const tk_gemm_shape* shape, const tk_exec_options* opts, const float* a,
+               const float* b, const float* c, float* out) {
+  return guarded([&] {
+    const tilekit::GemmShape g = gemm_shape(shape);
+    cudaStream_t st = host_stream();
+    const size_t na = g.m * g.k, nb = g.k * g.n, nc = g.m * g.n;
+    const bool read_c = g.beta != 0.0f;
+    DevBuf da(4 * na, st), db(4 * nb, st), dc(read_c ? 4 * nc : 0, st), dd(4 * nc, st);
+    h2d(da.p, a, 4 * na, st);
+    h2d(db.p, b, 4 * nb, st);
+    if (read_c) h2d(dc.p, c, 4 * nc, st);
+    const int prec = precision_of(opts);
+    if (prec == TK_PREC_FP32_EXACT)
+      launch_exact(gemm_args(g, da.f(), db.f(), dc.f(), dd.f()), kExactDefault, false, 1, st);
+    else
+      launch_tc_colmajor_gemm(g.m, g.n, g.k, g.alpha, g.beta, g.op_a == tilekit::Op::Transpose,
+                              g.op_b == tilekit::Op::Transpose, da.f(), db.f(), dc.f(), dd.f(),
+                              prec, opts ? opts->tc_tile_n : 0, st);
+    d2h(out, dd.p, 4 * nc, st);
+    finish(st);
   });
 }
 
@@ -817,6 +876,53 @@ int tk_conv2d_dev(const tk_conv_shape* shape, const tk_conv_params* params,
     } else {
       conv_dev(s, params, prec, d_in, d_filt, d_out, d_ws, st);
     }
+  });
+}
+
+int tk_bench_gemm(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const tk_exec_options* opts,
+                  const float* a, const float* b, const float* c, int warmup, int samples,
+                  int64_t* ns) {
+  return guarded([&] {
+    const tilekit::GemmShape g = gemm_shape(shape);
+    cudaStream_t st = host_stream();
+    const size_t na = g.m * g.k, nb = g.k * g.n, nc = g.m * g.n;
+    const bool read_c = g.beta != 0.0f;
+    DevBuf da(4 * na, st), db(4 * nb, st), dc(read_c ? 4 * nc : 0, st), dd(4 * nc, st);
+    h2d(da.p, a, 4 * na, st);
+    h2d(db.p, b, 4 * nb, st);
+    if (read_c) h2d(dc.p, c, 4 * nc, st);
+    const int prec = precision_of(opts);
+    const ExactLaunch L = cfg ? exact_launch_of(gemm_config(cfg)) : kExactDefault;
+    auto run = [&] {
+      if (prec == TK_PREC_FP32_EXACT) {
+        launch_exact(gemm_args(g, da.f(), db.f(), dc.f(), dd.f()), L, false, 1, st);
+      } else {
+        launch_tc_colmajor_gemm(g.m, g.n, g.k, g.alpha, g.beta, g.op_a == tilekit::Op::Transpose,
+                                g.op_b == tilekit::Op::Transpose, da.f(), db.f(), dc.f(), dd.f(),
+                                prec, opts ? opts->tc_tile_n : 0, st);
+      }
+    };
+    time_samples(run, warmup, samples, ns, st);
+  });
+}
+
+int tk_bench_conv2d(const tk_conv_shape* shape, const tk_conv_params* params,
+                    const tk_exec_options* opts, const float* in, const float* filt, int warmup,
+                    int samples, int64_t* ns) {
+  return guarded([&] {
+    if (!params) fail(TK_ERR_CONTRACT, "bench: params must not be NULL");
+    const tilekit::ConvShape s = conv_shape(shape);
+    const ConvGeom g = conv_geom(s);
+    if (params->algo == 1) check_tiled_params(s, params);
+    if (params->algo == 3) check_winograd(s, params);
+    const int prec = precision_of(opts);
+    cudaStream_t st = host_stream();
+    DevBuf din(4 * in_elems(g), st), dfl(4 * filt_elems(g), st), dout(4 * out_elems(g), st);
+    DevBuf ws(conv_workspace(g, params, prec), st);
+    h2d(din.p, in, 4 * in_elems(g), st);
+    h2d(dfl.p, filt, 4 * filt_elems(g), st);
+    auto run = [&] { conv_dev(s, params, prec, din.f(), dfl.f(), dout.f(), ws.p, st); };
+    time_samples(run, warmup, samples, ns, st);
   });
 }
 

@@ -1098,7 +1098,8 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   const void* xin = in;
   if (tf32) {
     float* ft = reinterpret_cast<float*>(cursor);
-    pack_kmajor<float>(filt, 1, g.K, g.K, K, kp, ft, true, st);
+    const char* rnd = getenv("TK_TF32_ROUND");
+    pack_kmajor<float>(filt, 1, g.K, g.K, K, kp, ft, !(rnd && rnd[0] == '0'), st);
     fa = ft;
   } else {
     __nv_bfloat16* ft = reinterpret_cast<__nv_bfloat16*>(cursor);

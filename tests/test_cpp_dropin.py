@@ -9,24 +9,29 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIBDIR = os.path.join(ROOT, "paper_1904_05347_b200")
-BIN = os.path.join(ROOT, "tests", "cpp", "test_dropin")
 
 
-def build():
-    src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
-    if not os.path.exists(BIN) or os.path.getmtime(BIN) < os.path.getmtime(src):
+def build(name):
+    src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
+    exe = os.path.join(ROOT, "tests", "cpp", name)
+    if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
         subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-I", os.path.join(ROOT, "include"),
-                        src, "-o", BIN, "-L", LIBDIR, "-ltilekit_b200",
+                        src, "-o", exe, "-L", LIBDIR, "-ltilekit_b200",
                         f"-Wl,-rpath,{LIBDIR}"], check=True)
-    return BIN
+    return exe
 
 
-def test_dropin_compiles_and_host_logic():
-    r = subprocess.run([build(), "cpu"], capture_output=True, text=True, timeout=120)
+@pytest.mark.parametrize("name", ["test_dropin", "test_tuner"])
+def test_cpp_host_logic(name, tmp_path):
+    r = subprocess.run([build(name), "cpu"], capture_output=True, text=True, timeout=120,
+                       cwd=tmp_path)
     assert r.returncode == 0, r.stdout + r.stderr
 
 
 @pytest.mark.gpu
-def test_dropin_gpu():
-    r = subprocess.run([build(), "gpu"], capture_output=True, text=True, timeout=600)
+@pytest.mark.parametrize("name", ["test_dropin", "test_tuner"])
+def test_cpp_gpu(name, tmp_path):
+    r = subprocess.run([build(name), "gpu"], capture_output=True, text=True, timeout=900,
+                       cwd=tmp_path)
+    print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
