@@ -305,10 +305,25 @@ def main():
         cap.wait_stream(stream)
         l0 = tk.launch_count()
         graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=dev)
         with torch.cuda.graph(graph, stream=cap):
-            for L in layers:
-                tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=prec,
-                              workspace=L["ws"], stream=cap)
+            # Filter-side work (prepare: tensor-core filter repack) depends only
+            # on the filters: fork it to a side stream so it overlaps earlier
+            # layers; each layer's run joins on its own prepare.
+            side.wait_stream(cap)
+            ready = []
+            with torch.cuda.stream(side):
+                for L in layers:
+                    tk.conv2d_prepare_dev(L["f"], L["shape"], L["algo"], L["ws"], precision=prec,
+                                          stream=side)
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    ready.append(ev)
+            for L, ev in zip(layers, ready):
+                cap.wait_event(ev)
+                tk.conv2d_run_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], L["ws"],
+                                  precision=prec, stream=cap)
+            cap.wait_stream(side)
         launches_per_step = tk.launch_count() - l0
         for _ in range(2):
             graph.replay()

@@ -206,6 +206,18 @@ TK_API int tk_conv2d_workspace_size(const tk_conv_shape* shape,
 TK_API int tk_conv2d_ex(const tk_conv_shape* shape, const tk_conv_params* params,
                  const tk_exec_options* opts, const float* in,
                  const float* filt, float* out);
+/* The same convolution in two phases on caller-provided workspace:
+ * prepare = the filter-side work (tensor-core filter repack, Winograd filter
+ * transform) -- it reads only d_filt, so it may run on another stream and
+ * overlap earlier work; run = everything that reads the input, ordered after
+ * prepare on the same workspace. */
+TK_API int tk_conv2d_prepare_dev(const tk_conv_shape* shape, const tk_conv_params* params,
+                                 const tk_exec_options* opts, const float* d_filt,
+                                 void* d_workspace, size_t workspace_bytes, void* stream);
+TK_API int tk_conv2d_run_dev(const tk_conv_shape* shape, const tk_conv_params* params,
+                             const tk_exec_options* opts, const float* d_in, const float* d_filt,
+                             float* d_out, void* d_workspace, size_t workspace_bytes,
+                             void* stream);
 TK_API int tk_im2col_dev(const tk_conv_shape* shape, const float* d_in,
                   float* d_patches, void* stream);
 

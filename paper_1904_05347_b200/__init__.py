@@ -117,7 +117,8 @@ EXPORTS = [
     "tk_gemm_batched_strided_dev", "tk_conv2d", "tk_conv2d_naive", "tk_conv2d_tiled",
     "tk_conv2d_im2col", "tk_conv2d_winograd", "tk_im2col", "tk_filter_matrix",
     "tk_conv2d_dev", "tk_conv2d_workspace_size", "tk_conv2d_ex", "tk_im2col_dev",
-    "tk_bench_gemm", "tk_bench_conv2d", "tk_gemm_ex",
+    "tk_bench_gemm", "tk_bench_conv2d", "tk_gemm_ex", "tk_conv2d_prepare_dev",
+    "tk_conv2d_run_dev",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -170,6 +171,10 @@ def lib() -> C.CDLL:
                           C.POINTER(ExecOptionsC), _vp, _vp, _vp, _vp, C.c_size_t, _vp],
         "tk_conv2d_workspace_size": [C.POINTER(ConvShapeC), C.POINTER(ConvParamsC),
                                      C.POINTER(ExecOptionsC), C.POINTER(C.c_size_t)],
+        "tk_conv2d_prepare_dev": [C.POINTER(ConvShapeC), C.POINTER(ConvParamsC),
+                                  C.POINTER(ExecOptionsC), _vp, _vp, C.c_size_t, _vp],
+        "tk_conv2d_run_dev": [C.POINTER(ConvShapeC), C.POINTER(ConvParamsC),
+                              C.POINTER(ExecOptionsC), _vp, _vp, _vp, _vp, C.c_size_t, _vp],
         "tk_gemm_ex": [C.POINTER(GemmShapeC), C.POINTER(ExecOptionsC), _vp, _vp, _vp, _vp],
         "tk_bench_gemm": [C.POINTER(GemmShapeC), C.POINTER(GemmConfigC), C.POINTER(ExecOptionsC),
                           _vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(C.c_int64)],
@@ -516,6 +521,24 @@ def conv2d_dev(inp, filt, out, shape: ConvShape, params: ConvAlgoParams, precisi
     _check(lib().tk_conv2d_dev(C.byref(shape.c()), C.byref(params.c()),
                                C.byref(exec_options(precision, tile_n)), _dptr(inp), _dptr(filt),
                                _dptr(out), _dptr(workspace), ws_bytes, _stream(stream)))
+
+
+def conv2d_prepare_dev(filt, shape: ConvShape, params: ConvAlgoParams, workspace,
+                       precision="fp32", stream=None) -> None:
+    """Filter-side phase of conv2d_dev (may run on its own stream)."""
+    ws_bytes = workspace.numel() * workspace.element_size()
+    _check(lib().tk_conv2d_prepare_dev(C.byref(shape.c()), C.byref(params.c()),
+                                       C.byref(exec_options(precision)), _dptr(filt),
+                                       _dptr(workspace), ws_bytes, _stream(stream)))
+
+
+def conv2d_run_dev(inp, filt, out, shape: ConvShape, params: ConvAlgoParams, workspace,
+                   precision="fp32", stream=None) -> None:
+    """Input-side phase of conv2d_dev; ordered after conv2d_prepare_dev."""
+    ws_bytes = workspace.numel() * workspace.element_size()
+    _check(lib().tk_conv2d_run_dev(C.byref(shape.c()), C.byref(params.c()),
+                                   C.byref(exec_options(precision)), _dptr(inp), _dptr(filt),
+                                   _dptr(out), _dptr(workspace), ws_bytes, _stream(stream)))
 
 
 def conv2d_workspace_size(shape: ConvShape, params: ConvAlgoParams, precision="fp32") -> int:

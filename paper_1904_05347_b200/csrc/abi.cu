@@ -368,7 +368,7 @@ float* carve(char*& cursor, size_t elems) {
 
 // Device-side Winograd: transforms + batched GEMM on caller buffers.
 void winograd_dev(const ConvGeom& g, int m, int precision, const float* in, const float* filt,
-                  float* out, void* ws, cudaStream_t st) {
+                  float* out, void* ws, cudaStream_t st, int phase = kConvAll) {
   const WinoGeom w = wino_geom(g, m);
   const WinoSizes sz = wino_sizes(w);
   char* cur = static_cast<char*>(ws);
@@ -377,8 +377,10 @@ void winograd_dev(const ConvGeom& g, int m, int precision, const float* in, cons
   float* prod = carve(cur, sz.p);
   // TMA needs 16-byte row strides; odd channel counts keep the exact GEMM.
   const bool tc = precision != TK_PREC_FP32_EXACT && w.C % 4 == 0;
+  // The filter transform depends only on the filter: the prepare phase.
+  if (phase & kConvPrepare) wino_filter_transform(w, filt, u, /*k_major=*/tc, st);
+  if (!(phase & kConvRun)) return;
   wino_input_transform(w, in, v, st);
-  wino_filter_transform(w, filt, u, /*k_major=*/tc, st);
   const int spots = w.t * w.t;
   if (!tc) {
     ExactArgs p{};
@@ -433,32 +435,35 @@ size_t conv_workspace(const ConvGeom& g, const tk_conv_params* p, int precision)
 
 // Dispatch of the conv2d selector on device buffers.
 void conv_dev(const tilekit::ConvShape& s, const tk_conv_params* p, int precision,
-              const float* in, const float* filt, float* out, void* ws, cudaStream_t st) {
+              const float* in, const float* filt, float* out, void* ws, cudaStream_t st,
+              int phase = kConvAll) {
   const ConvGeom g = conv_geom(s);
+  // Exact FP32 paths read the filter directly: nothing to prepare.
+  const bool exact_run = (phase & kConvRun) != 0;
   switch (p->algo) {
     case 0:  // Naive: the oracle's arithmetic
       if (precision == TK_PREC_FP32_EXACT) {
-        launch_exact(conv_args(g, in, filt, out), kExactDefault, true, 1, st);
+        if (exact_run) launch_exact(conv_args(g, in, filt, out), kExactDefault, true, 1, st);
         return;
       }
       break;
     case 1:  // Tiled
       check_tiled_params(s, p);
       if (precision == TK_PREC_FP32_EXACT) {
-        launch_exact(conv_args(g, in, filt, out), tiled_launch(p), true, 1, st);
+        if (exact_run) launch_exact(conv_args(g, in, filt, out), tiled_launch(p), true, 1, st);
         return;
       }
       break;
     case 2:  // Im2col: implicit GEMM (tensor cores when a TC precision is set)
       if (precision == TK_PREC_FP32_EXACT) {
-        launch_exact(conv_args(g, in, filt, out), kExactDefault, true, 1, st);
+        if (exact_run) launch_exact(conv_args(g, in, filt, out), kExactDefault, true, 1, st);
       } else {
-        launch_tc_conv(g, in, filt, out, precision, ws, st);
+        launch_tc_conv(g, in, filt, out, precision, ws, st, phase);
       }
       return;
     case 3: {
       const int m = check_winograd(s, p);
-      winograd_dev(g, m, precision, in, filt, out, ws, st);
+      winograd_dev(g, m, precision, in, filt, out, ws, st, phase);
       return;
     }
     default:
@@ -877,6 +882,41 @@ int tk_conv2d_dev(const tk_conv_shape* shape, const tk_conv_params* params,
       conv_dev(s, params, prec, d_in, d_filt, d_out, d_ws, st);
     }
   });
+}
+
+// Two-phase device convolution: prepare (filter-side work into the
+// workspace) then run.  The phases may go to different streams as long as
+// run is ordered after prepare on the same workspace.
+static int conv_phase_dev(const tk_conv_shape* shape, const tk_conv_params* params,
+                          const tk_exec_options* opts, const float* d_in, const float* d_filt,
+                          float* d_out, void* d_ws, size_t ws_bytes, void* stream, int phase) {
+  return guarded([&] {
+    require_gpu();
+    if (!params) fail(TK_ERR_CONTRACT, "conv2d: params must not be NULL");
+    const tilekit::ConvShape s = conv_shape(shape);
+    const int prec = precision_of(opts);
+    if (params->algo == 3) check_winograd(s, params);
+    if (params->algo == 1) check_tiled_params(s, params);
+    const size_t need = conv_workspace(conv_geom(s), params, prec);
+    if (need && (!d_ws || ws_bytes < need))
+      fail(TK_ERR_CONTRACT, "conv2d prepare/run: a workspace of " + std::to_string(need) +
+                                " bytes is required (tk_conv2d_workspace_size)");
+    conv_dev(s, params, prec, d_in, d_filt, d_out, d_ws, static_cast<cudaStream_t>(stream), phase);
+  });
+}
+
+int tk_conv2d_prepare_dev(const tk_conv_shape* shape, const tk_conv_params* params,
+                          const tk_exec_options* opts, const float* d_filt, void* d_ws,
+                          size_t ws_bytes, void* stream) {
+  return conv_phase_dev(shape, params, opts, nullptr, d_filt, nullptr, d_ws, ws_bytes, stream,
+                        kConvPrepare);
+}
+
+int tk_conv2d_run_dev(const tk_conv_shape* shape, const tk_conv_params* params,
+                      const tk_exec_options* opts, const float* d_in, const float* d_filt,
+                      float* d_out, void* d_ws, size_t ws_bytes, void* stream) {
+  return conv_phase_dev(shape, params, opts, d_in, d_filt, d_out, d_ws, ws_bytes, stream,
+                        kConvRun);
 }
 
 int tk_bench_gemm(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const tk_exec_options* opts,

@@ -819,6 +819,65 @@ void pack_kmajor(const float* src, long long rs, long long ks, long long rows, l
   TKB_CUDA(cudaGetLastError());
 }
 
+// HWCK filter [K][Kout] -> K-major [Kout][kp] (zero padded, TF32-rounded
+// or converted to bf16) without shared memory: each thread moves a 4 x 4
+// block through registers, so the kernel can co-reside with a running
+// tensor-core kernel (whose CTAs own the shared memory) when it is issued on
+// a side stream.
+template <typename T>
+__global__ void __launch_bounds__(256) pack_filter_kernel(const float* __restrict__ src,
+                                                          int K, int Kout, int kp,
+                                                          T* __restrict__ dst, int tf32_round) {
+  const int f4n = (Kout + 3) / 4, k4n = kp / 4;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)f4n * k4n) return;
+  const int f0 = (int)(idx % f4n) * 4, k0 = (int)(idx / f4n) * 4;
+  float v[4][4];  // v[k][f]
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = k0 + i;
+    if (k < K && f0 + 3 < Kout && (Kout & 3) == 0) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(src + (long long)k * Kout + f0));
+      v[i][0] = x.x;
+      v[i][1] = x.y;
+      v[i][2] = x.z;
+      v[i][3] = x.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        v[i][j] = (k < K && f0 + j < Kout) ? __ldg(src + (long long)k * Kout + f0 + j) : 0.0f;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (f0 + j >= Kout) break;
+    T* d = dst + (long long)(f0 + j) * kp + k0;
+    if constexpr (sizeof(T) == 4) {
+      *reinterpret_cast<float4*>(d) = make_float4(
+          cvt_out<float>(v[0][j], tf32_round), cvt_out<float>(v[1][j], tf32_round),
+          cvt_out<float>(v[2][j], tf32_round), cvt_out<float>(v[3][j], tf32_round));
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v[0][j], v[1][j]);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(v[2][j], v[3][j]);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&lo);
+      u.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(d) = u;
+    }
+  }
+}
+
+template <typename T>
+void pack_filter(const float* filt, int K, int Kout, int kp, T* dst, bool tf32_round,
+                 cudaStream_t st) {
+  if (kp % 4 != 0) fail(TK_ERR_CAPABILITY, "pack_filter: padded K must be a multiple of 4");
+  const long long n = (long long)((Kout + 3) / 4) * (kp / 4);
+  pack_filter_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(filt, K, Kout, kp, dst,
+                                                                     tf32_round ? 1 : 0);
+  note_launch();
+  TKB_CUDA(cudaGetLastError());
+}
+
 // fp32 -> bf16, 8 elements per thread (n % 8 == 0 fast path).
 __global__ void __launch_bounds__(256) to_bf16_kernel(const float4* __restrict__ src,
                                                       __nv_bfloat162* __restrict__ dst,
@@ -1038,8 +1097,9 @@ size_t tc_conv_workspace(const ConvGeom& g, int precision) {
 }
 
 void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float* out,
-                    int precision, void* ws, cudaStream_t st) {
+                    int precision, void* ws, cudaStream_t st, int phase) {
   require_tc(precision);
+  const bool prep = (phase & kConvPrepare) != 0, run = (phase & kConvRun) != 0;
   const long long K = (long long)g.R * g.S * g.C;
   const bool box = conv_boxable(g, precision);
   const long long kp = conv_kp(g, precision);
@@ -1050,7 +1110,8 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     // warps (any channel count / stride), the filter streams by TMA, the
     // output leaves through a TMA store.  fp32 operands, kind::tf32.
     float* ft = reinterpret_cast<float*>(cursor);
-    pack_kmajor<float>(filt, 1, g.K, g.K, K, kp, ft, true, st);
+    if (prep) pack_filter<float>(filt, (int)K, g.K, (int)kp, ft, true, st);
+    if (!run) return;
     const int pixels = g.N * g.OH * g.OW;
     const int cg = 2;
     TcArgs p{};
@@ -1099,17 +1160,18 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   if (tf32) {
     float* ft = reinterpret_cast<float*>(cursor);
     const char* rnd = getenv("TK_TF32_ROUND");
-    pack_kmajor<float>(filt, 1, g.K, g.K, K, kp, ft, !(rnd && rnd[0] == '0'), st);
+    if (prep) pack_filter<float>(filt, (int)K, g.K, (int)kp, ft, !(rnd && rnd[0] == '0'), st);
     fa = ft;
   } else {
     __nv_bfloat16* ft = reinterpret_cast<__nv_bfloat16*>(cursor);
     cursor += align256((size_t)g.K * kp * 2);
-    pack_kmajor<__nv_bfloat16>(filt, 1, g.K, g.K, K, kp, ft, false, st);
+    if (prep) pack_filter<__nv_bfloat16>(filt, (int)K, g.K, (int)kp, ft, false, st);
     __nv_bfloat16* xb = reinterpret_cast<__nv_bfloat16*>(cursor);
-    to_bf16(in, xb, (long long)g.N * g.H * g.W * g.C, st);
+    if (run) to_bf16(in, xb, (long long)g.N * g.H * g.W * g.C, st);
     fa = ft;
     xin = xb;
   }
+  if (!run) return;
 
   // Halo mode: small-feature stride-1 layers whose tap re-reads of the
   // input would otherwise dominate the L2->SM traffic.

@@ -39,7 +39,10 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
 // Implicit-GEMM convolution on tensor cores (NHWC in, HWCK filter, NHWC
 // out).  Workspace: packed filter (+ patch matrix on the fallback path).
 size_t tc_conv_workspace(const ConvGeom& g, int precision);
+// phase: kConvPrepare packs the filter into the workspace (depends only on
+// the filter), kConvRun runs the convolution from a prepared workspace.
+constexpr int kConvPrepare = 1, kConvRun = 2, kConvAll = 3;
 void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float* out,
-                    int precision, void* ws, cudaStream_t st);
+                    int precision, void* ws, cudaStream_t st, int phase = kConvAll);
 
 }  // namespace tkb

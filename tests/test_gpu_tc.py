@@ -107,3 +107,27 @@ def test_tc_vgg_batch32_full_size_property(tk, oracle, prec):
         want = oracle.conv2d_naive(conv, dx[img:img + 1].cpu().numpy(), f)
         err = oracle.max_scaled_error(dy[img:img + 1].cpu().numpy(), want)
         assert err <= TOL[prec], (img, err)
+
+
+@pytest.mark.parametrize("algo,prec", [("im2col", "tf32"), ("im2col", "bf16"),
+                                       ("winograd_t2x2", "tf32"), ("im2col", "fp32")])
+def test_two_phase_api_matches_single_call(tk, oracle, algo, prec):
+    """prepare (filter side) on one stream, run on another after an event:
+    bit-identical to the single-call conv2d_dev."""
+    import torch
+    s = tk.ConvShape(2, 28, 28, 64, 128, 3, 3, 1, True)
+    p = tk.parse_conv_params(algo)
+    x = torch.rand(s.in_shape, device="cuda") * 2 - 1
+    f = torch.rand(s.filt_shape, device="cuda") * 2 - 1
+    ref = torch.empty(s.out_shape, device="cuda")
+    tk.conv2d_dev(x, f, ref, s, p, precision=prec)
+    ws = torch.empty(max(tk.conv2d_workspace_size(s, p, prec), 4) // 4 + 1, device="cuda")
+    out = torch.empty(s.out_shape, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    tk.conv2d_prepare_dev(f, s, p, ws, precision=prec, stream=s1)
+    ev = torch.cuda.Event()
+    ev.record(s1)
+    s2.wait_event(ev)
+    tk.conv2d_run_dev(x, f, out, s, p, ws, precision=prec, stream=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
