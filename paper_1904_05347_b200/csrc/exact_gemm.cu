@@ -101,7 +101,7 @@ void launch_exact(const ExactArgs& p, const ExactLaunch& L, bool conv, int batch
     const int stages = L.stages < 1 ? 1 : (L.stages > 3 ? 3 : L.stages);
     const size_t words = (size_t)(al == kMN ? kExactBK * (BM + 4) : BM * (kExactBK + 4)) +
                          (size_t)(bl == kMN ? kExactBK * (BN + 4) : BN * (kExactBK + 4));
-    const size_t smem = words * 4 * stages;
+    const size_t smem = words * 4 * stages + (conv ? BM * 16 : 0);  // + pixel table
     check_fits((const void*)fn, threads, smem, L);
     if (smem > 48 * 1024)
       TKB_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -189,6 +189,73 @@ __device__ __forceinline__ void stage_patches(float* sm, const ExactArgs& p, int
   }
 }
 
+// Per-CTA pixel table for the implicit patch matrix: row e of the CTA tile
+// -> {element offset of (n, ih0, iw0, 0) in the NHWC input, ih0, iw0}, with
+// ih0 = oh*stride - pad_t, iw0 = ow*stride - pad_l (rows past M get an ih0
+// that fails every bounds test).  Built once per CTA so the slab loop does
+// no divisions.
+struct PixRow {
+  long long base;
+  int ih0, iw0;
+};
+
+__device__ __forceinline__ void build_pix_rows(PixRow* rows, const ExactArgs& p, int m0, int BM,
+                                               int tid, int nthreads) {
+  for (int e = tid; e < BM; e += nthreads) {
+    const int m = m0 + e;
+    PixRow r{0, -(1 << 28), 0};
+    if (m < p.M) {
+      const int ow = m % p.OW, t = m / p.OW;
+      const int oh = t % p.OH, n = t / p.OH;
+      r.ih0 = oh * p.stride - p.pad_t;
+      r.iw0 = ow * p.stride - p.pad_l;
+      r.base = (((long long)n * p.H + r.ih0) * p.W + r.iw0) * p.C;
+    }
+    rows[e] = r;
+  }
+}
+
+// Stage a K-slab of the implicit patch matrix using the pixel table.  A
+// thread's chunks always cover the same 4 consecutive k of the slab (the
+// chunk index advances by nthreads, a multiple of 8), so the tap
+// decomposition is done once per slab and thread.
+__device__ __forceinline__ void stage_patches_fast(float* sm, const ExactArgs& p, const PixRow* rows,
+                                                   int BM, int k0, int tid, int nthreads) {
+  const int kq = (tid & 7) << 2;
+  const int k = k0 + kq;
+  int kx[4], ky[4], kc[4];
+  bool kv[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int kk = k + v;
+    kv[v] = kk < p.K;
+    const int c = kk % p.C, tap = kk / p.C;
+    kc[v] = c;
+    ky[v] = tap % p.S;
+    kx[v] = tap / p.S;
+  }
+  const bool vec = (p.C & 3) == 0 && kv[3] &&  // four channels of one tap, 16B aligned
+                   (reinterpret_cast<uintptr_t>(p.a) & 15) == 0;
+  const long long koff = ((long long)kx[0] * p.W + ky[0]) * p.C + kc[0];
+  for (int e = tid >> 3; e < BM; e += nthreads >> 3) {
+    const PixRow r = rows[e];
+    float* dst = sm + SlabGeom<kK>::off(e, kq, BM);
+    if (vec) {
+      const int ih = r.ih0 + kx[0], iw = r.iw0 + ky[0];
+      const bool ok = (unsigned)ih < (unsigned)p.H && (unsigned)iw < (unsigned)p.W;
+      cp_async16(dst, ok ? p.a + r.base + koff : p.a, ok);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int ih = r.ih0 + kx[v], iw = r.iw0 + ky[v];
+        const bool ok = kv[v] && (unsigned)ih < (unsigned)p.H && (unsigned)iw < (unsigned)p.W;
+        cp_async4(dst + v,
+                  ok ? p.a + r.base + ((long long)kx[v] * p.W + ky[v]) * p.C + kc[v] : p.a, ok);
+      }
+    }
+  }
+}
+
 // Load the register fragment of one depth step from a staged slab.
 template <int T, int LAYOUT>
 __device__ __forceinline__ void load_frag(float (&f)[T], const float* sm, int t, int threads,
@@ -206,6 +273,36 @@ __device__ __forceinline__ void load_frag(float (&f)[T], const float* sm, int t,
   } else {
 #pragma unroll
     for (int u = 0; u < T; ++u) f[u] = sm[SlabGeom<LAYOUT>::off(own_index<T, LAYOUT>(t, threads, u), k, E)];
+  }
+}
+
+// Fragments of four consecutive depth steps k0..k0+3 (k0 % 4 == 0): one
+// 16-byte shared load per row for K-major slabs (the four k are contiguous),
+// one per 4 rows and step for MN-major slabs.  f[kk][u].
+template <int T, int LAYOUT>
+__device__ __forceinline__ void load_frag4(float (&f)[4][T], const float* sm, int t, int threads,
+                                           int E, int k0);
+template <int T, int LAYOUT>
+__device__ __forceinline__ void load_frag4(float (&f)[4][T], const float* sm, int t, int threads,
+                                           int E, int k0) {
+  if constexpr (LAYOUT == kK) {
+#pragma unroll
+    for (int u = 0; u < T; ++u) {
+      const float4 v = *reinterpret_cast<const float4*>(
+          sm + SlabGeom<kK>::off(own_index<T, kK>(t, threads, u), k0, E));
+      f[0][u] = v.x;
+      f[1][u] = v.y;
+      f[2][u] = v.z;
+      f[3][u] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      float g[T];
+      load_frag<T, kMN>(g, sm, t, threads, E, k0 + kk);
+#pragma unroll
+      for (int u = 0; u < T; ++u) f[kk][u] = g[u];
+    }
   }
 }
 
@@ -228,6 +325,11 @@ __global__ void exact_gemm_loc_kernel(ExactArgs p, int wg_r, int wg_c, int stage
 
   const int a_words = SlabGeom<AL>::words(BM), b_words = SlabGeom<BL>::words(BN);
   const int stage_words = a_words + b_words;
+  PixRow* pix_rows = reinterpret_cast<PixRow*>(smem + stages * stage_words);
+  if constexpr (CONV) {
+    build_pix_rows(pix_rows, p, m0, BM, tid, nthreads);
+    __syncthreads();
+  }
 
   float acc[H][W];
 #pragma unroll
@@ -242,7 +344,8 @@ __global__ void exact_gemm_loc_kernel(ExactArgs p, int wg_r, int wg_c, int stage
     float* sb = sa + a_words;
     const int k0 = s * kExactBK;
     if constexpr (CONV) {
-      stage_patches(sa, p, m0, BM, k0, tid, nthreads);
+      if ((nthreads & 7) == 0) stage_patches_fast(sa, p, pix_rows, BM, k0, tid, nthreads);
+      else stage_patches(sa, p, m0, BM, k0, tid, nthreads);
     } else {
       stage_matrix<AL>(sa, ga, p.a_sm, p.a_sk, m0, BM, p.M, k0, p.K, tid, nthreads);
     }
@@ -268,16 +371,37 @@ __global__ void exact_gemm_loc_kernel(ExactArgs p, int wg_r, int wg_c, int stage
     __syncthreads();
     const float* sa = smem + (s % stages) * stage_words;
     const float* sb = sa + a_words;
-    const int depth = min(kExactBK, p.K - s * kExactBK);
-#pragma unroll 4
-    for (int k = 0; k < depth; ++k) {
-      float fa[H], fb[W];
-      load_frag<H, AL>(fa, sa, tm, wg_r, BM, k);
-      load_frag<W, BL>(fb, sb, tn, wg_c, BN, k);
+    // Slab entries past K are staged as zeros on both operands; their +0
+    // products leave every running sum's bits unchanged (a sum started at
+    // +0 is never -0), so the last slab runs in whole groups of four too.
+    const int depth4 = (min(kExactBK, p.K - s * kExactBK) + 3) & ~3;
+#pragma unroll 1
+    for (int k0 = 0; k0 < depth4; k0 += 4) {
+      // K-major operands: one 16-byte load per row covers all four steps;
+      // MN-major operands are loaded per step (bounds register pressure).
+      float a4[AL == kK ? 4 : 1][H], b4[BL == kK ? 4 : 1][W];
+      if constexpr (AL == kK) load_frag4<H, kK>(a4, sa, tm, wg_r, BM, k0);
+      if constexpr (BL == kK) load_frag4<W, kK>(b4, sb, tn, wg_c, BN, k0);
 #pragma unroll
-      for (int i = 0; i < H; ++i)
+      for (int kk = 0; kk < 4; ++kk) {
+        float fa[H], fb[W];
+        if constexpr (AL == kK) {
 #pragma unroll
-        for (int j = 0; j < W; ++j) acc[i][j] = mac_exact(acc[i][j], fa[i], fb[j]);
+          for (int i = 0; i < H; ++i) fa[i] = a4[kk][i];
+        } else {
+          load_frag<H, kMN>(fa, sa, tm, wg_r, BM, k0 + kk);
+        }
+        if constexpr (BL == kK) {
+#pragma unroll
+          for (int j = 0; j < W; ++j) fb[j] = b4[kk][j];
+        } else {
+          load_frag<W, kMN>(fb, sb, tn, wg_c, BN, k0 + kk);
+        }
+#pragma unroll
+        for (int i = 0; i < H; ++i)
+#pragma unroll
+          for (int j = 0; j < W; ++j) acc[i][j] = mac_exact(acc[i][j], fa[i], fb[j]);
+      }
     }
     __syncthreads();
   }
