@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -221,6 +222,20 @@ int precision_of(const tk_exec_options* o) { return o ? o->precision : TK_PREC_F
 // Library default for the exact path: 8x8 register tile, 16x16 threads
 // (128x128 CTA tile), three-stage cp.async ring.
 constexpr ExactLaunch kExactDefault{8, 8, 16, 16, true, 3};
+
+// Convolutions with <= 64 output features would idle half of a 128-wide
+// feature tile: keep the 8x8 register tile, reshape the CTA to 256x64.
+// TK_EXACT_STAGES overrides the ring depth (tuning experiments).
+ExactLaunch exact_conv_default(const ConvGeom& g) {
+  ExactLaunch L = kExactDefault;
+  if (g.K <= 64) {
+    L.r = 32;
+    L.c = 8;
+    L.stages = 2;
+  }
+  if (const char* e = std::getenv("TK_EXACT_STAGES")) L.stages = std::atoi(e);
+  return L;
+}
 
 ExactLaunch exact_launch_of(const tilekit::GemmConfig& c) {
   ExactLaunch L;
@@ -443,7 +458,7 @@ void conv_dev(const tilekit::ConvShape& s, const tk_conv_params* p, int precisio
   switch (p->algo) {
     case 0:  // Naive: the oracle's arithmetic
       if (precision == TK_PREC_FP32_EXACT) {
-        if (exact_run) launch_exact(conv_args(g, in, filt, out), kExactDefault, true, 1, st);
+        if (exact_run) launch_exact(conv_args(g, in, filt, out), exact_conv_default(g), true, 1, st);
         return;
       }
       break;
@@ -456,7 +471,7 @@ void conv_dev(const tilekit::ConvShape& s, const tk_conv_params* p, int precisio
       break;
     case 2:  // Im2col: implicit GEMM (tensor cores when a TC precision is set)
       if (precision == TK_PREC_FP32_EXACT) {
-        if (exact_run) launch_exact(conv_args(g, in, filt, out), kExactDefault, true, 1, st);
+        if (exact_run) launch_exact(conv_args(g, in, filt, out), exact_conv_default(g), true, 1, st);
       } else {
         launch_tc_conv(g, in, filt, out, precision, ws, st, phase);
       }
@@ -473,19 +488,78 @@ void conv_dev(const tilekit::ConvShape& s, const tk_conv_params* p, int precisio
                               "\" is FP32-exact only; use im2col or winograd for tensor cores");
 }
 
-// Host-buffer conv: copy in, run, copy out.
+// Host-buffer conv: copy in, run, copy out -- pipelined over batch chunks
+// so the host->device copy of chunk i+1, the convolution of chunk i and the
+// device->host copy of chunk i-1 overlap (separate copy engines for the two
+// directions; concurrency needs page-locked host buffers, pageable ones
+// still work, serialised by the driver).  Chunks are equal slices of the
+// batch (NHWC: a contiguous range of images), so one prepared workspace
+// serves every chunk.
+struct HostPipe {
+  cudaStream_t compute = nullptr, copy_in = nullptr, copy_out = nullptr;
+  static constexpr int kMaxChunks = 8;
+  cudaEvent_t ready = nullptr, in_done[kMaxChunks] = {}, run_done[kMaxChunks] = {},
+              out_done = nullptr;
+  HostPipe() {
+    TKB_CUDA(cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking));
+    TKB_CUDA(cudaStreamCreateWithFlags(&copy_in, cudaStreamNonBlocking));
+    TKB_CUDA(cudaStreamCreateWithFlags(&copy_out, cudaStreamNonBlocking));
+    TKB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    TKB_CUDA(cudaEventCreateWithFlags(&out_done, cudaEventDisableTiming));
+    for (int i = 0; i < kMaxChunks; ++i) {
+      TKB_CUDA(cudaEventCreateWithFlags(&in_done[i], cudaEventDisableTiming));
+      TKB_CUDA(cudaEventCreateWithFlags(&run_done[i], cudaEventDisableTiming));
+    }
+  }
+};
+
+HostPipe& host_pipe() {
+  host_stream();  // device + pool checks
+  thread_local HostPipe pipe;
+  return pipe;
+}
+
+// Number of equal batch chunks: the largest divisor of the batch <= 8 that
+// keeps every chunk's copies >= 2 MiB (a copy's fixed cost is ~10 us).
+int pipeline_chunks(const ConvGeom& g) {
+  const size_t per_image = 4 * ((size_t)g.H * g.W * g.C + (size_t)g.OH * g.OW * g.K);
+  for (int n = HostPipe::kMaxChunks; n > 1; --n)
+    if (g.N % n == 0 && per_image * (size_t)(g.N / n) >= (2u << 20)) return n;
+  return 1;
+}
+
 void conv_host(const tilekit::ConvShape& s, const tk_conv_params* p, int precision,
                const float* in, const float* filt, float* out) {
   const ConvGeom g = conv_geom(s);
   if (p->algo == 1) check_tiled_params(s, p);
   if (p->algo == 3) check_winograd(s, p);
-  cudaStream_t st = host_stream();
-  DevBuf din(4 * in_elems(g), st), dfl(4 * filt_elems(g), st), dout(4 * out_elems(g), st);
-  DevBuf ws(conv_workspace(g, p, precision), st);
-  h2d(din.p, in, 4 * in_elems(g), st);
-  h2d(dfl.p, filt, 4 * filt_elems(g), st);
-  conv_dev(s, p, precision, din.f(), dfl.f(), dout.f(), ws.p, st);
-  d2h(out, dout.p, 4 * out_elems(g), st);
+  HostPipe& hp = host_pipe();
+  const int chunks = pipeline_chunks(g);
+  tilekit::ConvShape cs = s;
+  cs.batch = s.batch / (size_t)chunks;
+  const ConvGeom cg = conv_geom(cs);
+  const size_t in_chunk = in_elems(cg), out_chunk = out_elems(cg);
+  cudaStream_t st = hp.compute;
+  {
+    DevBuf din(4 * in_elems(g), st), dfl(4 * filt_elems(g), st), dout(4 * out_elems(g), st);
+    DevBuf ws(conv_workspace(cg, p, precision), st);
+    h2d(dfl.p, filt, 4 * filt_elems(g), st);
+    conv_dev(cs, p, precision, nullptr, dfl.f(), nullptr, ws.p, st, kConvPrepare);
+    TKB_CUDA(cudaEventRecord(hp.ready, st));  // allocations exist from here on
+    TKB_CUDA(cudaStreamWaitEvent(hp.copy_in, hp.ready, 0));
+    for (int i = 0; i < chunks; ++i) {
+      h2d(din.f() + i * in_chunk, in + i * in_chunk, 4 * in_chunk, hp.copy_in);
+      TKB_CUDA(cudaEventRecord(hp.in_done[i], hp.copy_in));
+      TKB_CUDA(cudaStreamWaitEvent(st, hp.in_done[i], 0));
+      conv_dev(cs, p, precision, din.f() + i * in_chunk, dfl.f(), dout.f() + i * out_chunk, ws.p,
+               st, kConvRun);
+      TKB_CUDA(cudaEventRecord(hp.run_done[i], st));
+      TKB_CUDA(cudaStreamWaitEvent(hp.copy_out, hp.run_done[i], 0));
+      d2h(out + i * out_chunk, dout.f() + i * out_chunk, 4 * out_chunk, hp.copy_out);
+    }
+    TKB_CUDA(cudaEventRecord(hp.out_done, hp.copy_out));
+    TKB_CUDA(cudaStreamWaitEvent(st, hp.out_done, 0));  // frees are ordered after the copies
+  }
   finish(st);
 }
 
