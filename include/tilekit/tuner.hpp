@@ -347,6 +347,11 @@ inline TuningRecord benchmark_config(const Problem& problem, const GemmConfig& c
   const Matrix b = detail::sized(tb ? s.n : s.k, tb ? s.k : s.n, seed + 1);
   const Matrix c = detail::sized(s.m, s.n, seed + 2);
   const bool exact = opts.exec.precision == b200::Precision::Fp32Exact;
+  if (exact) {  // the budget check gemm_tiled makes before any launch
+    const ConfigVerdict v = validate_config(cfg, dev, s);
+    if (!v.ok)
+      throw ConfigError("gemm_tiled: config \"" + cfg.name() + "\" rejected: " + v.summary());
+  }
   const std::string name =
       exact ? cfg.name() : "gemm@" + b200::precision_name(opts.exec.precision) +
                                (opts.exec.tc_tile_n ? "_n" + std::to_string(opts.exec.tc_tile_n) : "");

@@ -10,10 +10,12 @@
 // CPU baseline / --impl reference arm of bench.py (the reference's own
 // gemm_tiled / conv2d timed on the host cores).
 #define tilekit tilekit_ref
+#include "tilekit/analysis.hpp"
 #include "tilekit/config.hpp"
 #include "tilekit/conv.hpp"
 #include "tilekit/device.hpp"
 #include "tilekit/gemm.hpp"
+#include "tilekit/layers.hpp"
 #include "tilekit/numeric.hpp"
 #include "tilekit/tuner.hpp"
 #include "tilekit/winograd.hpp"
@@ -21,6 +23,7 @@
 
 #include <chrono>
 #include <cstring>
+#include <sstream>
 #include <string>
 
 namespace tk = tilekit_ref;
@@ -247,6 +250,52 @@ int64_t ref_time_conv2d(const ShapeC* s, const char* params, const float* in,
   auto t1 = std::chrono::steady_clock::now();
   if (rc != 0) return -rc;
   return std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+}
+
+// Copies text into a caller buffer; returns the full length (truncates).
+static size_t put_text(const std::string& t, char* out, size_t cap) {
+  if (cap) {
+    const size_t n = t.size() < cap - 1 ? t.size() : cap - 1;
+    std::memcpy(out, t.data(), n);
+    out[n] = 0;
+  }
+  return t.size();
+}
+
+// The reference's render_report over n points (analysis.hpp:157-181).
+// Returns the text length, or -1 with the message in ref_last_error.
+long long ref_render_report(int n, const char** problems, const char** configs,
+                            const double* oi, const double* gflops, const int* ok, int json,
+                            char* out, size_t cap) {
+  try {
+    std::vector<tk::RooflinePoint> pts(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      pts[i].problem = problems[i];
+      pts[i].config = configs[i];
+      pts[i].oi = oi[i];
+      pts[i].gflops = gflops[i];
+      pts[i].ok = ok[i] != 0;
+    }
+    return (long long)put_text(
+        tk::render_report(pts, json ? tk::ReportFormat::Json : tk::ReportFormat::Csv), out, cap);
+  } catch (const std::exception& e) {
+    fail(e);
+    return -1;
+  }
+}
+
+// The reference's load_layer_rows on in-memory text, re-serialised
+// (layers.hpp:90-185): returns the serialised table, or on a parse error
+// -1 with the exception message in ref_last_error.
+long long ref_layer_table(const char* text, const char* origin, char* out, size_t cap) {
+  try {
+    std::istringstream in(text);
+    return (long long)put_text(tk::serialize_layer_rows(tk::load_layer_rows(in, origin)), out,
+                               cap);
+  } catch (const std::exception& e) {
+    fail(e);
+    return -1;
+  }
 }
 
 }  // extern "C"
