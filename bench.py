@@ -549,7 +549,7 @@ def main():
         gc = torch.empty(n * n, device=dev)
         gshape = tk.GemmShape(n, n, n)
         for p_ in ("fp32", "tf32", "bf16"):
-            cfg = tk.parse_gemm_config("8x8_16x16_loc_db") if p_ == "fp32" else None
+            cfg = None  # library tile (exact: sized to fill the SMs)
             for _ in range(3):
                 tk.gemm_dev(gb, ga, None, gc, gshape, cfg, precision=p_, stream=stream)
             ts = []

@@ -223,18 +223,32 @@ int precision_of(const tk_exec_options* o) { return o ? o->precision : TK_PREC_F
 // (128x128 CTA tile), three-stage cp.async ring.
 constexpr ExactLaunch kExactDefault{8, 8, 16, 16, true, 3};
 
-// Convolutions with <= 64 output features would idle half of a 128-wide
-// feature tile: keep the 8x8 register tile, reshape the CTA to 256x64.
-// TK_EXACT_STAGES overrides the ring depth (tuning experiments).
-ExactLaunch exact_conv_default(const ConvGeom& g) {
+// Library tile for the exact path when the caller names no GemmConfig,
+// from the output extent (measured on B200, profiles/r01_sweep_fp32.csv and
+// the VGG16 layers): 128x128 CTAs (two per SM) while they fill four waves;
+// <= 64 output columns would idle half of that tile, so 256x64; smaller
+// problems drop to 64x128 / 64x64 CTAs to fill the 148 SMs.  Two stages:
+// a third costs the second resident CTA for no gain.
+// TK_EXACT_STAGES / TK_EXACT_TILE="h,w,r,c" override (tuning experiments).
+ExactLaunch exact_auto(long long M, long long N) {
+  auto tiles = [&](long long bm, long long bn) { return ((M + bm - 1) / bm) * ((N + bn - 1) / bn); };
   ExactLaunch L = kExactDefault;
-  if (g.K <= 64) {
+  L.stages = 2;
+  if (N <= 64) {
     L.r = 32;
     L.c = 8;
-    L.stages = 2;
+  } else if (tiles(128, 128) < 4 * 148) {
+    L.r = 8;  // 64 x 128
+    if (tiles(64, 128) < 2 * 148) L.w = 4;  // 64 x 64
   }
   if (const char* e = std::getenv("TK_EXACT_STAGES")) L.stages = std::atoi(e);
+  if (const char* e = std::getenv("TK_EXACT_TILE"))
+    std::sscanf(e, "%d,%d,%d,%d", &L.h, &L.w, &L.r, &L.c);
   return L;
+}
+
+ExactLaunch exact_conv_default(const ConvGeom& g) {
+  return exact_auto((long long)g.N * g.OH * g.OW, g.K);
 }
 
 ExactLaunch exact_launch_of(const tilekit::GemmConfig& c) {
@@ -417,7 +431,7 @@ void winograd_dev(const ConvGeom& g, int m, int precision, const float* in, cons
     p.alpha = 1.0f;
     p.read_c = 0;
     p.tx_on_m = 0;
-    launch_exact(p, kExactDefault, false, spots, st);
+    launch_exact(p, exact_auto((long long)w.tiles * spots, w.K), false, spots, st);
   } else {
     // P[tile][k] = sum_c Ut[k][c] * V[tile][c]: features on the MMA M side
     // so the epilogue stores coalesce along k.
@@ -692,7 +706,8 @@ int tk_gemm_naive(const tk_gemm_shape* shape, const float* a, const float* b, co
     h2d(da.p, a, 4 * na, st);
     h2d(db.p, b, 4 * nb, st);
     if (read_c) h2d(dc.p, c, 4 * nc, st);
-    launch_exact(gemm_args(g, da.f(), db.f(), dc.f(), dd.f()), kExactDefault, false, 1, st);
+    launch_exact(gemm_args(g, da.f(), db.f(), dc.f(), dd.f()), exact_auto((long long)g.m, (long long)g.n), false, 1,
+                 st);
     d2h(out, dd.p, 4 * nc, st);
     finish(st);
   });
@@ -706,7 +721,7 @@ int tk_gemm_dev(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const tk_
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int prec = precision_of(opts);
     if (prec == TK_PREC_FP32_EXACT) {
-      const ExactLaunch L = cfg ? exact_launch_of(gemm_config(cfg)) : kExactDefault;
+      const ExactLaunch L = cfg ? exact_launch_of(gemm_config(cfg)) : exact_auto((long long)g.m, (long long)g.n);
       launch_exact(gemm_args(g, d_a, d_b, d_c, d_out), L, false, 1, st);
     } else {
       launch_tc_colmajor_gemm(g.m, g.n, g.k, g.alpha, g.beta, g.op_a == tilekit::Op::Transpose,
@@ -729,7 +744,8 @@ int tk_gemm_ex(const tk_gemm_shape* shape, const tk_exec_options* opts, const fl
     if (read_c) h2d(dc.p, c, 4 * nc, st);
     const int prec = precision_of(opts);
     if (prec == TK_PREC_FP32_EXACT)
-      launch_exact(gemm_args(g, da.f(), db.f(), dc.f(), dd.f()), kExactDefault, false, 1, st);
+      launch_exact(gemm_args(g, da.f(), db.f(), dc.f(), dd.f()), exact_auto((long long)g.m, (long long)g.n), false, 1,
+                 st);
     else
       launch_tc_colmajor_gemm(g.m, g.n, g.k, g.alpha, g.beta, g.op_a == tilekit::Op::Transpose,
                               g.op_b == tilekit::Op::Transpose, da.f(), db.f(), dc.f(), dd.f(),
@@ -775,7 +791,7 @@ int tk_gemm_batched_strided(const float* a, size_t sa, const float* b, size_t sb
       p.d_batch = (long long)sc;
       p.alpha = 1.0f;
       p.tx_on_m = 1;
-      launch_exact(p, kExactDefault, false, (int)batch, st);
+      launch_exact(p, exact_auto((long long)(m * batch), (long long)n), false, (int)batch, st);
     }
     d2h(c, dc.p, 4 * ec, st);
     finish(st);
@@ -807,7 +823,8 @@ int tk_gemm_batched_strided_dev(const float* d_a, size_t sa, const float* d_b, s
     p.d_batch = (long long)sc;
     p.alpha = 1.0f;
     p.tx_on_m = 1;
-    launch_exact(p, kExactDefault, false, (int)batch, static_cast<cudaStream_t>(stream));
+    launch_exact(p, exact_auto((long long)(m * batch), (long long)n), false, (int)batch,
+                 static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -1006,7 +1023,7 @@ int tk_bench_gemm(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const t
     h2d(db.p, b, 4 * nb, st);
     if (read_c) h2d(dc.p, c, 4 * nc, st);
     const int prec = precision_of(opts);
-    const ExactLaunch L = cfg ? exact_launch_of(gemm_config(cfg)) : kExactDefault;
+    const ExactLaunch L = cfg ? exact_launch_of(gemm_config(cfg)) : exact_auto((long long)g.m, (long long)g.n);
     auto run = [&] {
       if (prec == TK_PREC_FP32_EXACT) {
         launch_exact(gemm_args(g, da.f(), db.f(), dc.f(), dd.f()), L, false, 1, st);
