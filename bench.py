@@ -434,8 +434,24 @@ def main():
     else:
         peak_tf = 148 * 128 * 2 * 1.965e9 / 1e12 / 2
         peak_note = "FP32 exact FMUL+FADD cap = 1/2 of 74.4 TF/s FFMA"
+    # DRAM traffic of the dominant kernel per step, from the committed ncu
+    # launch list of this same command (profiles/, tools/launch_summary.py),
+    # next to the compulsory bytes of the step (each layer's input, filter
+    # and output once, conv_oi's model).
+    traffic, traffic_src = None, None
+    import glob
+    profs = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_launches_{prec}.json")))
+    prof = profs[-1] if profs else ""
+    if prof:
+        kern = json.load(open(prof))["kernels"]
+        tb = sum(v["dram_bytes"] for k, v in kern.items() if "tc_gemm_kernel" in k
+                 or "exact_gemm" in k)
+        traffic, traffic_src = int(tb), os.path.relpath(prof, ROOT)
+    compulsory = sum(4 * (L["x"].numel() + L["f"].numel() + L["y"].numel()) for L in layers)
     roofline = {"bound": "tensor", "achieved": round(achieved_tf, 2), "peak": round(peak_tf, 1),
-                "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4), "traffic": None,
+                "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic,
+                "traffic_unit": "DRAM bytes per step, all conv launches (ncu dram__bytes_read+write)",
+                "traffic_source": traffic_src, "compulsory_bytes": int(compulsory),
                 "kernel": "exact_gemm_loc_kernel" if prec == "fp32" else "tc_gemm_kernel (implicit-GEMM conv)",
                 "peak_source": peak_note}
 

@@ -131,3 +131,48 @@ def test_two_phase_api_matches_single_call(tk, oracle, algo, prec):
     tk.conv2d_run_dev(x, f, out, s, p, ws, precision=prec, stream=s2)
     torch.cuda.synchronize()
     assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+def test_graph_captured_stack_matches_direct_calls(tk, prec):
+    """The bench's captured step (prepare forked to a side stream, each run
+    joining on its own prepare event, replayed as one CUDA graph) gives
+    bit-identical outputs to direct conv2d_dev calls, for layers covering the
+    gather (C=3), halo (C=64), pixN and pixM modes and a ragged shape."""
+    import torch
+    shapes = [(4, 56, 56, 3, 64), (4, 56, 56, 64, 64), (4, 28, 28, 128, 256),
+              (4, 14, 14, 256, 64), (3, 17, 23, 32, 96)]
+    p = tk.parse_conv_params("im2col")
+    layers = []
+    g = torch.Generator(device="cuda").manual_seed(7)
+    for N, H, W, C, K in shapes:
+        s = tk.ConvShape(N, H, W, C, K, 3, 3, 1, True)
+        x = torch.rand(s.in_shape, device="cuda", generator=g) * 2 - 1
+        f = torch.rand(s.filt_shape, device="cuda", generator=g) * 2 - 1
+        ref = torch.empty(s.out_shape, device="cuda")
+        tk.conv2d_dev(x, f, ref, s, p, precision=prec)
+        ws = torch.empty(max(tk.conv2d_workspace_size(s, p, prec), 4) // 4 + 1, device="cuda")
+        layers.append((s, x, f, ref, ws, torch.full(s.out_shape, float("nan"), device="cuda")))
+    torch.cuda.synchronize()
+    cap, side = torch.cuda.Stream(), torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=cap):
+        side.wait_stream(cap)
+        ready = []
+        with torch.cuda.stream(side):
+            for s, x, f, ref, ws, out in layers:
+                tk.conv2d_prepare_dev(f, s, p, ws, precision=prec, stream=side)
+                ev = torch.cuda.Event()
+                ev.record(side)
+                ready.append(ev)
+        for (s, x, f, ref, ws, out), ev in zip(layers, ready):
+            cap.wait_event(ev)
+            tk.conv2d_run_dev(x, f, out, s, p, ws, precision=prec, stream=cap)
+        cap.wait_stream(side)
+    for _ in range(3):
+        for *_, out in layers:
+            out.fill_(float("nan"))
+        graph.replay()
+        torch.cuda.synchronize()
+        for s, x, f, ref, ws, out in layers:
+            assert torch.equal(out.view(torch.int32), ref.view(torch.int32)), s
