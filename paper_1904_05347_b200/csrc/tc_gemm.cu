@@ -35,6 +35,8 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <vector>
+#include <cstdio>
 
 #include "common.cuh"
 #include "tc_gemm.cuh"
@@ -82,7 +84,48 @@ struct TcArgs {
   // gather mode: input geometry
   const float* in;
   int H, W, C, R, stride, Kreal;
+  // split-K (plain mode): unit t covers K-slabs [sp*kb_per, sp*kb_per +
+  // kb_per) of its tile, sp = t / (num_m*num_n*batch); partial tiles are
+  // stored at batch coordinate sp*batch + z and summed by splitk_reduce.
+  int splits, kb_per;
+  // With splits > 1 every unit stores its partial tile at part +
+  // sp*part_stride (the output's own layout); splitk_reduce then sums the
+  // partials in split order (deterministic, no atomics) into the output.
+  float* part;
+  long long part_stride;
+  // Timeline probe (TK_TC_TRACE=1, experiments only): per CTA, globaltimer
+  // stamps of kTraceEvents milestones.
+  unsigned long long* trace;
 };
+
+constexpr int kTraceEvents = 10;
+__device__ __forceinline__ void trace_mark(const TcArgs& p, int ev) {
+  if (p.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+    p.trace[blockIdx.x * kTraceEvents + ev] = t;
+  }
+}
+
+// Work unit t -> (m_blk, n_blk, z, split) and its K-slab range.
+struct Unit {
+  int m_blk, n_blk, z, sp, kb0, kb1;
+};
+
+__device__ __forceinline__ Unit decode_unit(const TcArgs& p, int t) {
+  Unit u;
+  u.m_blk = t % p.num_m;
+  int rest = t / p.num_m;
+  u.n_blk = rest % p.num_n;
+  rest /= p.num_n;
+  u.z = rest % p.batch;
+  u.sp = rest / p.batch;
+  u.kb0 = u.sp * p.kb_per;
+  u.kb1 = min(p.num_kb, u.kb0 + p.kb_per);
+  return u;
+}
+
+
 
 struct PixTile {
   int img, oh0, ow0;
@@ -134,6 +177,7 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
                    : "memory");
     }
   }
+  if (local == 0 && issuer) trace_mark(p, 8);  // TMEM drained to smem (first unit)
   ptx::tc_fence_before();
   ptx::fence_proxy_async();
   ptx::named_sync(1, 128);
@@ -147,6 +191,7 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
       else ptx::tma_store_3d(map_d, src, c0 + 32 * j, c1, c2);
     }
     ptx::bulk_commit();
+    if (local == 0) trace_mark(p, 9);  // stores issued (first unit)
   }
 }
 
@@ -279,6 +324,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   const uint32_t rank = CG == 2 ? ptx::cluster_rank() : 0;
   const bool leader = rank == 0;
+  if (threadIdx.x == 0) trace_mark(p, 0);  // entry
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&map_a);
@@ -303,8 +349,14 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   if constexpr (CG == 2) ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the setup above overlapped the previous
+  // kernel's tail; nothing below may touch global memory before it is done.
+  // The next kernel may be scheduled as soon as SMs free up.
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
+  if (threadIdx.x == 0) trace_mark(p, 1);  // barriers + TMEM ready
 
-  const int total = p.num_m * p.num_n * p.batch;
+  const int total = p.num_m * p.num_n * p.batch * p.splits;
   const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
 
   if (MODE == kConvHalo && warp == 0) {
@@ -413,14 +465,12 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = unit; t < total; t += nunits) {
-        const int m_blk = t % p.num_m;
-        const int rest = t / p.num_m;
-        const int n_blk = rest % p.num_n;
-        const int z = rest / p.num_n;
+        const Unit u = decode_unit(p, t);
+        const int m_blk = u.m_blk, n_blk = u.n_blk, z = u.z;
         PixTile pt{0, 0, 0};
         if constexpr (MODE == kConvPixN) pt = pix_tile(p, n_blk);
         if constexpr (MODE == kConvPixM) pt = pix_tile(p, m_blk);
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kb = u.kb0; kb < u.kb1; ++kb) {
           ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
           uint8_t* sa = base + stage * stage_bytes;
           uint8_t* sb = sa + a_bytes;
@@ -470,18 +520,22 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         ptx::mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        const Unit u = decode_unit(p, t);
+        for (int kb = u.kb0; kb < u.kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (local == 0 && kb == u.kb0 && lane == 0) trace_mark(p, 2);  // first slab landed
+          if (local == 0 && kb == u.kb1 - 1 && lane == 0) trace_mark(p, 3);  // last slab landed
           if (ptx::elect_one()) {
             const uint32_t sa = ptx::smem(base + stage * stage_bytes);
             const uint64_t ad = kdesc + (sa >> 4);
             const uint64_t bd = kdesc + ((sa + (uint32_t)a_bytes) >> 4);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              ptx::mma_cg<CG, TF32>(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+              ptx::mma_cg<CG, TF32>(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc,
+                                    (kb != u.kb0 || kk != 0));
             ptx::commit_cg<CG>(&empty[stage]);
-            if (kb == p.num_kb - 1) ptx::commit_cg<CG>(&tmem_full[acc]);
+            if (kb == u.kb1 - 1) ptx::commit_cg<CG>(&tmem_full[acc]);
           }
           __syncwarp();
           if (++stage == p.stages) {
@@ -520,14 +574,14 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
     if constexpr (CG == 2) empty_base = ptx::map_to_rank(empty_base, 0);
     int local = 0;
     for (int t = unit; t < total; t += nunits, ++local) {
-      const int m_blk = t % p.num_m;
-      const int rest = t / p.num_m;
-      const int n_blk = rest % p.num_n;
-      const int z = rest / p.num_n;
+      const Unit u = decode_unit(p, t);
+      const int m_blk = u.m_blk, n_blk = u.n_blk, z = u.z;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       ptx::mbar_wait_sleep(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
+      if (local == 0 && warp == 2 && lane == 0) trace_mark(p, 4);  // first accumulator ready
+      if (local == 1 && warp == 2 && lane == 0) trace_mark(p, 5);  // second accumulator ready
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
 
       if constexpr (MODE == kConvHalo) {
@@ -551,7 +605,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         if (p.store_tma) {
           tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, row, empty_base + 8u * acc,
                                  &tmem_empty[acc], &map_d, n_blk * p.BN,
-                                 m_blk * BM + rank * kRows, z, 0, 3);
+                                 m_blk * BM + rank * kRows, u.sp * p.batch + z, 0, 3);
           continue;
         }
         for (int col = 0; col < p.BN; col += 32) {
@@ -588,11 +642,13 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           const long long pix_off =
               ok ? (((long long)pt.img * p.OH + oh) * p.OW + ow) * p.Kout : -1ll;
 #pragma unroll
+          float* dst = p.splits > 1 ? p.part + u.sp * p.part_stride : p.d;
           for (int j = 0; j < 32; ++j) {
             const long long o = __shfl_sync(0xffffffffu, pix_off, j);
-            if (o >= 0 && m_ok) p.d[o + m] = v[j];
+            if (o >= 0 && m_ok) dst[o + m] = v[j];
           }
         }
+
       } else {
         const PixTile pt = pix_tile(p, m_blk);
         tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, row, empty_base + 8u * acc,
@@ -610,8 +666,10 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   }
 
   if (warp == 2 && lane == 0 && p.store_tma) ptx::bulk_wait<0>();
+  if (warp == 2 && lane == 0) trace_mark(p, 6);  // epilogue stores complete
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_mark(p, 7);  // exit
   if constexpr (CG == 2) ptx::cluster_sync();
   if (warp == 2) {
     ptx::tc_fence_after();
@@ -704,6 +762,10 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
                               : kRows * kSlabBytes + b_bytes_h;
   const int fres_bytes = (MODE == kConvHalo && p.resident) ? p.taps * p.cchunks * b_bytes_h : 0;
   const int ktab_bytes0 = MODE == kConvGather ? p.num_kb * 32 * 8 : 0;
+  // Tuning experiments: TK_TC_STAGES caps the ring, TK_TC_EPI=1 forces one
+  // staging buffer.
+  if (const char* e = getenv("TK_TC_STAGES")) stages_req = atoi(e);
+  if (const char* e = getenv("TK_TC_EPI")) p.epi_bufs = std::min(p.epi_bufs, atoi(e));
   // Double-buffered TMA-store staging when it leaves room for >= 3 stages.
   if (p.store_tma && p.epi_bufs > 1 &&
       232448 - 2048 - ktab_bytes0 - 2 * ((p.BN + 31) / 32) * kRows * kSlabBytes < 3 * stage_bytes)
@@ -723,7 +785,11 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   auto fn = tc_gemm_kernel<MODE, CG, TF32>;
   TKB_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-  const long long total = (long long)p.num_m * p.num_n * p.batch;
+  if (p.splits < 1 || (MODE != kPlain && MODE != kConvPixN)) {
+    p.splits = 1;
+    p.kb_per = p.num_kb;
+  }
+  const long long total = (long long)p.num_m * p.num_n * p.batch * p.splits;
   const int units = sm_count() / CG;
   int used = (int)(total < units ? total : units);
   // Halo mode with a resident filter: every CTA must keep one feature block.
@@ -735,15 +801,51 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   cfg.blockDim = dim3(threads_of<MODE>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool pdl = [] {
+    const char* e = getenv("TK_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cfg.numAttrs = pdl ? 2 : 1;
+  const char* tr = getenv("TK_TC_TRACE");
+  unsigned long long* trace = nullptr;
+  if (tr && tr[0] == '1') {
+    TKB_CUDA(cudaMalloc(&trace, (size_t)grid * kTraceEvents * 8));
+    TKB_CUDA(cudaMemset(trace, 0, (size_t)grid * kTraceEvents * 8));
+    p.trace = trace;
+  }
   TKB_CUDA(cudaLaunchKernelEx(&cfg, fn, ma, mb, md, p));
   note_launch();
+  if (trace) {
+    std::vector<unsigned long long> h((size_t)grid * kTraceEvents);
+    TKB_CUDA(cudaStreamSynchronize(st));
+    TKB_CUDA(cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost));
+    cudaFree(trace);
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[(size_t)b * kTraceEvents]);
+    static const char* names[kTraceEvents] = {"entry", "setup", "slab0", "slabN", "acc0",
+                                              "acc1", "stored", "exit", "drained", "issued"};
+    std::fprintf(stderr, "tc trace MODE=%d CG=%d grid=%d units=%lld stages=%d BN=%d (us from first entry: min/med/max)\n",
+                 MODE, CG, grid, total, stages, p.BN);
+    for (int e = 0; e < kTraceEvents; ++e) {
+      std::vector<double> v;
+      for (int b = 0; b < grid; ++b) {
+        const unsigned long long x = h[(size_t)b * kTraceEvents + e];
+        if (x) v.push_back((double)(x - t0) / 1e3);
+      }
+      if (v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      std::fprintf(stderr, "  %-7s n=%3zu  %8.2f %8.2f %8.2f\n", names[e], v.size(), v.front(),
+                   v[v.size() / 2], v.back());
+    }
+  }
 }
 
 template <int MODE>
@@ -896,6 +998,81 @@ void to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st)
   const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)sm_count() * 8);
   to_bf16_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(src),
                                          reinterpret_cast<__nv_bfloat162*>(dst), n4);
+  note_launch();
+  TKB_CUDA(cudaGetLastError());
+}
+
+// out[i] = sum_s part[s*stride + i] in split order (deterministic), 4
+// elements per thread (n % 4 == 0, 16-byte aligned rows).
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __restrict__ part,
+                                                            long long stride4, int splits,
+                                                            float4* __restrict__ out, long long n4) {
+  constexpr int kMaxSplits = 16;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 v[kMaxSplits];  // every split's load in flight before the ordered sum
+#pragma unroll
+    for (int s = 0; s < kMaxSplits; ++s)
+      if (s < splits) v[s] = __ldcs(part + s * stride4 + i);
+    float4 a = v[0];
+#pragma unroll
+    for (int s = 1; s < kMaxSplits; ++s) {
+      if (s < splits) {
+        a.x += v[s].x;
+        a.y += v[s].y;
+        a.z += v[s].z;
+        a.w += v[s].w;
+      }
+    }
+    out[i] = a;
+  }
+}
+
+void splitk_reduce(const float* part, long long n, int splits, float* out, cudaStream_t st) {
+  const long long n4 = n / 4;
+  const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)sm_count() * 8);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(part), n4, splits,
+                                               reinterpret_cast<float4*>(out), n4);
+  note_launch();
+  TKB_CUDA(cudaGetLastError());
+}
+
+// Pointwise (1x1) conv operand: the input pixels the strided window visits,
+// compacted to [N*OH*OW][C] and converted to T (fp32 copy or bf16), 4
+// channels per thread.  Stride 1 + bf16 is a plain conversion.
+template <typename T>
+__global__ void __launch_bounds__(256) pointwise_gather_kernel(const float* __restrict__ in,
+                                                               ConvGeom g, T* __restrict__ out,
+                                                               long long n4) {
+  const int c4 = g.C / 4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long pix = i / c4;
+    const int c = (int)(i - pix * c4) * 4;
+    const int ow = (int)(pix % g.OW);
+    const long long t = pix / g.OW;
+    const int oh = (int)(t % g.OH);
+    const int n = (int)(t / g.OH);
+    const float4 v = __ldg(reinterpret_cast<const float4*>(
+        in + (((long long)n * g.H + (long long)oh * g.stride) * g.W + (long long)ow * g.stride) * g.C +
+        c));
+    if constexpr (sizeof(T) == 4) {
+      reinterpret_cast<float4*>(out)[i] = v;
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&lo);
+      u.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(out)[i] = u;
+    }
+  }
+}
+
+template <typename T>
+void pointwise_gather(const float* in, const ConvGeom& g, T* out, cudaStream_t st) {
+  const long long n4 = (long long)g.N * g.OH * g.OW * (g.C / 4);
+  const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)sm_count() * 16);
+  pointwise_gather_kernel<T><<<blocks, 256, 0, st>>>(in, g, out, n4);
   note_launch();
   TKB_CUDA(cudaGetLastError());
 }
@@ -1077,23 +1254,213 @@ bool conv_boxable(const ConvGeom& g, int precision) {
   return g.C % slab_elems(precision) == 0 && g.stride == 1;
 }
 
-long long conv_kp(const ConvGeom& g, int precision) {
-  const long long K = (long long)g.R * g.S * g.C;
-  if (conv_boxable(g, precision)) return K;
-  return (K + 31) / 32 * 32;  // fallback path is always TF32 on fp32 patches
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
+// How a convolution runs on the tensor cores and what its workspace holds.
+//   kGatherPlan    any C / stride: producer warps build the pixel operand
+//   kBoxPlan       C a whole number of slabs, stride 1: halo / pixN / pixM
+//   kPointwisePlan 1x1 window: a plain GEMM [pixels][C] x [Kout][C]^T on the
+//                  NHWC input itself (stride 1, TF32) or on a compacted /
+//                  converted copy (stride 2, BF16), split over K when the
+//                  output has too few tiles to fill the SMs
+enum PlanKind : int { kGatherPlan = 0, kBoxPlan = 1, kPointwisePlan = 2 };
+
+struct ConvPlan {
+  int kind = kGatherPlan;
+  bool tf32 = true;
+  long long kp = 0;          // packed filter row length (elements)
+  size_t filt_bytes = 0;     // packed filter
+  size_t in_bytes = 0;       // converted / compacted input copy
+  size_t part_bytes = 0;     // split-K partial tiles
+  int cg = 2, bn = 0, splits = 1, kb_per = 0, num_kb = 0;
+  // kBoxPlan layout
+  bool halo = false, pix_on_n = false;
+  BoxShape bx{};
+  int num_m = 0, num_n = 0;
+};
+
+// Split-K count from a small cost model (times in us, B200 at ~1.9 GHz):
+// a unit of kb slabs costs kb * max(MMA, operand-feed) + 1 (fill + epilogue),
+// units run in waves over the SM pairs, and a split adds the reduction pass
+// (launch + every partial read once and the output written, ~4 TB/s).  The
+// partials must stay under `cap` bytes.
+int choose_splits(long long units, int num_kb, long long pairs, int bm, int bn,
+                  size_t out_bytes, size_t cap) {
+  const double mma_clk = 4.0 * (double)bm * bn * 8 / 3782.0;      // per slab, per pair
+  const double feed_clk = (double)(bm / 2 + bn / 2) * 128 / 70.0;  // bytes per SM / (B/clk)
+  const double slab_us = std::max(mma_clk, feed_clk) / 1900.0;
+  auto cost = [&](int s) {
+    const long long waves = (units * s + pairs - 1) / pairs;
+    const int kb = (num_kb + s - 1) / s;
+    double t = (double)waves * (kb * slab_us + 1.0);
+    if (s > 1) t += 2.0 + (double)(s + 1) * out_bytes / 4.0e6;
+    return t;
+  };
+  int best = 1;
+  double best_t = cost(1);
+  for (int s = 2; s <= 16 && num_kb / s >= 4; ++s) {
+    if ((size_t)s * out_bytes > cap) break;
+    const double t = cost(s);
+    if (t < best_t * 0.9) {
+      best = s;
+      best_t = t;
+    }
+  }
+  return best;
 }
 
-size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+void finish_splits(ConvPlan& c, int num_kb, int splits, size_t out_bytes, long long tiles) {
+  c.num_kb = num_kb;
+  c.splits = 1;
+  c.kb_per = num_kb;
+  if (splits > 1) {
+    c.kb_per = (num_kb + splits - 1) / splits;
+    c.splits = (num_kb + c.kb_per - 1) / c.kb_per;  // no empty split
+  }
+  (void)tiles;
+  if (c.splits > 1) c.part_bytes = align256((size_t)c.splits * out_bytes);
+}
+
+ConvPlan plan_conv(const ConvGeom& g, int precision) {
+  ConvPlan c;
+  const long long K = (long long)g.R * g.S * g.C;
+  const bool tf32 = precision == TK_PREC_TF32;
+  const int esize = tf32 ? 4 : 2, ek = kSlabBytes / esize;
+  const long long pix = (long long)g.N * g.OH * g.OW;
+  const char* force = getenv("TK_CONV_MODE");
+  const bool pointwise = g.R == 1 && g.S == 1 && g.pad_t == 0 && g.pad_l == 0 && g.C % 8 == 0 &&
+                         g.K % 4 == 0 && !(force && std::string(force) != "plain");
+  if (pointwise) {
+    c.kind = kPointwisePlan;
+    c.tf32 = tf32;
+    c.kp = (g.C + ek - 1) / ek * ek;
+    c.filt_bytes = align256((size_t)g.K * c.kp * esize);
+    c.in_bytes = (g.stride != 1 || !tf32) ? align256((size_t)pix * g.C * esize) : 0;
+    c.cg = pix > kRows ? 2 : 1;
+    const int step = 16 * c.cg;
+    c.bn = g.K >= 256 ? 256 : (g.K + step - 1) / step * step;
+    const long long pairs = sm_count() / c.cg;
+    auto units = [&](int bn) {
+      return ((pix + kRows * c.cg - 1) / (kRows * c.cg)) * ((g.K + bn - 1) / bn);
+    };
+    if (c.bn > 128 && units(c.bn) < pairs) c.bn = 128;
+    c.num_m = (int)((pix + kRows * c.cg - 1) / (kRows * c.cg));
+    c.num_n = (g.K + c.bn - 1) / c.bn;
+    const int num_kb = (int)(c.kp / ek);
+    const size_t out_bytes = (size_t)pix * g.K * 4;
+    finish_splits(c, num_kb,
+                  choose_splits(units(c.bn), num_kb, pairs, kRows * c.cg, c.bn, out_bytes,
+                                96ull << 20),
+                  out_bytes, (long long)c.num_m * c.num_n);
+    return c;
+  }
+  if (conv_boxable(g, precision)) {
+    c.kind = kBoxPlan;
+    c.tf32 = tf32;
+    c.kp = K;
+    c.filt_bytes = align256((size_t)g.K * K * esize);
+    c.in_bytes = tf32 ? 0 : align256((size_t)g.N * g.H * g.W * g.C * 2);
+    // Halo mode: small-feature stride-1 layers whose tap re-reads of the
+    // input would otherwise dominate the L2->SM traffic.
+    const bool halo_ok = g.stride == 1 && g.R * g.S <= 9 && g.S <= 3 && g.K % 32 == 0 &&
+                         ((g.K <= 128 && g.C <= 128) || (force && std::string(force).rfind("halo", 0) == 0));
+    c.halo = halo_ok && !(force && std::string(force).rfind("halo", 0) != 0);
+    c.num_kb = (int)(K / ek);
+    c.kb_per = c.num_kb;
+    if (c.halo) return c;
+    c.pix_on_n = g.K >= kRows;
+    c.cg = c.pix_on_n ? (g.K >= 2 * kRows ? 2 : 1) : 2;
+    c.bx = pick_box(g, c.pix_on_n, c.cg);
+    if (c.bx.wb == 0) return c;  // reported by the launcher
+    const long long pix_tiles = (long long)g.N * c.bx.tiles_w * c.bx.tiles_h;
+    if (c.pix_on_n) {
+      c.num_m = (g.K + kRows * c.cg - 1) / (kRows * c.cg);
+      c.num_n = (int)pix_tiles;
+      const size_t out_bytes = (size_t)g.N * g.OH * g.OW * g.K * 4;
+      const bool aligned = g.K % 4 == 0;
+      const long long pairs = sm_count() / c.cg;
+      const char* nosplit = getenv("TK_NO_SPLIT");
+      const int sp = (aligned && !(nosplit && nosplit[0] == '1'))
+                         ? choose_splits((long long)c.num_m * c.num_n, c.num_kb, pairs,
+                                         kRows * c.cg, c.bx.wb * c.bx.tileH, out_bytes, 64ull << 20)
+                         : 1;
+      finish_splits(c, c.num_kb, sp, out_bytes, (long long)c.num_m * c.num_n);
+    } else {
+      c.num_m = (int)pix_tiles;
+      c.num_n = 1;
+    }
+    return c;
+  }
+  c.kind = kGatherPlan;  // fp32 operands, kind::tf32 for every TC precision
+  c.tf32 = true;
+  c.kp = (K + 31) / 32 * 32;
+  c.filt_bytes = align256((size_t)g.K * c.kp * 4);
+  return c;
+}
+
+bool tf32_filter_rounding() {
+  const char* rnd = getenv("TK_TF32_ROUND");
+  return !(rnd && rnd[0] == '0');
+}
+
+// 1x1 convolution as a plain tensor-core GEMM (see plan_conv).
+void launch_pointwise(const ConvGeom& g, const ConvPlan& c, const float* in, const float* filt,
+                      float* out, char* ws, cudaStream_t st, bool prep, bool run) {
+  const int esize = c.tf32 ? 4 : 2, ek = kSlabBytes / esize;
+  char* cursor = ws;
+  void* ft = cursor;
+  cursor += c.filt_bytes;
+  float* part = reinterpret_cast<float*>(ws + c.filt_bytes + c.in_bytes);
+  if (prep) {
+    if (c.tf32) pack_filter<float>(filt, g.C, g.K, (int)c.kp, (float*)ft, tf32_filter_rounding(), st);
+    else pack_filter<__nv_bfloat16>(filt, g.C, g.K, (int)c.kp, (__nv_bfloat16*)ft, false, st);
+  }
+  if (!run) return;
+  const long long pix = (long long)g.N * g.OH * g.OW;
+  const void* a = in;
+  if (c.in_bytes) {
+    if (c.tf32) pointwise_gather<float>(in, g, (float*)cursor, st);
+    else pointwise_gather<__nv_bfloat16>(in, g, (__nv_bfloat16*)cursor, st);
+    a = cursor;
+    cursor += c.in_bytes;
+  }
+  float* dst = c.splits > 1 ? part : out;
+  if (pix > 2147483647ll) fail(TK_ERR_CAPABILITY, "tc_conv: too many output pixels");
+  TcArgs p{};
+  p.M = (int)pix;
+  p.N = g.K;
+  p.K = (int)c.kp;
+  p.BN = c.bn;
+  p.ek = ek;
+  p.num_m = c.num_m;
+  p.num_n = c.num_n;
+  p.batch = 1;
+  p.num_kb = c.num_kb;
+  p.splits = c.splits;
+  p.kb_per = c.kb_per;
+  p.d = out;
+  p.d_sm = g.K;
+  p.d_sn = 1;
+  p.part = part;
+  p.part_stride = pix * g.K;
+  p.alpha = 1.0f;
+  const CUtensorMap ma = map_rows(a, esize, g.C, pix, 1, 0, kRows);
+  const CUtensorMap mb = map_rows(ft, esize, c.kp, g.K, 1, 0, c.bn / c.cg);
+  cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)pix, (cuuint64_t)c.splits};
+  cuuint64_t strides[2] = {(cuuint64_t)g.K * 4, (cuuint64_t)(pix * g.K * 4)};
+  cuuint32_t box[3] = {32, (cuuint32_t)kRows, 1};
+  const CUtensorMap md = make_map(dst, 4, 3, dims, strides, box);
+  p.store_tma = 1;
+  p.epi_bufs = 2;
+  dispatch<kPlain>(ma, mb, md, p, c.cg, c.tf32, st);
+  if (c.splits > 1) splitk_reduce(part, pix * g.K, c.splits, out, st);
+}
 
 }  // namespace
 
 size_t tc_conv_workspace(const ConvGeom& g, int precision) {
-  const long long kp = conv_kp(g, precision);
-  const bool box = conv_boxable(g, precision);
-  const size_t esz = (box && precision == TK_PREC_BF16) ? 2 : 4;
-  size_t bytes = align256((size_t)g.K * kp * esz);
-  if (box && precision == TK_PREC_BF16) bytes += align256((size_t)g.N * g.H * g.W * g.C * 2);
-  return bytes;
+  const ConvPlan c = plan_conv(g, precision);
+  return c.filt_bytes + c.in_bytes + c.part_bytes;
 }
 
 void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float* out,
@@ -1101,11 +1468,15 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   require_tc(precision);
   const bool prep = (phase & kConvPrepare) != 0, run = (phase & kConvRun) != 0;
   const long long K = (long long)g.R * g.S * g.C;
-  const bool box = conv_boxable(g, precision);
-  const long long kp = conv_kp(g, precision);
+  const ConvPlan plan = plan_conv(g, precision);
+  const long long kp = plan.kp;
   char* cursor = static_cast<char*>(ws);
+  if (plan.kind == kPointwisePlan) {
+    launch_pointwise(g, plan, in, filt, out, cursor, st, prep, run);
+    return;
+  }
 
-  if (!box) {
+  if (plan.kind == kGatherPlan) {
     // Gather mode: the pixel operand is built in shared memory by producer
     // warps (any channel count / stride), the filter streams by TMA, the
     // output leaves through a TMA store.  fp32 operands, kind::tf32.
@@ -1159,8 +1530,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   const void* xin = in;
   if (tf32) {
     float* ft = reinterpret_cast<float*>(cursor);
-    const char* rnd = getenv("TK_TF32_ROUND");
-    if (prep) pack_filter<float>(filt, (int)K, g.K, (int)kp, ft, !(rnd && rnd[0] == '0'), st);
+    if (prep) pack_filter<float>(filt, (int)K, g.K, (int)kp, ft, tf32_filter_rounding(), st);
     fa = ft;
   } else {
     __nv_bfloat16* ft = reinterpret_cast<__nv_bfloat16*>(cursor);
@@ -1171,15 +1541,11 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     fa = ft;
     xin = xb;
   }
-  if (!run) return;
 
-  // Halo mode: small-feature stride-1 layers whose tap re-reads of the
-  // input would otherwise dominate the L2->SM traffic.
+  float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + plan.filt_bytes + plan.in_bytes);
+  if (!run) return;
   const char* force = getenv("TK_CONV_MODE");
-  const bool halo_ok = g.stride == 1 && g.R * g.S <= 9 && g.S <= 3 && g.K % 32 == 0 &&
-                       ((g.K <= 128 && g.C <= 128) ||
-                        (force && std::string(force) == "halo"));
-  const bool use_halo = halo_ok && !(force && std::string(force) != "halo");
+  const bool use_halo = plan.halo;
   if (use_halo) {
     const int cg = 2;
     TcArgs p{};
@@ -1232,9 +1598,9 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     return;
   }
 
-  const bool pix_on_n = g.K >= kRows;
-  const int cg = pix_on_n ? (g.K >= 2 * kRows ? 2 : 1) : 2;
-  const BoxShape bx = pick_box(g, pix_on_n, cg);
+  const bool pix_on_n = plan.pix_on_n;
+  const int cg = plan.cg;
+  const BoxShape bx = plan.bx;
   if (bx.wb == 0) fail(TK_ERR_CAPABILITY, "tc_conv: no pixel box fits this output plane");
   TcArgs p{};
   p.K = (int)K;
@@ -1262,9 +1628,14 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     p.N = p.BN * pix_tiles;
     p.num_m = (g.K + kRows * cg - 1) / (kRows * cg);
     p.num_n = pix_tiles;
+    p.splits = plan.splits;
+    p.kb_per = plan.kb_per;
+    p.part = part;
+    p.part_stride = (long long)g.N * g.OH * g.OW * g.K;
     const CUtensorMap ma = map_rows2d(fa, esize, kp, g.K, kRows);
     const CUtensorMap mb = map_nhwc(xin, esize, g, bx.wb, bx.boxH);
     dispatch<kConvPixN>(ma, mb, ma, p, cg, tf32, st);
+    if (p.splits > 1) splitk_reduce(part, p.part_stride, p.splits, out, st);
   } else {
     p.BN = (g.K + 16 * cg - 1) / (16 * cg) * (16 * cg);
     p.M = kRows * cg * pix_tiles;

@@ -69,12 +69,13 @@ def test_resnet_layer_exact(tk, oracle, row):
 
 
 @pytest.mark.timeout(120)
-def test_gather_mode_many_tiles_many_slabs(tk, oracle):
+def test_gather_mode_many_tiles_many_slabs(tk, oracle, monkeypatch):
     """Regression: res3a_branch2a (1x1/s2, C=256) at batch 32 runs the gather
     producer with several tiles per CTA and more K-slabs per tile than
     pipeline stages (the configuration that once deadlocked).  Images 0 and
     31 are checked against single-image oracle runs."""
     import torch
+    monkeypatch.setenv("TK_CONV_MODE", "gather")  # 1x1 layers default to the pointwise GEMM
     N, H, C, K = 32, 56, 256, 128
     s = tk.ConvShape(N, H, H, C, K, 1, 1, 2, True)
     gen = torch.Generator(device="cuda").manual_seed(3)
@@ -88,3 +89,33 @@ def test_gather_mode_many_tiles_many_slabs(tk, oracle):
         conv = oracle.Conv(1, H, H, C, K, 1, 1, 2, True)
         want = oracle.conv2d_naive(conv, dx[img:img + 1].cpu().numpy(), f)
         assert oracle.max_scaled_error(dy[img:img + 1].cpu().numpy(), want) <= TOL["tf32"]
+
+
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("row", [RESNET[20], RESNET[19], RESNET[15], RESNET[13]],
+                         ids=["res5b_branch2a", "res5a_branch1", "res4b_branch2a",
+                              "res4a_branch2c"])
+def test_pointwise_full_batch_split_k(tk, oracle, row, prec):
+    """1x1 layers at batch 32 run as a plain GEMM on the NHWC input, split
+    over K with a deterministic reduction where the output has few tiles:
+    images 0 and 31 against the oracle, and two runs bit-identical."""
+    import torch
+    name, r, stride, (h, w, c), (oh, ow, k) = row
+    N = 32
+    s = tk.ConvShape(N, h, w, c, k, 1, 1, stride, True)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    dx = torch.rand((N, h, w, c), device="cuda", generator=gen) * 2 - 1
+    df = torch.rand((1, 1, c, k), device="cuda", generator=gen) * 2 - 1
+    ys = []
+    for _ in range(2):
+        dy = torch.full(s.out_shape, float("nan"), device="cuda")
+        tk.conv2d_dev(dx, df, dy, s, tk.parse_conv_params("im2col"), precision=prec)
+        ys.append(dy)
+    torch.cuda.synchronize()
+    assert torch.equal(ys[0].view(torch.int32), ys[1].view(torch.int32))
+    f = df.cpu().numpy()
+    for img in (0, N - 1):
+        conv = oracle.Conv(1, h, w, c, k, 1, 1, stride, True)
+        want = oracle.conv2d_naive(conv, dx[img:img + 1].cpu().numpy(), f)
+        assert oracle.max_scaled_error(ys[0][img:img + 1].cpu().numpy(), want) <= TOL[prec]

@@ -21,6 +21,9 @@ ap.add_argument("prec", nargs="?", default="tf32")
 ap.add_argument("batch", nargs="?", type=int, default=32)
 ap.add_argument("--only", default="")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--flush", default="read", choices=["read", "write"],
+                help="evict L2 by reading (clean lines) or writing (dirty lines whose "
+                     "write-back then lands on the timed kernel) a 256 MiB buffer")
 a = ap.parse_args()
 
 rows = []
@@ -30,7 +33,8 @@ if a.which in ("resnet50", "all"):
     rows += [(n, r, s, h, c, k) for n, r, s, h, c, k, _ in bench.RESNET50]
 peaks, _ = bench.load_peaks()
 peak = peaks["bf16_tflops"] / (2.0 if a.prec == "tf32" else 1.0)
-flush = torch.empty(64 << 20, device="cuda")
+flush = torch.ones(64 << 20, device="cuda")
+flush_sink = torch.empty((), device="cuda")
 p = tk.parse_conv_params("im2col")
 st = torch.cuda.Stream()
 print(f"{'layer':18s} {'us':>8s} {'TF/s':>8s} {'%peak':>6s}  ({a.prec}, batch {a.batch}, peak {peak:.0f})")
@@ -49,7 +53,10 @@ for name, r, s, h, c, k in rows:
         tk.conv2d_run_dev(x, f, y, shp, p, ws, precision=a.prec, stream=st)
     ts = []
     for i in range(a.reps + 2):
-        flush.zero_()
+        if a.flush == "write":
+            flush.zero_()
+        else:
+            flush_sink.copy_(flush.sum())
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         with torch.cuda.stream(st):  # replay() launches on the current stream
