@@ -93,6 +93,9 @@ struct TcArgs {
   // partials in split order (deterministic, no atomics) into the output.
   float* part;
   long long part_stride;
+  // L2-aware raster (plain / pixN): tiles are visited in groups of `raster`
+  // M-blocks, N-blocks within a group, so a wave of CTAs shares A and B tiles.
+  int raster;
   // Timeline probe (TK_TC_TRACE=1, experiments only): per CTA, globaltimer
   // stamps of kTraceEvents milestones.
   unsigned long long* trace;
@@ -114,10 +117,21 @@ struct Unit {
 
 __device__ __forceinline__ Unit decode_unit(const TcArgs& p, int t) {
   Unit u;
-  u.m_blk = t % p.num_m;
-  int rest = t / p.num_m;
-  u.n_blk = rest % p.num_n;
-  rest /= p.num_n;
+  const int per = p.num_m * p.num_n;
+  int rest = t / per;
+  const int t2 = t - rest * per;
+  if (p.raster > 1) {
+    const int span = p.raster * p.num_n;
+    const int group = t2 / span;
+    const int first_m = group * p.raster;
+    const int gsize = min(p.num_m - first_m, p.raster);
+    const int local = t2 - group * span;
+    u.m_blk = first_m + local % gsize;
+    u.n_blk = local / gsize;
+  } else {
+    u.m_blk = t2 % p.num_m;
+    u.n_blk = t2 / p.num_m;
+  }
   u.z = rest % p.batch;
   u.sp = rest / p.batch;
   u.kb0 = u.sp * p.kb_per;
@@ -789,6 +803,17 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     p.splits = 1;
     p.kb_per = p.num_kb;
   }
+  {
+    static const int raster = [] {
+      const char* e = getenv("TK_RASTER");
+      return e ? atoi(e) : 8;
+    }();
+    const long long units_all = (long long)p.num_m * p.num_n * p.batch * p.splits;
+    // Grouping only pays once tiles queue up behind the resident wave.
+    p.raster = ((MODE == kPlain || MODE == kConvPixN) && units_all > 2LL * (sm_count() / CG))
+                   ? raster
+                   : 0;
+  }
   const long long total = (long long)p.num_m * p.num_n * p.batch * p.splits;
   const int units = sm_count() / CG;
   int used = (int)(total < units ? total : units);
@@ -911,9 +936,102 @@ __global__ void __launch_bounds__(256) pack_kmajor_kernel(const float* __restric
   }
 }
 
+// Row-contiguous source (ks == 1): dst[r][kk] = src[r*rs + kk], 4 elements
+// per thread, vector loads and stores, zero tail up to kp.
+template <typename T>
+__global__ void __launch_bounds__(256) pack_rows_kernel(const float* __restrict__ src, long long rs,
+                                                        long long rows, long long k, long long kp,
+                                                        T* __restrict__ dst, int tf32_round) {
+  const long long per_row = kp / 4;
+  const long long total = rows * per_row;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / per_row, kk = (i - r * per_row) * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (kk + 3 < k) v = __ldcs(reinterpret_cast<const float4*>(src + r * rs + kk));
+    else {
+      if (kk < k) v.x = src[r * rs + kk];
+      if (kk + 1 < k) v.y = src[r * rs + kk + 1];
+      if (kk + 2 < k) v.z = src[r * rs + kk + 2];
+    }
+    T* d = dst + r * kp + kk;
+    if constexpr (sizeof(T) == 4) {
+      *reinterpret_cast<float4*>(d) = make_float4(cvt_out<float>(v.x, tf32_round), cvt_out<float>(v.y, tf32_round),
+                                                  cvt_out<float>(v.z, tf32_round), cvt_out<float>(v.w, tf32_round));
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&lo);
+      u.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(d) = u;
+    }
+  }
+}
+
+// dst[r][kk] = src[r + kk*ks] for a 64-row x 64-k tile per block: float4
+// loads along r, float4 (fp32) / 8-byte (bf16) stores along kk.
+template <typename T>
+__global__ void __launch_bounds__(256) pack_transpose_kernel(const float* __restrict__ src,
+                                                             long long ks, long long rows,
+                                                             long long k, long long kp,
+                                                             T* __restrict__ dst, int tf32_round) {
+  __shared__ float tile[64][65];  // [kk][r]
+  const long long r0 = (long long)blockIdx.y * 64, k0 = (long long)blockIdx.x * 64;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int kk = t / 16 + 16 * j, r4 = (t % 16) * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k0 + kk < k && r0 + r4 < rows)  // rows % 4 == 0: whole float4 in range
+      v = __ldcs(reinterpret_cast<const float4*>(src + (k0 + kk) * ks + r0 + r4));
+    tile[kk][r4] = v.x;
+    tile[kk][r4 + 1] = v.y;
+    tile[kk][r4 + 2] = v.z;
+    tile[kk][r4 + 3] = v.w;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int r = t / 16 + 16 * j, kk4 = (t % 16) * 4;
+    if (r0 + r >= rows || k0 + kk4 >= kp) continue;
+    const float a = tile[kk4][r], b = tile[kk4 + 1][r], c = tile[kk4 + 2][r], d = tile[kk4 + 3][r];
+    T* o = dst + (r0 + r) * kp + k0 + kk4;
+    if constexpr (sizeof(T) == 4) {
+      *reinterpret_cast<float4*>(o) = make_float4(cvt_out<float>(a, tf32_round), cvt_out<float>(b, tf32_round),
+                                                  cvt_out<float>(c, tf32_round), cvt_out<float>(d, tf32_round));
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&lo);
+      u.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(o) = u;
+    }
+  }
+}
+
 template <typename T>
 void pack_kmajor(const float* src, long long rs, long long ks, long long rows, long long k,
                  long long kp, T* dst, bool tf32_round, cudaStream_t st) {
+  const bool src16 = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  // Column-contiguous source (a column-major operand read along its rows):
+  // 64 x 64 tiles transposed through shared memory with 16-byte accesses
+  // on both sides.
+  if (rs == 1 && ks % 4 == 0 && rows % 4 == 0 && kp % 4 == 0 && src16) {
+    dim3 grid((unsigned)((kp + 63) / 64), (unsigned)((rows + 63) / 64));
+    if (grid.y > 65535) fail(TK_ERR_CAPABILITY, "pack: too many rows");
+    pack_transpose_kernel<T><<<grid, 256, 0, st>>>(src, ks, rows, k, kp, dst, tf32_round ? 1 : 0);
+    note_launch();
+    TKB_CUDA(cudaGetLastError());
+    return;
+  }
+  if (ks == 1 && rs % 4 == 0 && kp % 4 == 0 && src16) {
+    const long long n = rows * (kp / 4);
+    const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sm_count() * 16);
+    pack_rows_kernel<T><<<blocks, 256, 0, st>>>(src, rs, rows, k, kp, dst, tf32_round ? 1 : 0);
+    note_launch();
+    TKB_CUDA(cudaGetLastError());
+    return;
+  }
   dim3 grid((unsigned)((kp + 31) / 32), (unsigned)((rows + 31) / 32));
   if (grid.y > 65535) fail(TK_ERR_CAPABILITY, "pack: too many rows");
   pack_kmajor_kernel<T><<<grid, dim3(32, 8), 0, st>>>(src, rs, ks, rows, k, kp, dst, tf32_round);

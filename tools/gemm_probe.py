@@ -17,7 +17,7 @@ for m, n, k in shapes:
     a = torch.rand(m * k, device="cuda") - 0.5
     b = torch.rand(k * n, device="cuda") - 0.5
     c = torch.empty(m * n, device="cuda")
-    shape = tk.GemmShape(m, n, k, 1.0, 0.0, "t", "n")
+    shape = tk.GemmShape(m, n, k, 1.0, 0.0, os.environ.get("TA", "t"), "n")
     for tn in (0, 64, 128, 256):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=st):
