@@ -96,6 +96,13 @@ struct TcArgs {
   // L2-aware raster (plain / pixN): tiles are visited in groups of `raster`
   // M-blocks, N-blocks within a group, so a wave of CTAs shares A and B tiles.
   int raster;
+  // Wave-quantisation tail (plain / pixN, splits == 1): tiles >= tail_start
+  // (the last partial wave) are cut into tail_q K-pieces of tail_kb slabs so
+  // the final wave spreads over every SM pair; each piece stores its
+  // partial tile column-major (tile-local, [BN][128] per CTA) in tail_part,
+  // and tail_reduce sums the pieces in order into the output.
+  int tail_start, tail_q, tail_kb;
+  float* tail_part;
   // Timeline probe (TK_TC_TRACE=1, experiments only): per CTA, globaltimer
   // stamps of kTraceEvents milestones.
   unsigned long long* trace;
@@ -113,10 +120,19 @@ __device__ __forceinline__ void trace_mark(const TcArgs& p, int ev) {
 // Work unit t -> (m_blk, n_blk, z, split) and its K-slab range.
 struct Unit {
   int m_blk, n_blk, z, sp, kb0, kb1;
+  int slot;  // tail piece slot (-1: a whole tile)
 };
 
 __device__ __forceinline__ Unit decode_unit(const TcArgs& p, int t) {
   Unit u;
+  u.slot = -1;
+  int piece = -1;
+  if (p.tail_q > 1 && t >= p.tail_start) {
+    const int d = t - p.tail_start;
+    piece = d % p.tail_q;
+    u.slot = d;
+    t = p.tail_start + d / p.tail_q;
+  }
   const int per = p.num_m * p.num_n;
   int rest = t / per;
   const int t2 = t - rest * per;
@@ -136,7 +152,26 @@ __device__ __forceinline__ Unit decode_unit(const TcArgs& p, int t) {
   u.sp = rest / p.batch;
   u.kb0 = u.sp * p.kb_per;
   u.kb1 = min(p.num_kb, u.kb0 + p.kb_per);
+  if (piece >= 0) {
+    u.kb0 = piece * p.tail_kb;
+    u.kb1 = min(p.num_kb, u.kb0 + p.tail_kb);
+  }
   return u;
+}
+
+// Tail piece epilogue: this thread's accumulator row (TMEM lane `row`) into
+// the slot's column-major [BN][128] partial tile (lanes = consecutive rows:
+// coalesced 128-byte stores per column).
+__device__ __forceinline__ void store_tail_piece(const TcArgs& p, uint32_t taddr, int slot,
+                                                 uint32_t rank, int cg, int row) {
+  float* dst = p.tail_part + ((long long)slot * cg + rank) * ((long long)p.BN * 128);
+  for (int col = 0; col < p.BN; col += 32) {
+    float v[32];
+    ptx::tmem_ld32(taddr + col, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col + j < p.BN) dst[(long long)(col + j) * 128 + row] = v[j];
+  }
 }
 
 
@@ -370,7 +405,9 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   ptx::griddep_wait();
   if (threadIdx.x == 0) trace_mark(p, 1);  // barriers + TMEM ready
 
-  const int total = p.num_m * p.num_n * p.batch * p.splits;
+  const int total = p.tail_q > 1
+                        ? p.tail_start + (p.num_m * p.num_n * p.batch - p.tail_start) * p.tail_q
+                        : p.num_m * p.num_n * p.batch * p.splits;
   const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
 
   if (MODE == kConvHalo && warp == 0) {
@@ -598,6 +635,16 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       if (local == 1 && warp == 2 && lane == 0) trace_mark(p, 5);  // second accumulator ready
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
 
+      if ((MODE == kPlain || MODE == kConvPixN) && u.slot >= 0) {
+        store_tail_piece(p, taddr, u.slot, rank, CG, row);
+        ptx::tc_fence_before();
+        ptx::named_sync(1, 128);
+        if (warp == 2 && lane == 0) {
+          if constexpr (CG == 2) ptx::mbar_arrive_cluster(empty_base + 8u * acc);
+          else ptx::mbar_arrive(&tmem_empty[acc]);
+        }
+        continue;
+      }
       if constexpr (MODE == kConvHalo) {
         const int hn = t % p.num_n, hm = t / p.num_n;
         const PixTile pt = pix_tile(p, hm);
@@ -767,6 +814,100 @@ int sm_count() {
   return n;
 }
 
+// Sum the tail pieces of each tail tile in piece order into the output.
+// Block = (tail tile r, CTA rank, 8 columns); thread = one column x 4 rows
+// (float4 along the column-major partial).  pixN: row = output feature,
+// column = pixel of the tile's box (features are contiguous in NHWC: float4
+// stores); plain: row = M index, column = N index.
+template <int MODE, int CG>
+__global__ void __launch_bounds__(256) tail_reduce_kernel(TcArgs p) {
+  const int col_blocks = (p.BN + 7) / 8;
+  const int r = blockIdx.x / (CG * col_blocks);
+  const int rem = blockIdx.x - r * CG * col_blocks;
+  const int rank = rem / col_blocks;
+  const int col = (rem - rank * col_blocks) * 8 + threadIdx.x / 32;
+  const int row = (threadIdx.x % 32) * 4;
+  if (col >= p.BN) return;
+  const Unit u = decode_unit(p, p.tail_start + r * p.tail_q);
+  const long long tile = (long long)p.BN * 128;
+  const float* src =
+      p.tail_part + ((long long)r * p.tail_q * CG + rank) * tile + (long long)col * 128 + row;
+  float4 a = __ldcs(reinterpret_cast<const float4*>(src));
+  for (int q = 1; q < p.tail_q; ++q) {
+    const float4 b = __ldcs(reinterpret_cast<const float4*>(src + (long long)q * CG * tile));
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+  }
+  const int m = u.m_blk * kRows * CG + rank * kRows + row;
+  if constexpr (MODE == kConvPixN) {
+    const PixTile pt = pix_tile(p, u.n_blk);
+    const int h = col / p.Wb, w = col - (col / p.Wb) * p.Wb;
+    const int oh = pt.oh0 + h, ow = pt.ow0 + w;
+    if (oh >= p.OH || ow >= p.OW) return;
+    float* o = p.d + (((long long)pt.img * p.OH + oh) * p.OW + ow) * p.Kout + m;
+    if (m + 3 < p.Kout && (p.Kout & 3) == 0) {
+      *reinterpret_cast<float4*>(o) = a;
+    } else {
+      const float v[4] = {a.x, a.y, a.z, a.w};
+      for (int i = 0; i < 4; ++i)
+        if (m + i < p.Kout) o[i] = v[i];
+    }
+  } else {
+    const int n = u.n_blk * p.BN + col;
+    if (n >= p.N) return;
+    const float v[4] = {a.x, a.y, a.z, a.w};
+    for (int i = 0; i < 4; ++i)
+      if (m + i < p.M)
+        p.d[(long long)u.z * p.d_batch + (long long)(m + i) * p.d_sm + (long long)n * p.d_sn] =
+            p.alpha * v[i];
+  }
+}
+
+inline long long total_tiles_of(const TcArgs& p) { return (long long)p.num_m * p.num_n * p.batch; }
+
+struct TailPlan {
+  int start = 0, q = 0, kb = 0;
+  size_t bytes = 0;
+};
+
+// Wave-quantisation tail: with T tiles on P SM pairs, the last T % P tiles
+// would run as a partial wave as long as a full one; cut each into q <= P /
+// (T % P) K-pieces instead when the cost model (same constants as
+// choose_splits: per-slab max(MMA, operand feed), ~1 us per unit, the
+// reduction pass at ~4 TB/s + launch) says the shorter final round pays.
+TailPlan plan_tail(long long tiles, int num_kb, int cg, int bn) {
+  TailPlan t;
+  static const bool off = [] {
+    const char* e = getenv("TK_TAIL");
+    return e && e[0] == '0';
+  }();
+  const long long pairs = sm_count() / cg;
+  const long long rem = tiles % pairs, full = tiles / pairs;
+  if (off || rem == 0 || full < 1 || num_kb < 8) return t;
+  const int bm = kRows * cg;
+  const double mma_clk = 4.0 * (double)bm * bn * 8 / 3782.0;
+  const double feed_clk = (double)(bm / 2 + bn / 2) * 128 / 70.0;
+  const double slab_us = std::max(mma_clk, feed_clk) / 1900.0;
+  const double tile_bytes = (double)bm * bn * 4;
+  const double base = num_kb * slab_us + 1.0;
+  double best = base * 0.85;  // demand a clear win
+  for (int q = 2; q <= pairs / rem && num_kb / q >= 4; ++q) {
+    const int kb = (num_kb + q - 1) / q;
+    const double cost = kb * slab_us + 1.0 + 2.0 + (q + 1) * rem * tile_bytes / 4.0e6;
+    if (cost < best) {
+      best = cost;
+      t.q = (num_kb + kb - 1) / kb;
+      t.kb = kb;
+    }
+  }
+  if (t.q < 2) return TailPlan{};
+  t.start = (int)(tiles - rem);
+  t.bytes = (size_t)rem * t.q * cg * bn * 128 * 4;
+  return t;
+}
+
 template <int MODE, int CG, bool TF32>
 void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, TcArgs p,
                 int stages_req, cudaStream_t st) {
@@ -814,7 +955,10 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
                    ? raster
                    : 0;
   }
-  const long long total = (long long)p.num_m * p.num_n * p.batch * p.splits;
+  if (p.tail_q > 1 && (p.splits > 1 || (MODE != kPlain && MODE != kConvPixN))) p.tail_q = 0;
+  const long long total =
+      p.tail_q > 1 ? (long long)p.tail_start + (total_tiles_of(p) - p.tail_start) * p.tail_q
+                   : (long long)p.num_m * p.num_n * p.batch * p.splits;
   const int units = sm_count() / CG;
   int used = (int)(total < units ? total : units);
   // Halo mode with a resident filter: every CTA must keep one feature block.
@@ -848,6 +992,15 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   }
   TKB_CUDA(cudaLaunchKernelEx(&cfg, fn, ma, mb, md, p));
   note_launch();
+  if constexpr (MODE == kPlain || MODE == kConvPixN) {
+    if (p.tail_q > 1) {
+      const long long rem = total_tiles_of(p) - p.tail_start;
+      const long long blocks = rem * CG * ((p.BN + 7) / 8);
+      tail_reduce_kernel<MODE, CG><<<(unsigned)blocks, 256, 0, st>>>(p);
+      note_launch();
+      TKB_CUDA(cudaGetLastError());
+    }
+  }
   if (trace) {
     std::vector<unsigned long long> h((size_t)grid * kTraceEvents);
     TKB_CUDA(cudaStreamSynchronize(st));
@@ -1314,7 +1467,19 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
     p.store_tma = 1;
     p.epi_bufs = 2;
   }
+  void* tail_buf = nullptr;
+  if (!p.read_c) {
+    const TailPlan tp = plan_tail((long long)p.num_m * p.num_n * p.batch, p.num_kb, cg, bn);
+    if (tp.q > 1) {
+      TKB_CUDA(cudaMallocAsync(&tail_buf, tp.bytes, st));
+      p.tail_start = tp.start;
+      p.tail_q = tp.q;
+      p.tail_kb = tp.kb;
+      p.tail_part = static_cast<float*>(tail_buf);
+    }
+  }
   dispatch<kPlain>(ma, mb, md, p, cg, tf32, st);
+  if (tail_buf) cudaFreeAsync(tail_buf, st);
 }
 
 void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float beta, bool ta,
@@ -1391,6 +1556,7 @@ struct ConvPlan {
   size_t in_bytes = 0;       // converted / compacted input copy
   size_t part_bytes = 0;     // split-K partial tiles
   int cg = 2, bn = 0, splits = 1, kb_per = 0, num_kb = 0;
+  TailPlan tail{};           // wave-quantisation tail (plain / pixN)
   // kBoxPlan layout
   bool halo = false, pix_on_n = false;
   BoxShape bx{};
@@ -1470,6 +1636,7 @@ ConvPlan plan_conv(const ConvGeom& g, int precision) {
                   choose_splits(units(c.bn), num_kb, pairs, kRows * c.cg, c.bn, out_bytes,
                                 96ull << 20),
                   out_bytes, (long long)c.num_m * c.num_n);
+    if (c.splits == 1) c.tail = plan_tail((long long)c.num_m * c.num_n, c.num_kb, c.cg, c.bn);
     return c;
   }
   if (conv_boxable(g, precision)) {
@@ -1503,6 +1670,8 @@ ConvPlan plan_conv(const ConvGeom& g, int precision) {
                                          kRows * c.cg, c.bx.wb * c.bx.tileH, out_bytes, 64ull << 20)
                          : 1;
       finish_splits(c, c.num_kb, sp, out_bytes, (long long)c.num_m * c.num_n);
+      if (c.splits == 1)
+        c.tail = plan_tail((long long)c.num_m * c.num_n, c.num_kb, c.cg, c.bx.wb * c.bx.tileH);
     } else {
       c.num_m = (int)pix_tiles;
       c.num_n = 1;
@@ -1562,6 +1731,12 @@ void launch_pointwise(const ConvGeom& g, const ConvPlan& c, const float* in, con
   p.part = part;
   p.part_stride = pix * g.K;
   p.alpha = 1.0f;
+  if (c.tail.q > 1) {
+    p.tail_start = c.tail.start;
+    p.tail_q = c.tail.q;
+    p.tail_kb = c.tail.kb;
+    p.tail_part = reinterpret_cast<float*>(reinterpret_cast<char*>(part) + c.part_bytes);
+  }
   const CUtensorMap ma = map_rows(a, esize, g.C, pix, 1, 0, kRows);
   const CUtensorMap mb = map_rows(ft, esize, c.kp, g.K, 1, 0, c.bn / c.cg);
   cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)pix, (cuuint64_t)c.splits};
@@ -1578,7 +1753,7 @@ void launch_pointwise(const ConvGeom& g, const ConvPlan& c, const float* in, con
 
 size_t tc_conv_workspace(const ConvGeom& g, int precision) {
   const ConvPlan c = plan_conv(g, precision);
-  return c.filt_bytes + c.in_bytes + c.part_bytes;
+  return c.filt_bytes + c.in_bytes + c.part_bytes + align256(c.tail.bytes);
 }
 
 void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float* out,
@@ -1750,6 +1925,12 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     p.kb_per = plan.kb_per;
     p.part = part;
     p.part_stride = (long long)g.N * g.OH * g.OW * g.K;
+    if (plan.tail.q > 1) {
+      p.tail_start = plan.tail.start;
+      p.tail_q = plan.tail.q;
+      p.tail_kb = plan.tail.kb;
+      p.tail_part = reinterpret_cast<float*>(reinterpret_cast<char*>(part) + plan.part_bytes);
+    }
     const CUtensorMap ma = map_rows2d(fa, esize, kp, g.K, kRows);
     const CUtensorMap mb = map_nhwc(xin, esize, g, bx.wb, bx.boxH);
     dispatch<kConvPixN>(ma, mb, ma, p, cg, tf32, st);
