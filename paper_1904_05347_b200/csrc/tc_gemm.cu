@@ -54,10 +54,13 @@ constexpr int kMaxStages = 8;
 
 enum TcMode : int { kPlain = 0, kConvPixN = 1, kConvPixM = 2, kConvGather = 3, kConvHalo = 4 };
 
+#ifndef TKB_GATHER_GROUPS
+#define TKB_GATHER_GROUPS 2
+#endif
 // Gather mode adds kGatherGroups x 4 producer warps (6..) that build the
 // pixel operand; groups take alternate K-slabs so their load latencies
 // overlap.
-constexpr int kGatherGroups = 2;
+constexpr int kGatherGroups = TKB_GATHER_GROUPS;
 template <int MODE>
 constexpr int threads_of() {
   return MODE == kConvGather ? kThreads + 128 * kGatherGroups : kThreads;
@@ -613,7 +616,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         }
         ktab[k] = e;
       }
-      ptx::named_sync(4, 128 * kGatherGroups);
+      ptx::named_sync(2 + kGatherGroups, 128 * kGatherGroups);  // after the group barriers
     }
     gather_producer<CG>(p, base, stage_bytes, full, empty, ktab, warp, lane, rank, unit, nunits,
                         total);
