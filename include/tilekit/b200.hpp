@@ -25,17 +25,46 @@ enum class Precision {
   Tf32x3 = TK_PREC_3XTF32,         // split-precision TF32
 };
 
+// Tensor-core convolution operand path (tk_tc_mode).
+enum class TcMode {
+  Auto = TK_TC_AUTO,
+  Halo = TK_TC_HALO,
+  PixN = TK_TC_PIXN,
+  PixM = TK_TC_PIXM,
+  Gather = TK_TC_GATHER,
+  Pointwise = TK_TC_POINTWISE,
+};
+
 struct ExecOptions {
   Precision precision = Precision::Fp32Exact;
-  int tc_tile_n = 0;  // 0 = auto
-  int tc_stages = 0;  // 0 = auto
+  int tc_tile_n = 0;   // GEMM N tile, 0 = auto
+  int tc_stages = 0;   // shared-memory ring depth, 0 = auto
+  int tc_cluster = 0;  // 1 = one SM, 2 = CTA pair, 0 = auto
+  TcMode tc_mode = TcMode::Auto;
+  int tc_split = 0;    // 0 = cost model, 1 = never split K, n > 1 = n splits
 
   tk_exec_options c() const {
     tk_exec_options o{};
     o.precision = static_cast<int>(precision);
     o.tc_tile_n = tc_tile_n;
     o.tc_stages = tc_stages;
+    o.tc_cluster = tc_cluster;
+    o.tc_mode = static_cast<int>(tc_mode);
+    o.tc_split = tc_split;
     return o;
+  }
+
+  // Config-name suffix of the non-default knobs, e.g. "_n128_s4_c1_halo".
+  std::string suffix() const {
+    static const char* modes[] = {"", "_halo", "_pixn", "_pixm", "_gather", "_pointwise"};
+    std::string s;
+    if (tc_tile_n) s += "_n" + std::to_string(tc_tile_n);
+    if (tc_stages) s += "_s" + std::to_string(tc_stages);
+    if (tc_cluster) s += "_c" + std::to_string(tc_cluster);
+    s += modes[static_cast<int>(tc_mode)];
+    if (tc_split == 1) s += "_nosplit";
+    else if (tc_split > 1) s += "_k" + std::to_string(tc_split);
+    return s;
   }
 };
 

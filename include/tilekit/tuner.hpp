@@ -91,7 +91,10 @@ struct ParamSpace {
   // B200 axes (b200::tune only)
   std::vector<b200::Precision> precisions{b200::Precision::Fp32Exact, b200::Precision::Tf32,
                                           b200::Precision::Bf16};
-  std::vector<int> tc_tiles{0};  // 0 = library choice
+  std::vector<int> tc_tiles{0};  // GEMM N tile, 0 = library choice
+  std::vector<int> tc_stages{0};     // shared-memory ring depth, 0 = library choice
+  std::vector<int> tc_clusters{0};   // 1 = one SM, 2 = CTA pair, 0 = library choice
+  std::vector<b200::TcMode> tc_modes{b200::TcMode::Auto};  // conv operand path
 };
 
 inline std::vector<GemmConfig> stock_gemm_configs() {
@@ -218,6 +221,13 @@ struct TuningRecord {
   std::int64_t mean_ns = 0;
   double gflops = 0.0;
   bool valid = true;
+  // B200 additions (extra NDJSON keys the reference's load_db ignores):
+  // the throughput as a fraction of the precision's nominal dense peak
+  // (tensor pipe for TF32/BF16, the FMUL+FADD issue cap for exact FP32) and
+  // the compulsory-traffic bandwidth (operands once, result once; the
+  // analysis.hpp model) over the median time.
+  double frac_of_peak = 0.0;
+  double algo_gbs = 0.0;
 
   bool operator==(const TuningRecord&) const = default;
 };
@@ -308,6 +318,27 @@ inline Tensor4 sized(Tensor4Layout l, std::size_t a, std::size_t b, std::size_t 
   return t;
 }
 
+// Nominal dense peaks of a B200 (TF/s) per precision.
+inline double nominal_peak_tflops(b200::Precision p) {
+  switch (p) {
+    case b200::Precision::Tf32: return 1125.0;
+    case b200::Precision::Bf16: return 2250.0;
+    case b200::Precision::Tf32x3: return 375.0;
+    default: return 148 * 128 * 1.965e-3;  // one FMUL + one FADD per MAC: half of FFMA
+  }
+}
+
+inline double compulsory_bytes(const Problem& p) {
+  if (p.kind == Problem::Kind::Gemm) {
+    const double m = (double)p.gemm.m, n = (double)p.gemm.n, k = (double)p.gemm.k;
+    return 4.0 * (m * k + k * n + m * n * (p.gemm.beta != 0.0f ? 2.0 : 1.0));
+  }
+  const ConvShape& c = p.conv;
+  return 4.0 * ((double)c.batch * c.in_rows * c.in_cols * c.channels +
+                (double)c.window_rows * c.window_cols * c.channels * c.features +
+                (double)c.batch * c.out_rows() * c.out_cols() * c.features);
+}
+
 template <typename Bench>
 TuningRecord run_bench(const Problem& problem, const std::string& config,
                        const DeviceSpec& dev, const BenchOptions& opts,
@@ -326,8 +357,10 @@ TuningRecord run_bench(const Problem& problem, const std::string& config,
     device_bench(t.data());
   }
   summarize_times(std::move(t), rec);
-  rec.gflops = static_cast<double>(problem.flops()) /
-               static_cast<double>(std::max<std::int64_t>(rec.median_ns, 1));
+  const double ns = static_cast<double>(std::max<std::int64_t>(rec.median_ns, 1));
+  rec.gflops = static_cast<double>(problem.flops()) / ns;
+  rec.frac_of_peak = rec.gflops / (1e3 * nominal_peak_tflops(opts.exec.precision));
+  rec.algo_gbs = compulsory_bytes(problem) / ns;
   return rec;
 }
 
@@ -353,8 +386,7 @@ inline TuningRecord benchmark_config(const Problem& problem, const GemmConfig& c
       throw ConfigError("gemm_tiled: config \"" + cfg.name() + "\" rejected: " + v.summary());
   }
   const std::string name =
-      exact ? cfg.name() : "gemm@" + b200::precision_name(opts.exec.precision) +
-                               (opts.exec.tc_tile_n ? "_n" + std::to_string(opts.exec.tc_tile_n) : "");
+      exact ? cfg.name() : "gemm@" + b200::precision_name(opts.exec.precision) + opts.exec.suffix();
   TuningRecord rec = detail::run_bench(
       problem, name, dev, opts, [&] { gemm_tiled(a, b, c, s, cfg, dev); },
       [&](std::int64_t* out) {
@@ -398,7 +430,8 @@ inline TuningRecord benchmark_config(const Problem& problem, const ConvAlgoParam
                                      s.channels, s.features, seed + 1);
   const bool exact = opts.exec.precision == b200::Precision::Fp32Exact;
   const std::string name =
-      exact ? params.name() : params.name() + "@" + b200::precision_name(opts.exec.precision);
+      exact ? params.name()
+            : params.name() + "@" + b200::precision_name(opts.exec.precision) + opts.exec.suffix();
   TuningRecord rec = detail::run_bench(
       problem, name, dev, opts,
       [&] {
@@ -623,8 +656,9 @@ inline void save_db(const std::vector<TuningRecord>& records, const std::string&
         << ",\"min_ns\":" << r.min_ns << ",\"mean_ns\":" << r.mean_ns << ",\"gflops\":" << r.gflops
         << ",\"valid\":" << (r.valid ? "true" : "false");
     const std::size_t at = r.config.find('@');
-    out << ",\"precision\":\"" << (at == std::string::npos ? "fp32" : r.config.substr(at + 1))
-        << "\"}\n";
+    const std::string tag = at == std::string::npos ? "fp32" : r.config.substr(at + 1);
+    out << ",\"precision\":\"" << tag.substr(0, tag.find('_')) << "\",\"frac_of_peak\":"
+        << r.frac_of_peak << ",\"algo_gbs\":" << r.algo_gbs << "}\n";
   }
   if (!out) throw IoError("save_db: write to " + path + " failed");
 }
@@ -675,6 +709,8 @@ inline std::vector<TuningRecord> load_db(const std::string& path) {
     if (valid != "true" && valid != "false")
       throw ParseError(loc + ": malformed tuning record: \"valid\" is not a bool");
     r.valid = valid == "true";
+    if (kv.count("frac_of_peak")) r.frac_of_peak = as_num("frac_of_peak");
+    if (kv.count("algo_gbs")) r.algo_gbs = as_num("algo_gbs");
     const auto key = std::make_tuple(r.problem, r.config, r.device);
     const auto it = where.find(key);
     if (it != where.end()) {
@@ -722,16 +758,32 @@ inline TuneResult tune(const Problem& problem, const ParamSpace& space, const De
       }
       continue;
     }
-    for (int tile : space.tc_tiles) {
-      o.exec.tc_tile_n = tile;
-      if (problem.kind == Problem::Kind::Gemm) {
-        records.push_back(benchmark_config(problem, GemmConfig{}, dev, o));
-      } else {
+    for (int stages : space.tc_stages) {
+      for (int cluster : space.tc_clusters) {
+        o.exec.tc_stages = stages;
+        o.exec.tc_cluster = cluster;
+        if (problem.kind == Problem::Kind::Gemm) {
+          for (int tile : space.tc_tiles) {
+            o.exec.tc_tile_n = tile;
+            records.push_back(benchmark_config(problem, GemmConfig{}, dev, o));
+          }
+          continue;
+        }
         ParamSpace tc = space;
         tc.algos = {ConvAlgo::Im2col, ConvAlgo::Winograd};
         for (const ConvAlgoParams& p : enumerate_conv_configs(tc, problem.conv)) {
           if (p.algo == ConvAlgo::Winograd && prec != Precision::Tf32) continue;
-          records.push_back(benchmark_config(problem, p, dev, o));
+          for (TcMode mode : space.tc_modes) {
+            if (p.algo == ConvAlgo::Winograd && mode != TcMode::Auto) continue;
+            o.exec.tc_mode = mode;
+            // A knob combination the shape cannot run is a rejected
+            // candidate, not a failed tune.
+            try {
+              records.push_back(benchmark_config(problem, p, dev, o));
+            } catch (const CapabilityError&) {
+            }
+          }
+          o.exec.tc_mode = TcMode::Auto;
         }
       }
     }

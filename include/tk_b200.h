@@ -112,10 +112,25 @@ typedef struct tk_conv_params {
  * semantics: exact FP32, library-chosen kernel shape. */
 typedef struct tk_exec_options {
   int precision;     /* enum tk_precision                                  */
-  int tc_tile_n;     /* tensor-core N tile (0 = auto; 64/128/192/256)       */
-  int tc_stages;     /* smem pipeline depth (0 = auto)                      */
-  int reserved[5];
+  int tc_tile_n;     /* tensor-core N tile of a GEMM (0 = auto; 64..256)   */
+  int tc_stages;     /* smem pipeline depth (0 = auto, else 2..8)          */
+  int tc_cluster;    /* 0 = auto, 1 = one SM (UMMA M 128), 2 = SM pair     */
+  int tc_mode;       /* conv operand path: enum tk_tc_mode                  */
+  int tc_split;      /* 0 = cost model, 1 = never split K (no split-K, no
+                        wave tail), n > 1 = n K-splits where supported     */
+  int reserved[2];
 } tk_exec_options;
+
+/* Tensor-core convolution operand paths (tk_exec_options.tc_mode); a mode
+ * (or tc_cluster) the shape cannot use is rejected with TK_ERR_CAPABILITY. */
+enum tk_tc_mode {
+  TK_TC_AUTO = 0,
+  TK_TC_HALO = 1,      /* one halo box per channel chunk, taps as views    */
+  TK_TC_PIXN = 2,      /* features on the MMA M side, pixel boxes on N     */
+  TK_TC_PIXM = 3,      /* pixels on M, features on N                       */
+  TK_TC_GATHER = 4,    /* producer warps build the pixel operand           */
+  TK_TC_POINTWISE = 5  /* 1x1: plain GEMM on the NHWC input                */
+};
 
 /* ---- library --------------------------------------------------------- */
 TK_API const char* tk_last_error(void);

@@ -106,7 +106,8 @@ class ConvParamsC(C.Structure):
 
 class ExecOptionsC(C.Structure):
     _fields_ = [("precision", C.c_int), ("tc_tile_n", C.c_int), ("tc_stages", C.c_int),
-                ("reserved", C.c_int * 5)]
+                ("tc_cluster", C.c_int), ("tc_mode", C.c_int), ("tc_split", C.c_int),
+                ("reserved", C.c_int * 2)]
 
 
 # Every symbol the header declares (checked by the CPU tests).
@@ -405,9 +406,14 @@ def parse_conv_params(text: str) -> ConvAlgoParams:
     raise ParseError(f'conv params "{text}": unrecognized name')
 
 
-def exec_options(precision="fp32", tile_n=0, stages=0) -> ExecOptionsC:
+TC_MODES = {"auto": 0, "halo": 1, "pixn": 2, "pixm": 3, "gather": 4, "pointwise": 5}
+
+
+def exec_options(precision="fp32", tile_n=0, stages=0, cluster=0, mode="auto",
+                 split=0) -> ExecOptionsC:
     p = PRECISIONS[precision] if isinstance(precision, str) else int(precision)
-    return ExecOptionsC(p, tile_n, stages)
+    m = TC_MODES[mode] if isinstance(mode, str) else int(mode)
+    return ExecOptionsC(p, tile_n, stages, cluster, m, split)
 
 
 # ---------------------------------------------------------------------------

@@ -217,6 +217,24 @@ size_t out_elems(const ConvGeom& g) { return (size_t)g.N * g.OH * g.OW * g.K; }
 
 int precision_of(const tk_exec_options* o) { return o ? o->precision : TK_PREC_FP32_EXACT; }
 
+// Tensor-core knobs of one C-ABI call (restored on return).
+struct KnobScope {
+  TcKnobs saved;
+  explicit KnobScope(const tk_exec_options* o) : saved(tc_knobs()) {
+    TcKnobs k;
+    if (o) {
+      k.stages = o->tc_stages;
+      k.cluster = o->tc_cluster;
+      k.mode = o->tc_mode;
+      k.split = o->tc_split;
+    }
+    tc_knobs() = k;
+  }
+  ~KnobScope() { tc_knobs() = saved; }
+  KnobScope(const KnobScope&) = delete;
+  KnobScope& operator=(const KnobScope&) = delete;
+};
+
 // ---- exact GEMM plumbing ---------------------------------------------------
 
 // Library default for the exact path: 8x8 register tile, 16x16 threads
@@ -716,6 +734,7 @@ int tk_gemm_naive(const tk_gemm_shape* shape, const float* a, const float* b, co
 int tk_gemm_dev(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const tk_exec_options* opts,
                 const float* d_a, const float* d_b, const float* d_c, float* d_out, void* stream) {
   return guarded([&] {
+    KnobScope knobs(opts);
     require_gpu();
     const tilekit::GemmShape g = gemm_shape(shape);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -734,6 +753,7 @@ int tk_gemm_dev(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const tk_
 int tk_gemm_ex(const tk_gemm_shape* shape, const tk_exec_options* opts, const float* a,
                const float* b, const float* c, float* out) {
   return guarded([&] {
+    KnobScope knobs(opts);
     const tilekit::GemmShape g = gemm_shape(shape);
     cudaStream_t st = host_stream();
     const size_t na = g.m * g.k, nb = g.k * g.n, nc = g.m * g.n;
@@ -848,6 +868,7 @@ int tk_conv2d(const tk_conv_shape* shape, const tk_conv_params* params, const fl
 int tk_conv2d_ex(const tk_conv_shape* shape, const tk_conv_params* params,
                  const tk_exec_options* opts, const float* in, const float* filt, float* out) {
   return guarded([&] {
+    KnobScope knobs(opts);
     if (!params) fail(TK_ERR_CONTRACT, "conv2d: params must not be NULL");
     conv_host(conv_shape(shape), params, precision_of(opts), in, filt, out);
   });
@@ -947,6 +968,7 @@ int tk_filter_matrix(size_t r, size_t s, size_t c, size_t k, const float* filt, 
 int tk_conv2d_workspace_size(const tk_conv_shape* shape, const tk_conv_params* params,
                              const tk_exec_options* opts, size_t* bytes) {
   return guarded([&] {
+    KnobScope knobs(opts);
     if (!params || !bytes) fail(TK_ERR_CONTRACT, "conv2d_workspace_size: NULL argument");
     const tilekit::ConvShape s = conv_shape(shape);
     if (params->algo == 3) check_winograd(s, params);
@@ -958,6 +980,7 @@ int tk_conv2d_dev(const tk_conv_shape* shape, const tk_conv_params* params,
                   const tk_exec_options* opts, const float* d_in, const float* d_filt,
                   float* d_out, void* d_ws, size_t ws_bytes, void* stream) {
   return guarded([&] {
+    KnobScope knobs(opts);
     require_gpu();
     if (!params) fail(TK_ERR_CONTRACT, "conv2d: params must not be NULL");
     const tilekit::ConvShape s = conv_shape(shape);
@@ -982,6 +1005,7 @@ static int conv_phase_dev(const tk_conv_shape* shape, const tk_conv_params* para
                           const tk_exec_options* opts, const float* d_in, const float* d_filt,
                           float* d_out, void* d_ws, size_t ws_bytes, void* stream, int phase) {
   return guarded([&] {
+    KnobScope knobs(opts);
     require_gpu();
     if (!params) fail(TK_ERR_CONTRACT, "conv2d: params must not be NULL");
     const tilekit::ConvShape s = conv_shape(shape);
@@ -1014,6 +1038,7 @@ int tk_bench_gemm(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const t
                   const float* a, const float* b, const float* c, int warmup, int samples,
                   int64_t* ns) {
   return guarded([&] {
+    KnobScope knobs(opts);
     const tilekit::GemmShape g = gemm_shape(shape);
     cudaStream_t st = host_stream();
     const size_t na = g.m * g.k, nb = g.k * g.n, nc = g.m * g.n;
@@ -1041,6 +1066,7 @@ int tk_bench_conv2d(const tk_conv_shape* shape, const tk_conv_params* params,
                     const tk_exec_options* opts, const float* in, const float* filt, int warmup,
                     int samples, int64_t* ns) {
   return guarded([&] {
+    KnobScope knobs(opts);
     if (!params) fail(TK_ERR_CONTRACT, "bench: params must not be NULL");
     const tilekit::ConvShape s = conv_shape(shape);
     const ConvGeom g = conv_geom(s);

@@ -44,6 +44,11 @@
 
 namespace tkb {
 
+TcKnobs& tc_knobs() {
+  thread_local TcKnobs k;
+  return k;
+}
+
 namespace {
 
 constexpr int kRows = 128;       // A rows staged per CTA (UMMA M per SM)
@@ -888,7 +893,7 @@ TailPlan plan_tail(long long tiles, int num_kb, int cg, int bn) {
   }();
   const long long pairs = sm_count() / cg;
   const long long rem = tiles % pairs, full = tiles / pairs;
-  if (off || rem == 0 || full < 1 || num_kb < 8) return t;
+  if (off || tc_knobs().split == 1 || rem == 0 || full < 1 || num_kb < 8) return t;
   const int bm = kRows * cg;
   const double mma_clk = 4.0 * (double)bm * bn * 8 / 3782.0;
   const double feed_clk = (double)(bm / 2 + bn / 2) * 128 / 70.0;
@@ -922,6 +927,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   const int ktab_bytes0 = MODE == kConvGather ? p.num_kb * 32 * 8 : 0;
   // Tuning experiments: TK_TC_STAGES caps the ring, TK_TC_EPI=1 forces one
   // staging buffer.
+  if (tc_knobs().stages > 0) stages_req = tc_knobs().stages;
   if (const char* e = getenv("TK_TC_STAGES")) stages_req = atoi(e);
   if (const char* e = getenv("TK_TC_EPI")) p.epi_bufs = std::min(p.epi_bufs, atoi(e));
   // Double-buffered TMA-store staging when it leaves room for >= 3 stages.
@@ -1431,7 +1437,8 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
   const int esize = tf32 ? 4 : 2;
   const int ek = kSlabBytes / esize;
   if ((g.K * esize) % 16 != 0) fail(TK_ERR_CAPABILITY, "tc_gemm: rows must be 16-byte multiples");
-  const int cg = g.M > kRows ? 2 : 1;
+  int cg = g.M > kRows ? 2 : 1;
+  if (tc_knobs().cluster == 1 || tc_knobs().cluster == 2) cg = tc_knobs().cluster;
   int bn = g.tile_n > 0 ? g.tile_n : (g.N >= 256 ? 256 : ((g.N + 15) / 16) * 16);
   if (bn > 256) bn = 256;
   const int step = 16 * cg;
@@ -1573,6 +1580,13 @@ struct ConvPlan {
 // partials must stay under `cap` bytes.
 int choose_splits(long long units, int num_kb, long long pairs, int bm, int bn,
                   size_t out_bytes, size_t cap) {
+  const int forced = tc_knobs().split;
+  if (forced == 1) return 1;
+  if (forced > 1) {
+    int sp = std::min(forced, std::max(1, num_kb / 2));
+    while (sp > 1 && (size_t)sp * out_bytes > cap) --sp;
+    return sp;
+  }
   const double mma_clk = 4.0 * (double)bm * bn * 8 / 3782.0;      // per slab, per pair
   const double feed_clk = (double)(bm / 2 + bn / 2) * 128 / 70.0;  // bytes per SM / (B/clk)
   const double slab_us = std::max(mma_clk, feed_clk) / 1900.0;
@@ -1608,15 +1622,17 @@ void finish_splits(ConvPlan& c, int num_kb, int splits, size_t out_bytes, long l
   if (c.splits > 1) c.part_bytes = align256((size_t)c.splits * out_bytes);
 }
 
-ConvPlan plan_conv(const ConvGeom& g, int precision) {
+ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
   ConvPlan c;
   const long long K = (long long)g.R * g.S * g.C;
   const bool tf32 = precision == TK_PREC_TF32;
   const int esize = tf32 ? 4 : 2, ek = kSlabBytes / esize;
   const long long pix = (long long)g.N * g.OH * g.OW;
   const char* force = getenv("TK_CONV_MODE");
+  const int mode = tc_knobs().mode;
   const bool pointwise = g.R == 1 && g.S == 1 && g.pad_t == 0 && g.pad_l == 0 && g.C % 8 == 0 &&
-                         g.K % 4 == 0 && !(force && std::string(force) != "plain");
+                         g.K % 4 == 0 && !(force && std::string(force) != "plain") &&
+                         (mode == TK_TC_AUTO || mode == TK_TC_POINTWISE);
   if (pointwise) {
     c.kind = kPointwisePlan;
     c.tf32 = tf32;
@@ -1642,7 +1658,7 @@ ConvPlan plan_conv(const ConvGeom& g, int precision) {
     if (c.splits == 1) c.tail = plan_tail((long long)c.num_m * c.num_n, c.num_kb, c.cg, c.bn);
     return c;
   }
-  if (conv_boxable(g, precision)) {
+  if (conv_boxable(g, precision) && mode != TK_TC_GATHER) {
     c.kind = kBoxPlan;
     c.tf32 = tf32;
     c.kp = K;
@@ -1653,11 +1669,17 @@ ConvPlan plan_conv(const ConvGeom& g, int precision) {
     const bool halo_ok = g.stride == 1 && g.R * g.S <= 9 && g.S <= 3 && g.K % 32 == 0 &&
                          ((g.K <= 128 && g.C <= 128) || (force && std::string(force).rfind("halo", 0) == 0));
     c.halo = halo_ok && !(force && std::string(force).rfind("halo", 0) != 0);
+    const bool halo_geom = g.stride == 1 && g.R * g.S <= 9 && g.S <= 3 && g.K % 32 == 0;
+    if (mode == TK_TC_HALO && halo_geom) c.halo = true;
+    if (mode == TK_TC_PIXN || mode == TK_TC_PIXM) c.halo = false;
     c.num_kb = (int)(K / ek);
     c.kb_per = c.num_kb;
     if (c.halo) return c;
     c.pix_on_n = g.K >= kRows;
+    if (mode == TK_TC_PIXN) c.pix_on_n = true;
+    if (mode == TK_TC_PIXM && g.K % 4 == 0 && g.K <= 256) c.pix_on_n = false;  // BN <= 256
     c.cg = c.pix_on_n ? (g.K >= 2 * kRows ? 2 : 1) : 2;
+    if (c.pix_on_n && (tc_knobs().cluster == 1 || tc_knobs().cluster == 2)) c.cg = tc_knobs().cluster;
     c.bx = pick_box(g, c.pix_on_n, c.cg);
     if (c.bx.wb == 0) return c;  // reported by the launcher
     const long long pix_tiles = (long long)g.N * c.bx.tiles_w * c.bx.tiles_h;
@@ -1685,6 +1707,26 @@ ConvPlan plan_conv(const ConvGeom& g, int precision) {
   c.tf32 = true;
   c.kp = (K + 31) / 32 * 32;
   c.filt_bytes = align256((size_t)g.K * c.kp * 4);
+  return c;
+}
+
+// The plan, with explicitly requested knobs (tk_exec_options.tc_mode /
+// tc_cluster) that this shape cannot honour rejected as CapabilityError --
+// a tuner then skips the candidate instead of timing a mislabeled one.
+ConvPlan plan_conv(const ConvGeom& g, int precision) {
+  const ConvPlan c = plan_conv_impl(g, precision);
+  const int mode = tc_knobs().mode, cluster = tc_knobs().cluster;
+  const bool ok = mode == TK_TC_AUTO ||
+                  (mode == TK_TC_POINTWISE && c.kind == kPointwisePlan) ||
+                  (mode == TK_TC_GATHER && c.kind == kGatherPlan) ||
+                  (mode == TK_TC_HALO && c.kind == kBoxPlan && c.halo) ||
+                  (mode == TK_TC_PIXN && c.kind == kBoxPlan && !c.halo && c.pix_on_n) ||
+                  (mode == TK_TC_PIXM && c.kind == kBoxPlan && !c.halo && !c.pix_on_n);
+  if (!ok) fail(TK_ERR_CAPABILITY, "tc_conv: operand path " + std::to_string(mode) +
+                                       " does not apply to this convolution");
+  if (cluster != 0 && cluster != c.cg)  // only the pixN plan takes the cluster knob
+    fail(TK_ERR_CAPABILITY, "tc_conv: cluster size " + std::to_string(cluster) +
+                                " does not apply to this convolution's operand path");
   return c;
 }
 

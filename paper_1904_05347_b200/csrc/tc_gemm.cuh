@@ -29,6 +29,14 @@ struct TcGemm {
 
 void launch_tc_gemm(const TcGemm& g, cudaStream_t st);
 
+// Per-call tensor-core knobs (tk_exec_options.tc_stages / tc_cluster /
+// tc_mode / tc_split), set by the C ABI for the duration of one call on the
+// calling thread; zero = automatic.
+struct TcKnobs {
+  int stages = 0, cluster = 0, mode = 0, split = 0;
+};
+TcKnobs& tc_knobs();
+
 // Column-major C = alpha*OPa(A)*OPb(B) + beta*C (the reference GemmShape
 // convention) on tensor cores; transposes operands into K-major scratch
 // where needed.

@@ -203,10 +203,33 @@ static void gpu_checks() {
   for (const auto& r : ct.records) {
     CHECK(r.valid);
     const auto at = r.config.find('@');
-    precs.insert(at == std::string::npos ? "fp32" : r.config.substr(at + 1));
+    const std::string tag = at == std::string::npos ? "fp32" : r.config.substr(at + 1);
+    precs.insert(tag.substr(0, tag.find('_')));
+    CHECK(r.frac_of_peak > 0.0 && r.algo_gbs > 0.0);  // Winograd counts direct flops: may exceed 1
   }
   CHECK(precs.count("fp32") && precs.count("tf32") && precs.count("bf16"));
   CHECK(ct.best.config.find('@') != std::string::npos);  // tensor cores win on this layer
+
+  // Pipeline depth, cluster shape and operand path as tuning axes: every
+  // candidate runs, verifies, and is named by its knobs.
+  ParamSpace kn;
+  kn.precisions = {b200::Precision::Tf32};
+  kn.tc_stages = {0, 4};
+  kn.tc_clusters = {0, 1};
+  kn.tc_modes = {b200::TcMode::Auto, b200::TcMode::PixN, b200::TcMode::PixM};
+  ConvShape ks = vs;
+  ks.batch = 2;
+  const TuneResult kt = b200::tune(Problem::of(ks), kn, b200, o);
+  std::set<std::string> names;
+  for (const auto& r : kt.records) {
+    CHECK(r.valid);
+    names.insert(r.config);
+  }
+  CHECK(names.count("im2col@tf32") && names.count("im2col@tf32_s4") &&
+        names.count("im2col@tf32_c1_pixn") && names.count("im2col@tf32_s4_pixm"));
+  std::printf("knob tune best for %s: %s (%.1f GFLOP/s, %.0f%% of peak)\n",
+              kt.best.problem.c_str(), kt.best.config.c_str(), kt.best.gflops,
+              100.0 * kt.best.frac_of_peak);
   save_db(ct.records, "tilekit_test_gpu.ndjson");
   CHECK(load_db("tilekit_test_gpu.ndjson").size() == ct.records.size());
   std::remove("tilekit_test_gpu.ndjson");

@@ -46,11 +46,16 @@ int main(int argc, char** argv) {
   space.tile_cols = {2, 4};
   space.channel_vectors = {4};
   space.feature_vectors = {4};
+  // tensor cores: pipeline depth x cluster shape x operand path
+  space.tc_stages = {0, 4};
+  space.tc_clusters = {0, 1};
+  space.tc_modes = {b200::TcMode::Auto, b200::TcMode::Halo, b200::TcMode::PixN,
+                    b200::TcMode::PixM, b200::TcMode::Pointwise};
   BenchOptions opts;
   opts.warmup = 2;
   opts.samples = 5;
   std::vector<TuningRecord> all;
-  std::printf("%-16s %-26s %12s %10s\n", "layer", "best", "GFLOP/s", "median_us");
+  std::printf("%-16s %-30s %12s %10s %7s\n", "layer", "best", "GFLOP/s", "median_us", "%peak");
   for (const Layer& L : layers) {
     ConvShape s;
     s.batch = batch;
@@ -62,8 +67,8 @@ int main(int argc, char** argv) {
     s.padding = Padding::Same;
     const TuneResult t = b200::tune(Problem::of(s), space, dev, opts);
     all.insert(all.end(), t.records.begin(), t.records.end());
-    std::printf("%-16s %-26s %12.1f %10.1f\n", L.name, t.best.config.c_str(), t.best.gflops,
-                t.best.median_ns / 1e3);
+    std::printf("%-16s %-30s %12.1f %10.1f %6.1f%%\n", L.name, t.best.config.c_str(),
+                t.best.gflops, t.best.median_ns / 1e3, 100.0 * t.best.frac_of_peak);
     std::fflush(stdout);
   }
   save_db(all, db);
