@@ -290,8 +290,11 @@ inline ConvShape conv_proxy(ConvShape s) {
   s.batch = std::min<std::size_t>(s.batch, 2);
   s.in_rows = std::max(s.window_rows, std::min<std::size_t>(s.in_rows, 24));
   s.in_cols = std::max(s.window_cols, std::min<std::size_t>(s.in_cols, 24));
-  s.channels = std::min<std::size_t>(s.channels, 16);
-  s.features = std::min<std::size_t>(s.features, 16);
+  // Channel / feature counts pick the tensor-core operand path (slab
+  // alignment, halo vs pixel boxes): keep them, so a candidate is verified
+  // on the path it was timed on.
+  s.channels = std::min<std::size_t>(s.channels, 512);
+  s.features = std::min<std::size_t>(s.features, 512);
   return s;
 }
 

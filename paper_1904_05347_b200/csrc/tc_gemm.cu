@@ -54,7 +54,8 @@ namespace {
 constexpr int kRows = 128;       // A rows staged per CTA (UMMA M per SM)
 constexpr int kSlabBytes = 128;  // bytes of K per operand row per stage
 constexpr int kThreads = 192;
-constexpr int kAccCols = 256;
+constexpr int kAccCols = 256;  // TMEM: 2 x 256 fp32 columns allocated
+constexpr int kMaxAcc = 8;     // accumulator slots when BN <= 64 (512 / 64)
 constexpr int kMaxStages = 8;
 
 enum TcMode : int { kPlain = 0, kConvPixN = 1, kConvPixM = 2, kConvGather = 3, kConvHalo = 4 };
@@ -84,6 +85,10 @@ struct TcArgs {
   int store_tma;               // epilogue via swizzled smem tile + TMA store
   int epi_bytes;               // bytes of epilogue staging
   int epi_bufs;                // staging buffers for the TMA-store epilogue
+  // TMEM accumulator ring: acc_slots slots of acc_cols columns (512 / slots);
+  // more slots for narrow tiles let the MMA run further ahead of the
+  // epilogue, decoupling their per-tile handshakes.
+  int acc_slots, acc_cols;
   // conv geometry
   int OH, OW, Kout, Wb, tileH, boxH, tiles_w, tiles_h, pad_t, pad_l, cchunks, S;
   // halo mode: virtual pitch P, TH rows per CTA, TW useful columns, R*S taps
@@ -369,8 +374,8 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   uint64_t* full = bars;
   uint64_t* empty = bars + kMaxStages;
   uint64_t* tmem_full = bars + 2 * kMaxStages;
-  uint64_t* tmem_empty = tmem_full + 2;
-  uint64_t* fbar = tmem_empty + 2;  // resident-filter barrier
+  uint64_t* tmem_empty = tmem_full + kMaxAcc;
+  uint64_t* fbar = tmem_empty + kMaxAcc;  // resident-filter barrier
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fbar + 1);
   // TMA-store staging: epi_bufs x (BN/32) swizzled 128-row x 128-byte tiles
   uint8_t* epi_stage = reinterpret_cast<uint8_t*>(bars) + 1024;
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       ptx::mbar_init(&full[s], MODE == kConvGather ? 1 + CG : 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < p.acc_slots; ++a) {
       ptx::mbar_init(&tmem_full[a], 1);
       ptx::mbar_init(&tmem_empty[a], CG);
     }
@@ -480,11 +485,11 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       uint32_t phase = 0;
       int local = 0;
       for (int t = unit; t < total; t += nunits, ++local) {
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
+        const int acc = local % p.acc_slots;
+        const uint32_t acc_phase = (uint32_t)(local / p.acc_slots) & 1u;
         ptx::mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        const uint32_t d_tmem = tmem_base + acc * p.acc_cols;
         for (int ch = 0; ch < p.cchunks; ++ch) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
@@ -574,11 +579,11 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       uint32_t phase = 0;
       int local = 0;
       for (int t = unit; t < total; t += nunits, ++local) {
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
+        const int acc = local % p.acc_slots;
+        const uint32_t acc_phase = (uint32_t)(local / p.acc_slots) & 1u;
         ptx::mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        const uint32_t d_tmem = tmem_base + acc * p.acc_cols;
         const Unit u = decode_unit(p, t);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
@@ -635,13 +640,13 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
     for (int t = unit; t < total; t += nunits, ++local) {
       const Unit u = decode_unit(p, t);
       const int m_blk = u.m_blk, n_blk = u.n_blk, z = u.z;
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
+      const int acc = local % p.acc_slots;
+      const uint32_t acc_phase = (uint32_t)(local / p.acc_slots) & 1u;
       ptx::mbar_wait_sleep(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
       if (local == 0 && warp == 2 && lane == 0) trace_mark(p, 4);  // first accumulator ready
       if (local == 1 && warp == 2 && lane == 0) trace_mark(p, 5);  // second accumulator ready
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kAccCols;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * p.acc_cols;
 
       if ((MODE == kPlain || MODE == kConvPixN) && u.slot >= 0) {
         store_tail_piece(p, taddr, u.slot, rank, CG, row);
@@ -949,6 +954,15 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   auto fn = tc_gemm_kernel<MODE, CG, TF32>;
   TKB_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
+  {
+    static const int forced = [] {
+      const char* e = getenv("TK_TC_ACC");
+      return e ? atoi(e) : 0;
+    }();
+    p.acc_slots = p.BN <= 64 ? 8 : (p.BN <= 128 ? 4 : 2);
+    if (forced == 2 || forced == 4 || forced == 8) p.acc_slots = std::min(p.acc_slots, forced);
+    p.acc_cols = 2 * kAccCols / p.acc_slots;
+  }
   if (p.splits < 1 || (MODE != kPlain && MODE != kConvPixN)) {
     p.splits = 1;
     p.kb_per = p.num_kb;

@@ -225,8 +225,11 @@ static void gpu_checks() {
     CHECK(r.valid);
     names.insert(r.config);
   }
-  CHECK(names.count("im2col@tf32") && names.count("im2col@tf32_s4") &&
-        names.count("im2col@tf32_c1_pixn") && names.count("im2col@tf32_s4_pixm"));
+  const bool all = names.count("im2col@tf32") && names.count("im2col@tf32_s4") &&
+                   names.count("im2col@tf32_c1_pixn") && names.count("im2col@tf32_s4_pixm");
+  CHECK(all);
+  if (!all)
+    for (const auto& n : names) std::printf("  candidate %s\n", n.c_str());
   std::printf("knob tune best for %s: %s (%.1f GFLOP/s, %.0f%% of peak)\n",
               kt.best.problem.c_str(), kt.best.config.c_str(), kt.best.gflops,
               100.0 * kt.best.frac_of_peak);
