@@ -1066,6 +1066,14 @@ void require_tc(int precision) {
     fail(TK_ERR_CAPABILITY, "tensor-core path: precision must be TF32 or BF16 in this version");
 }
 
+// TMA tensor maps and the vectorised pack/convert kernels address global
+// memory in 16-byte units.
+void require_aligned(const void* p, const char* what) {
+  if (p && (reinterpret_cast<uintptr_t>(p) & 15) != 0)
+    fail(TK_ERR_CAPABILITY, std::string("tensor-core path: ") + what +
+                                " must be 16-byte aligned (device allocations are)");
+}
+
 // ---- packing / conversion kernels -------------------------------------------
 
 __device__ __forceinline__ float round_tf32(float x) {
@@ -1514,8 +1522,9 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
   const long long kp = tf32 ? (long long)((k + 3) / 4 * 4) : (long long)((k + 7) / 8 * 8);
   // TF32 operands already K-major with 16-byte rows are used in place;
   // everything else is packed (and converted for BF16).
-  const bool a_ok = tf32 && ta && kp == (long long)k;
-  const bool b_ok = tf32 && !tb && kp == (long long)k;
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool a_ok = tf32 && ta && kp == (long long)k && aligned(a);
+  const bool b_ok = tf32 && !tb && kp == (long long)k && aligned(b);
   const size_t esz = tf32 ? 4 : 2;
   void* pa = nullptr;
   void* pb = nullptr;
@@ -1819,6 +1828,11 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
                     int precision, void* ws, cudaStream_t st, int phase) {
   require_tc(precision);
   const bool prep = (phase & kConvPrepare) != 0, run = (phase & kConvRun) != 0;
+  if (prep) require_aligned(filt, "the filter");
+  if (run) {
+    require_aligned(in, "the input");
+    require_aligned(out, "the output");
+  }
   const long long K = (long long)g.R * g.S * g.C;
   const ConvPlan plan = plan_conv(g, precision);
   const long long kp = plan.kp;
