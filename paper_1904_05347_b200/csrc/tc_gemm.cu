@@ -121,7 +121,8 @@ struct TcArgs {
   unsigned long long* trace;
 };
 
-constexpr int kTraceEvents = 10;
+constexpr int kTraceEvents = 18;
+constexpr int kTraceUnit = 8;  // steady-state unit probed by events 10..17
 __device__ __forceinline__ void trace_mark(const TcArgs& p, int ev) {
   if (p.trace) {
     unsigned long long t;
@@ -240,6 +241,7 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
     }
   }
   if (local == 0 && issuer) trace_mark(p, 8);  // TMEM drained to smem (first unit)
+  if (local == kTraceUnit && issuer) trace_mark(p, 14);
   ptx::tc_fence_before();
   ptx::fence_proxy_async();
   ptx::named_sync(1, 128);
@@ -254,6 +256,7 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
     }
     ptx::bulk_commit();
     if (local == 0) trace_mark(p, 9);  // stores issued (first unit)
+    if (local == kTraceUnit) trace_mark(p, 15);
   }
 }
 
@@ -333,6 +336,7 @@ __device__ __forceinline__ void gather_producer(const TcArgs& p, uint8_t* base, 
                         : 0.0f;
         }
       }
+      if (local == kTraceUnit && t == 0) trace_mark(p, 16);
       ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
       const uint32_t sa = sbase + stage * stage_bytes;
 #pragma unroll
@@ -348,6 +352,7 @@ __device__ __forceinline__ void gather_producer(const TcArgs& p, uint8_t* base, 
       if (t == 0) {
         if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::map_to_rank(ptx::smem(&full[stage]), 0));
         else ptx::mbar_arrive(&full[stage]);
+        if (local == kTraceUnit) trace_mark(p, 17);
       }
     }
   }
@@ -583,6 +588,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         const uint32_t acc_phase = (uint32_t)(local / p.acc_slots) & 1u;
         ptx::mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
+        if (local == kTraceUnit && lane == 0) trace_mark(p, 10);
         const uint32_t d_tmem = tmem_base + acc * p.acc_cols;
         const Unit u = decode_unit(p, t);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
@@ -590,6 +596,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           ptx::tc_fence_after();
           if (local == 0 && kb == u.kb0 && lane == 0) trace_mark(p, 2);  // first slab landed
           if (local == 0 && kb == u.kb1 - 1 && lane == 0) trace_mark(p, 3);  // last slab landed
+          if (local == kTraceUnit && kb == u.kb0 && lane == 0) trace_mark(p, 11);
           if (ptx::elect_one()) {
             const uint32_t sa = ptx::smem(base + stage * stage_bytes);
             const uint64_t ad = kdesc + (sa >> 4);
@@ -600,6 +607,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
                                     (kb != u.kb0 || kk != 0));
             ptx::commit_cg<CG>(&empty[stage]);
             if (kb == u.kb1 - 1) ptx::commit_cg<CG>(&tmem_full[acc]);
+            if (kb == u.kb1 - 1 && local == kTraceUnit) trace_mark(p, 12);
           }
           __syncwarp();
           if (++stage == p.stages) {
@@ -646,6 +654,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       ptx::tc_fence_after();
       if (local == 0 && warp == 2 && lane == 0) trace_mark(p, 4);  // first accumulator ready
       if (local == 1 && warp == 2 && lane == 0) trace_mark(p, 5);  // second accumulator ready
+      if (local == kTraceUnit && warp == 2 && lane == 0) trace_mark(p, 13);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * p.acc_cols;
 
       if ((MODE == kPlain || MODE == kConvPixN) && u.slot >= 0) {
@@ -1031,8 +1040,10 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     cudaFree(trace);
     unsigned long long t0 = ~0ull;
     for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[(size_t)b * kTraceEvents]);
-    static const char* names[kTraceEvents] = {"entry", "setup", "slab0", "slabN", "acc0",
-                                              "acc1", "stored", "exit", "drained", "issued"};
+    static const char* names[kTraceEvents] = {
+        "entry", "setup", "slab0", "slabN", "acc0", "acc1", "stored", "exit", "drained", "issued",
+        "u8:mma_acc_free", "u8:mma_slab_in", "u8:mma_commit", "u8:epi_acc_in", "u8:epi_drained",
+        "u8:epi_issued", "u8:gather_loaded", "u8:gather_arrived"};
     std::fprintf(stderr, "tc trace MODE=%d CG=%d grid=%d units=%lld stages=%d BN=%d (us from first entry: min/med/max)\n",
                  MODE, CG, grid, total, stages, p.BN);
     for (int e = 0; e < kTraceEvents; ++e) {
