@@ -1704,6 +1704,23 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
                          ((g.K <= 128 && g.C <= 128) || (force && std::string(force).rfind("halo", 0) == 0));
     c.halo = halo_ok && !(force && std::string(force).rfind("halo", 0) != 0);
     const bool halo_geom = g.stride == 1 && g.R * g.S <= 9 && g.S <= 3 && g.K % 32 == 0;
+    // Between halo and pixel boxes for >= 128 channels the deciding factor
+    // is how well pixN's tiles fill the SM pairs (measured with the tuner,
+    // profiles/r01_tune_*_knobs.ndjson): full waves favour pixN (VGG
+    // conv2_2, 3% faster), a mostly idle last wave favours halo's 4x more,
+    // narrower tiles (ResNet res4a_branch2b: 30 vs 40 us).
+    if (halo_geom && g.C >= 128 && g.K <= 256 && !force && mode == TK_TC_AUTO) {
+      const int pcg = g.K >= 2 * kRows ? 2 : 1;
+      const BoxShape pb = pick_box(g, true, pcg);
+      if (pb.wb != 0) {
+        const long long units = ((g.K + kRows * pcg - 1) / (kRows * pcg)) *
+                                (long long)g.N * pb.tiles_w * pb.tiles_h;
+        const long long pairs = sm_count() / pcg;
+        const double eff = (double)units / (double)(((units + pairs - 1) / pairs) * pairs);
+        if (c.halo && eff >= 0.9) c.halo = false;
+        if (!c.halo && eff < 0.6) c.halo = true;
+      }
+    }
     if (mode == TK_TC_HALO && halo_geom) c.halo = true;
     if (mode == TK_TC_PIXN || mode == TK_TC_PIXM) c.halo = false;
     c.num_kb = (int)(K / ek);
