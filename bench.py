@@ -445,8 +445,9 @@ def main():
     prof = profs[-1] if profs else ""
     if prof:
         kern = json.load(open(prof))["kernels"]
-        tb = sum(v["dram_bytes"] for k, v in kern.items() if "tc_gemm_kernel" in k
-                 or "exact_gemm" in k)
+        tb = sum(v["dram_bytes"] for k, v in kern.items()
+                 if any(x in k for x in ("tc_gemm_kernel", "exact_gemm", "tail_reduce",
+                                         "splitk_reduce")))
         traffic, traffic_src = int(tb), os.path.relpath(prof, ROOT)
     compulsory = sum(4 * (L["x"].numel() + L["f"].numel() + L["y"].numel()) for L in layers)
     roofline = {"bound": "tensor", "achieved": round(achieved_tf, 2), "peak": round(peak_tf, 1),
