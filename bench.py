@@ -498,13 +498,31 @@ def main():
                              // 4 + 1, device=dev)
             rn.append((shp, x, f, y, ws, mult, shp.flops()))
         rn_flops = sum(fl * m for *_, m, fl in rn)
+        im2col = tk.parse_conv_params("im2col")
         for p_ in ("tf32", "bf16"):
-            def rn_pass():
-                for shp, x, f, y, ws, mult, _ in rn:
-                    for _ in range(mult):
-                        tk.conv2d_dev(x, f, y, shp, tk.parse_conv_params("im2col"), precision=p_,
-                                      workspace=ws if p_ == prec else None, stream=stream)
-            rn_pass()
+            # One workspace per layer instance (each of a shape's `mult`
+            # instances is its own layer with its own prepared filter).
+            inst = [(shp, x, f, y, torch.empty(tk.conv2d_workspace_size(shp, im2col, p_) // 4 + 1,
+                                               device=dev))
+                    for shp, x, f, y, _, mult, _ in rn for _ in range(mult)]
+
+            def rn_pass(s_main, s_side):
+                # As the VGG step: filter prepares forked to a side stream,
+                # each run joins on its own prepare.
+                s_side.wait_stream(s_main)
+                ready = []
+                with torch.cuda.stream(s_side):
+                    for shp, x, f, y, ws in inst:
+                        tk.conv2d_prepare_dev(f, shp, im2col, ws, precision=p_, stream=s_side)
+                        ev = torch.cuda.Event()
+                        ev.record(s_side)
+                        ready.append(ev)
+                for (shp, x, f, y, ws), ev in zip(inst, ready):
+                    s_main.wait_event(ev)
+                    tk.conv2d_run_dev(x, f, y, shp, im2col, ws, precision=p_, stream=s_main)
+                s_main.wait_stream(s_side)
+            side_rn = torch.cuda.Stream(device=dev)
+            rn_pass(stream, side_rn)
             torch.cuda.synchronize()
             g_rn = None
             if not args.no_graph:
@@ -512,11 +530,7 @@ def main():
                 cap.wait_stream(stream)
                 g_rn = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g_rn, stream=cap):
-                    for shp, x, f, y, ws, mult, _ in rn:
-                        for _ in range(mult):
-                            tk.conv2d_dev(x, f, y, shp, tk.parse_conv_params("im2col"),
-                                          precision=p_, workspace=ws if p_ == prec else None,
-                                          stream=cap)
+                    rn_pass(cap, side_rn)
                 g_rn.replay()
                 torch.cuda.synchronize()
             ts = []
@@ -527,7 +541,7 @@ def main():
                 if g_rn is not None:
                     g_rn.replay()
                 else:
-                    rn_pass()
+                    rn_pass(stream, side_rn)
                 b_.record(stream)
                 b_.synchronize()
                 ts.append(a_.elapsed_time(b_))
