@@ -561,9 +561,11 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
             ptx::tma3<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows, z);
           } else if constexpr (MODE == kConvPixN) {
             ptx::tma2<CG>(sa, &map_a, fb, k0, m_blk * BM + rank * kRows);
-            ptx::tma4<CG>(sb, &map_b, fb, c0, pt.ow0 + dy, pt.oh0 + rank * p.boxH + dx, pt.img);
+            ptx::tma4<CG>(sb, &map_b, fb, c0, pt.ow0 * p.stride + dy,
+                          (pt.oh0 + rank * p.boxH) * p.stride + dx, pt.img);
           } else if constexpr (MODE == kConvPixM) {
-            ptx::tma4<CG>(sa, &map_a, fb, c0, pt.ow0 + dy, pt.oh0 + rank * p.boxH + dx, pt.img);
+            ptx::tma4<CG>(sa, &map_a, fb, c0, pt.ow0 * p.stride + dy,
+                          (pt.oh0 + rank * p.boxH) * p.stride + dx, pt.img);
             ptx::tma2<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows);
           } else {
             ptx::tma2<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows);
@@ -785,9 +787,12 @@ EncodeTiledFn encode_fn() {
 
 // esize: 4 (fp32 / tf32) or 2 (bf16).  dims[0] is the contiguous K axis.
 CUtensorMap make_map(const void* base, int esize, int rank, const cuuint64_t* dims,
-                     const cuuint64_t* strides, const cuuint32_t* box) {
+                     const cuuint64_t* strides, const cuuint32_t* box,
+                     const cuuint32_t* traversal = nullptr) {
   CUtensorMap m;
   cuuint32_t elem_strides[5] = {1, 1, 1, 1, 1};
+  if (traversal)
+    for (int i = 0; i < rank; ++i) elem_strides[i] = traversal[i];
   const CUresult r = encode_fn()(
       &m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
       (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, elem_strides,
@@ -816,12 +821,18 @@ CUtensorMap map_rows2d(const void* base, int esize, long long K, long long rows,
 }
 
 // NHWC activations, box {slab channels, Wb, Hb, 1}.
-CUtensorMap map_nhwc(const void* base, int esize, const ConvGeom& g, int wb, int hb) {
+// With stride s > 1 the box traverses W and H with element stride s: it
+// spans s*wb x s*hb input pixels and lands the wb x hb pixels a stride-s
+// window visits (one tap), densely, in shared memory.
+CUtensorMap map_nhwc(const void* base, int esize, const ConvGeom& g, int wb, int hb,
+                     int stride = 1) {
   cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
   cuuint64_t strides[3] = {(cuuint64_t)g.C * esize, (cuuint64_t)g.W * g.C * esize,
                            (cuuint64_t)g.H * g.W * g.C * esize};
-  cuuint32_t box[4] = {(cuuint32_t)(kSlabBytes / esize), (cuuint32_t)wb, (cuuint32_t)hb, 1};
-  return make_map(base, esize, 4, dims, strides, box);
+  cuuint32_t box[4] = {(cuuint32_t)(kSlabBytes / esize), (cuuint32_t)(wb * stride),
+                       (cuuint32_t)(hb * stride), 1};
+  const cuuint32_t trav[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+  return make_map(base, esize, 4, dims, strides, box, stride > 1 ? trav : nullptr);
 }
 
 int sm_count() {
@@ -1450,6 +1461,7 @@ BoxShape pick_box(const ConvGeom& g, bool pix_on_n, int cg) {
         if (P != kRows * cg || th % cg != 0) continue;
       }
       if (wb > 2 * g.OW + 16 || th > 2 * g.OH + 16) continue;
+      if (wb * g.stride > 256 || (th / cg) * g.stride > 256) continue;  // TMA box extent
       const int tw = (g.OW + wb - 1) / wb, tt = (g.OH + th - 1) / th;
       const double waste = (double)tw * wb * tt * th / ((double)g.OW * g.OH);
       const double score = waste * (1.0 + 24.0 / P);
@@ -1577,8 +1589,10 @@ namespace {
 // Slab width in elements for the precision.
 int slab_elems(int precision) { return precision == TK_PREC_TF32 ? 32 : 64; }
 
+// Pixel boxes need whole slabs of channels; stride 2 through a traversal
+// stride (box extent s*wb <= 256).
 bool conv_boxable(const ConvGeom& g, int precision) {
-  return g.C % slab_elems(precision) == 0 && g.stride == 1;
+  return g.C % slab_elems(precision) == 0 && (g.stride == 1 || g.stride == 2);
 }
 
 size_t align256(size_t b) { return (b + 255) / 256 * 256; }
@@ -1664,9 +1678,15 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
   const long long pix = (long long)g.N * g.OH * g.OW;
   const char* force = getenv("TK_CONV_MODE");
   const int mode = tc_knobs().mode;
+  // Strided 1x1 in TF32 reads the strided pixels straight through a
+  // traversal-stride pixel box (no compacting pass); BF16 needs a conversion
+  // pass anyway, which compacts for free.
+  // (Small planes waste too much of a pixel box: 7x7 -> 8x8 boxes.)
+  const bool strided_box = g.stride > 1 && tf32 && conv_boxable(g, precision) &&
+                           mode != TK_TC_POINTWISE && g.OH * g.OW >= 196;
   const bool pointwise = g.R == 1 && g.S == 1 && g.pad_t == 0 && g.pad_l == 0 && g.C % 8 == 0 &&
                          g.K % 4 == 0 && !(force && std::string(force) != "plain") &&
-                         (mode == TK_TC_AUTO || mode == TK_TC_POINTWISE);
+                         (mode == TK_TC_AUTO || mode == TK_TC_POINTWISE) && !strided_box;
   if (pointwise) {
     c.kind = kPointwisePlan;
     c.tf32 = tf32;
@@ -2015,6 +2035,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   p.pad_l = g.pad_l;
   p.cchunks = g.C / ek;
   p.S = g.S;
+  p.stride = g.stride;
   const int pix_tiles = g.N * bx.tiles_w * bx.tiles_h;
   if (pix_on_n) {
     p.BN = bx.wb * bx.tileH;
@@ -2033,7 +2054,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
       p.tail_part = reinterpret_cast<float*>(reinterpret_cast<char*>(part) + plan.part_bytes);
     }
     const CUtensorMap ma = map_rows2d(fa, esize, kp, g.K, kRows);
-    const CUtensorMap mb = map_nhwc(xin, esize, g, bx.wb, bx.boxH);
+    const CUtensorMap mb = map_nhwc(xin, esize, g, bx.wb, bx.boxH, g.stride);
     dispatch<kConvPixN>(ma, mb, ma, p, cg, tf32, st);
     if (p.splits > 1) splitk_reduce(part, p.part_stride, p.splits, out, st);
   } else {
@@ -2042,7 +2063,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     p.N = g.K;
     p.num_m = pix_tiles;
     p.num_n = 1;
-    const CUtensorMap ma = map_nhwc(xin, esize, g, bx.wb, bx.boxH);
+    const CUtensorMap ma = map_nhwc(xin, esize, g, bx.wb, bx.boxH, g.stride);
     const CUtensorMap mb = map_rows2d(fa, esize, kp, g.K, p.BN / cg);
     if (g.K % 4 != 0) fail(TK_ERR_CAPABILITY, "tc_conv: output features must be a multiple of 4");
     cuuint64_t dims[4] = {(cuuint64_t)g.K, (cuuint64_t)g.OW, (cuuint64_t)g.OH, (cuuint64_t)g.N};
