@@ -1701,6 +1701,11 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
       return ((pix + kRows * c.cg - 1) / (kRows * c.cg)) * ((g.K + bn - 1) / bn);
     };
     if (c.bn > 128 && units(c.bn) < pairs) c.bn = 128;
+    // Short-K (HBM-bound) layers are epilogue-bound: a 128-wide tile keeps
+    // two TMA-store staging buffers, so a tile's store overlaps the next
+    // drain.
+    if (c.bn > 128 && c.kp / ek <= 4) c.bn = 128;
+    if (const char* e = getenv("TK_PW_BN")) c.bn = atoi(e);
     c.num_m = (int)((pix + kRows * c.cg - 1) / (kRows * c.cg));
     c.num_n = (g.K + c.bn - 1) / c.bn;
     const int num_kb = (int)(c.kp / ek);
