@@ -91,6 +91,9 @@ struct TcArgs {
   int acc_slots, acc_cols;
   // conv geometry
   int OH, OW, Kout, Wb, tileH, boxH, tiles_w, tiles_h, pad_t, pad_l, cchunks, S;
+  // pixN on small planes: one pixel tile = `imgs` whole images (box
+  // {slab, Wb, tileH, imgs / CG} per CTA); Nimg = batch for the edge check.
+  int imgs, Nimg;
   // halo mode: virtual pitch P, TH rows per CTA, TW useful columns, R*S taps
   int P, TH, TW, taps, halo_bytes;
   int resident;                // halo mode: this CTA's filter slice lives in smem
@@ -197,8 +200,9 @@ struct PixTile {
 __device__ __forceinline__ PixTile pix_tile(const TcArgs& p, int t) {
   PixTile r;
   const int per_img = p.tiles_w * p.tiles_h;
-  r.img = t / per_img;
-  const int rem = t - r.img * per_img;
+  const int ti = t / per_img;
+  r.img = ti * (p.imgs > 1 ? p.imgs : 1);
+  const int rem = t - ti * per_img;
   r.oh0 = (rem / p.tiles_w) * p.tileH;
   r.ow0 = (rem % p.tiles_w) * p.Wb;
   return r;
@@ -561,8 +565,12 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
             ptx::tma3<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows, z);
           } else if constexpr (MODE == kConvPixN) {
             ptx::tma2<CG>(sa, &map_a, fb, k0, m_blk * BM + rank * kRows);
-            ptx::tma4<CG>(sb, &map_b, fb, c0, pt.ow0 * p.stride + dy,
-                          (pt.oh0 + rank * p.boxH) * p.stride + dx, pt.img);
+            if (p.imgs > 1)  // each CTA boxes its imgs / CG whole images
+              ptx::tma4<CG>(sb, &map_b, fb, c0, pt.ow0 * p.stride + dy, pt.oh0 * p.stride + dx,
+                            pt.img + (int)rank * (p.imgs / CG));
+            else
+              ptx::tma4<CG>(sb, &map_b, fb, c0, pt.ow0 * p.stride + dy,
+                            (pt.oh0 + rank * p.boxH) * p.stride + dx, pt.img);
           } else if constexpr (MODE == kConvPixM) {
             ptx::tma4<CG>(sa, &map_a, fb, c0, pt.ow0 * p.stride + dy,
                           (pt.oh0 + rank * p.boxH) * p.stride + dx, pt.img);
@@ -721,11 +729,13 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           // warp then walks the 32 columns with shuffles (one coalesced
           // 128-byte store of 32 consecutive features per column).
           const int n = col + (int)lane;
-          const int h = n / p.Wb, w = n - (n / p.Wb) * p.Wb;
-          const int oh = pt.oh0 + h, ow = pt.ow0 + w;
-          const bool ok = n < p.BN && oh < p.OH && ow < p.OW;
+          const int per = p.Wb * p.tileH;  // columns per image of the tile
+          const int ii = n / per, nn = n - (n / per) * per;
+          const int h = nn / p.Wb, w = nn - (nn / p.Wb) * p.Wb;
+          const int oh = pt.oh0 + h, ow = pt.ow0 + w, img = pt.img + ii;
+          const bool ok = n < p.BN && oh < p.OH && ow < p.OW && img < p.Nimg;
           const long long pix_off =
-              ok ? (((long long)pt.img * p.OH + oh) * p.OW + ow) * p.Kout : -1ll;
+              ok ? (((long long)img * p.OH + oh) * p.OW + ow) * p.Kout : -1ll;
 #pragma unroll
           float* dst = p.splits > 1 ? p.part + u.sp * p.part_stride : p.d;
           for (int j = 0; j < 32; ++j) {
@@ -825,12 +835,12 @@ CUtensorMap map_rows2d(const void* base, int esize, long long K, long long rows,
 // spans s*wb x s*hb input pixels and lands the wb x hb pixels a stride-s
 // window visits (one tap), densely, in shared memory.
 CUtensorMap map_nhwc(const void* base, int esize, const ConvGeom& g, int wb, int hb,
-                     int stride = 1) {
+                     int stride = 1, int nb = 1) {
   cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
   cuuint64_t strides[3] = {(cuuint64_t)g.C * esize, (cuuint64_t)g.W * g.C * esize,
                            (cuuint64_t)g.H * g.W * g.C * esize};
   cuuint32_t box[4] = {(cuuint32_t)(kSlabBytes / esize), (cuuint32_t)(wb * stride),
-                       (cuuint32_t)(hb * stride), 1};
+                       (cuuint32_t)(hb * stride), (cuuint32_t)nb};
   const cuuint32_t trav[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   return make_map(base, esize, 4, dims, strides, box, stride > 1 ? trav : nullptr);
 }
@@ -876,10 +886,12 @@ __global__ void __launch_bounds__(256) tail_reduce_kernel(TcArgs p) {
   const int m = u.m_blk * kRows * CG + rank * kRows + row;
   if constexpr (MODE == kConvPixN) {
     const PixTile pt = pix_tile(p, u.n_blk);
-    const int h = col / p.Wb, w = col - (col / p.Wb) * p.Wb;
-    const int oh = pt.oh0 + h, ow = pt.ow0 + w;
-    if (oh >= p.OH || ow >= p.OW) return;
-    float* o = p.d + (((long long)pt.img * p.OH + oh) * p.OW + ow) * p.Kout + m;
+    const int per = p.Wb * p.tileH;
+    const int ii = col / per, cc = col - (col / per) * per;
+    const int h = cc / p.Wb, w = cc - (cc / p.Wb) * p.Wb;
+    const int oh = pt.oh0 + h, ow = pt.ow0 + w, img = pt.img + ii;
+    if (oh >= p.OH || ow >= p.OW || img >= p.Nimg) return;
+    float* o = p.d + (((long long)img * p.OH + oh) * p.OW + ow) * p.Kout + m;
     if (m + 3 < p.Kout && (p.Kout & 3) == 0) {
       *reinterpret_cast<float4*>(o) = a;
     } else {
@@ -1618,6 +1630,7 @@ struct ConvPlan {
   // kBoxPlan layout
   bool halo = false, pix_on_n = false;
   BoxShape bx{};
+  int imgs = 1;  // pixN: whole images per pixel tile (small planes)
   int num_m = 0, num_n = 0;
 };
 
@@ -1757,8 +1770,17 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
     c.cg = c.pix_on_n ? (g.K >= 2 * kRows ? 2 : 1) : 2;
     if (c.pix_on_n && (tc_knobs().cluster == 1 || tc_knobs().cluster == 2)) c.cg = tc_knobs().cluster;
     c.bx = pick_box(g, c.pix_on_n, c.cg);
+    // Planes of at most 8 x 8 (ResNet res5, 7 x 7): one 8 x 8 box per image
+    // wastes little and 256 / 64 = 4 images fill a 256-wide tile (instead of
+    // a 64-wide tile whose N = 64 MMAs and filter re-reads dominate).
+    if (c.pix_on_n && c.cg == 2 && g.OH <= 8 && g.OW <= 8 && g.N >= 4 &&
+        !(force && std::string(force) == "pixn1")) {
+      c.imgs = 4;
+      c.bx = BoxShape{8, 8, 8, 1, 1};
+    }
     if (c.bx.wb == 0) return c;  // reported by the launcher
-    const long long pix_tiles = (long long)g.N * c.bx.tiles_w * c.bx.tiles_h;
+    const long long pix_tiles =
+        ((long long)g.N + c.imgs - 1) / c.imgs * c.bx.tiles_w * c.bx.tiles_h;
     if (c.pix_on_n) {
       c.num_m = (g.K + kRows * c.cg - 1) / (kRows * c.cg);
       c.num_n = (int)pix_tiles;
@@ -1766,13 +1788,13 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
       const bool aligned = g.K % 4 == 0;
       const long long pairs = sm_count() / c.cg;
       const char* nosplit = getenv("TK_NO_SPLIT");
+      const int pbn = c.bx.wb * c.bx.tileH * c.imgs;
       const int sp = (aligned && !(nosplit && nosplit[0] == '1'))
                          ? choose_splits((long long)c.num_m * c.num_n, c.num_kb, pairs,
-                                         kRows * c.cg, c.bx.wb * c.bx.tileH, out_bytes, 64ull << 20)
+                                         kRows * c.cg, pbn, out_bytes, 64ull << 20)
                          : 1;
       finish_splits(c, c.num_kb, sp, out_bytes, (long long)c.num_m * c.num_n);
-      if (c.splits == 1)
-        c.tail = plan_tail((long long)c.num_m * c.num_n, c.num_kb, c.cg, c.bx.wb * c.bx.tileH);
+      if (c.splits == 1) c.tail = plan_tail((long long)c.num_m * c.num_n, c.num_kb, c.cg, pbn);
     } else {
       c.num_m = (int)pix_tiles;
       c.num_n = 1;
@@ -2041,9 +2063,11 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   p.cchunks = g.C / ek;
   p.S = g.S;
   p.stride = g.stride;
-  const int pix_tiles = g.N * bx.tiles_w * bx.tiles_h;
+  p.imgs = plan.imgs;
+  p.Nimg = g.N;
+  const int pix_tiles = (g.N + plan.imgs - 1) / plan.imgs * bx.tiles_w * bx.tiles_h;
   if (pix_on_n) {
-    p.BN = bx.wb * bx.tileH;
+    p.BN = bx.wb * bx.tileH * plan.imgs;
     p.M = g.K;
     p.N = p.BN * pix_tiles;
     p.num_m = (g.K + kRows * cg - 1) / (kRows * cg);
@@ -2059,7 +2083,9 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
       p.tail_part = reinterpret_cast<float*>(reinterpret_cast<char*>(part) + plan.part_bytes);
     }
     const CUtensorMap ma = map_rows2d(fa, esize, kp, g.K, kRows);
-    const CUtensorMap mb = map_nhwc(xin, esize, g, bx.wb, bx.boxH, g.stride);
+    const CUtensorMap mb =
+        plan.imgs > 1 ? map_nhwc(xin, esize, g, bx.wb, bx.tileH, g.stride, plan.imgs / cg)
+                      : map_nhwc(xin, esize, g, bx.wb, bx.boxH, g.stride);
     dispatch<kConvPixN>(ma, mb, ma, p, cg, tf32, st);
     if (p.splits > 1) splitk_reduce(part, p.part_stride, p.splits, out, st);
   } else {

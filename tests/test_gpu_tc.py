@@ -49,6 +49,7 @@ def test_tc_gemm_colmajor(tk, oracle, m, n, k, ta, tb, prec):
 @pytest.mark.parametrize("shape", [
     (2, 14, 14, 32, 128), (2, 14, 14, 64, 256), (2, 30, 30, 128, 64), (1, 56, 56, 64, 64), (1, 28, 28, 64, 64), (2, 56, 56, 64, 128), (1, 28, 28, 256, 512),
     (3, 17, 23, 32, 96), (1, 112, 112, 64, 128), (2, 7, 7, 512, 512), (1, 9, 9, 3, 16),
+    (5, 7, 7, 256, 256), (4, 6, 5, 256, 512), (9, 4, 4, 256, 256),  # multi-image pixel tiles
 ])
 def test_tc_conv_im2col(tk, oracle, shape, prec):
     N, H, W, C, K = shape
