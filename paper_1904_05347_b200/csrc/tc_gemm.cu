@@ -124,7 +124,7 @@ struct TcArgs {
   unsigned long long* trace;
 };
 
-constexpr int kTraceEvents = 18;
+constexpr int kTraceEvents = 21;
 constexpr int kTraceUnit = 8;  // steady-state unit probed by events 10..17
 __device__ __forceinline__ void trace_mark(const TcArgs& p, int ev) {
   if (p.trace) {
@@ -247,12 +247,15 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
   if (local == 0 && issuer) trace_mark(p, 8);  // TMEM drained to smem (first unit)
   if (local == kTraceUnit && issuer) trace_mark(p, 14);
   ptx::tc_fence_before();
+  if (local == kTraceUnit && issuer) trace_mark(p, 18);
   ptx::fence_proxy_async();
+  if (local == kTraceUnit && issuer) trace_mark(p, 19);
   ptx::named_sync(1, 128);
   if (issuer) {
     // Accumulator fully read by all 128 threads: hand TMEM back to the MMA.
-    if constexpr (CG == 2) ptx::mbar_arrive_cluster(empty_cluster_addr);
+    if constexpr (CG == 2) ptx::mbar_arrive_remote(empty_cluster_addr);
     else ptx::mbar_arrive(empty_local);
+    if (local == kTraceUnit) trace_mark(p, 20);  // (overrides: after the TMEM release)
     for (int j = 0; j < nchunks; ++j) {
       const uint8_t* src = sbuf + j * kRows * kSlabBytes;
       if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + 32 * j, c1, c2, c3);
@@ -672,7 +675,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         ptx::tc_fence_before();
         ptx::named_sync(1, 128);
         if (warp == 2 && lane == 0) {
-          if constexpr (CG == 2) ptx::mbar_arrive_cluster(empty_base + 8u * acc);
+          if constexpr (CG == 2) ptx::mbar_arrive_remote(empty_base + 8u * acc);
           else ptx::mbar_arrive(&tmem_empty[acc]);
         }
         continue;
@@ -754,7 +757,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       ptx::tc_fence_before();
       ptx::named_sync(1, 128);
       if (warp == 2 && lane == 0) {
-        if constexpr (CG == 2) ptx::mbar_arrive_cluster(empty_base + 8u * acc);
+        if constexpr (CG == 2) ptx::mbar_arrive_remote(empty_base + 8u * acc);
         else ptx::mbar_arrive(&tmem_empty[acc]);
       }
     }
@@ -1066,7 +1069,8 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     static const char* names[kTraceEvents] = {
         "entry", "setup", "slab0", "slabN", "acc0", "acc1", "stored", "exit", "drained", "issued",
         "u8:mma_acc_free", "u8:mma_slab_in", "u8:mma_commit", "u8:epi_acc_in", "u8:epi_drained",
-        "u8:epi_issued", "u8:gather_loaded", "u8:gather_arrived"};
+        "u8:epi_issued", "u8:gather_loaded", "u8:gather_arrived", "u8:epi_tmem_fence",
+        "u8:epi_proxy_fence", "u8:epi_released"};
     std::fprintf(stderr, "tc trace MODE=%d CG=%d grid=%d units=%lld stages=%d BN=%d (us from first entry: min/med/max)\n",
                  MODE, CG, grid, total, stages, p.BN);
     for (int e = 0; e < kTraceEvents; ++e) {
