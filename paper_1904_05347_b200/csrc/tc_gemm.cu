@@ -357,6 +357,8 @@ __device__ __forceinline__ void gather_producer(const TcArgs& p, uint8_t* base, 
       ptx::fence_proxy_async();
       ptx::named_sync(2 + group, 128);
       if (t == 0) {
+        // Cluster-scope release: the leader's MMA reads these generic-proxy
+        // writes (CTA-scope would not order them for another CTA's observer).
         if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::map_to_rank(ptx::smem(&full[stage]), 0));
         else ptx::mbar_arrive(&full[stage]);
         if (local == kTraceUnit) trace_mark(p, 17);
