@@ -94,6 +94,10 @@ struct TcArgs {
   // pixN on small planes: one pixel tile = `imgs` whole images (box
   // {slab, Wb, tileH, imgs / CG} per CTA); Nimg = batch for the edge check.
   int imgs, Nimg;
+  // pixN "flat rows": batch x output rows as one row space of N*OH rows;
+  // tile t = rows [t*tileH, +tileH), each CTA boxes boxH full-width rows
+  // that lie in one image (OH % boxH == 0) -- no row padding per image.
+  int flat;
   // halo mode: virtual pitch P, TH rows per CTA, TW useful columns, R*S taps
   int P, TH, TW, taps, halo_bytes;
   int resident;                // halo mode: this CTA's filter slice lives in smem
@@ -570,7 +574,10 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
             ptx::tma3<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows, z);
           } else if constexpr (MODE == kConvPixN) {
             ptx::tma2<CG>(sa, &map_a, fb, k0, m_blk * BM + rank * kRows);
-            if (p.imgs > 1)  // each CTA boxes its imgs / CG whole images
+            if (p.flat) {
+              const int r = n_blk * p.tileH + (int)rank * p.boxH;
+              ptx::tma4<CG>(sb, &map_b, fb, c0, dy, (r % p.OH) * p.stride + dx, r / p.OH);
+            } else if (p.imgs > 1)  // each CTA boxes its imgs / CG whole images
               ptx::tma4<CG>(sb, &map_b, fb, c0, pt.ow0 * p.stride + dy, pt.oh0 * p.stride + dx,
                             pt.img + (int)rank * (p.imgs / CG));
             else
@@ -734,10 +741,20 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           // warp then walks the 32 columns with shuffles (one coalesced
           // 128-byte store of 32 consecutive features per column).
           const int n = col + (int)lane;
-          const int per = p.Wb * p.tileH;  // columns per image of the tile
-          const int ii = n / per, nn = n - (n / per) * per;
-          const int h = nn / p.Wb, w = nn - (nn / p.Wb) * p.Wb;
-          const int oh = pt.oh0 + h, ow = pt.ow0 + w, img = pt.img + ii;
+          int oh, ow, img;
+          if (p.flat) {
+            const int r = n_blk * p.tileH + n / p.Wb;
+            img = r / p.OH;
+            oh = r - img * p.OH;
+            ow = n - (n / p.Wb) * p.Wb;
+          } else {
+            const int per = p.Wb * p.tileH;  // columns per image of the tile
+            const int ii = n / per, nn = n - (n / per) * per;
+            const int h = nn / p.Wb, w = nn - (nn / p.Wb) * p.Wb;
+            oh = pt.oh0 + h;
+            ow = pt.ow0 + w;
+            img = pt.img + ii;
+          }
           const bool ok = n < p.BN && oh < p.OH && ow < p.OW && img < p.Nimg;
           const long long pix_off =
               ok ? (((long long)img * p.OH + oh) * p.OW + ow) * p.Kout : -1ll;
@@ -891,10 +908,19 @@ __global__ void __launch_bounds__(256) tail_reduce_kernel(TcArgs p) {
   const int m = u.m_blk * kRows * CG + rank * kRows + row;
   if constexpr (MODE == kConvPixN) {
     const PixTile pt = pix_tile(p, u.n_blk);
-    const int per = p.Wb * p.tileH;
-    const int ii = col / per, cc = col - (col / per) * per;
-    const int h = cc / p.Wb, w = cc - (cc / p.Wb) * p.Wb;
-    const int oh = pt.oh0 + h, ow = pt.ow0 + w, img = pt.img + ii;
+    int oh, ow, img;
+    if (p.flat) {
+      const int r = u.n_blk * p.tileH + col / p.Wb;
+      img = r / p.OH;
+      oh = r - img * p.OH;
+      ow = col - (col / p.Wb) * p.Wb;
+    } else {
+      const int per = p.Wb * p.tileH;
+      const int ii = col / per, cc = col - (col / per) * per;
+      oh = pt.oh0 + cc / p.Wb;
+      ow = pt.ow0 + cc - (cc / p.Wb) * p.Wb;
+      img = pt.img + ii;
+    }
     if (oh >= p.OH || ow >= p.OW || img >= p.Nimg) return;
     float* o = p.d + (((long long)img * p.OH + oh) * p.OW + ow) * p.Kout + m;
     if (m + 3 < p.Kout && (p.Kout & 3) == 0) {
@@ -1637,6 +1663,7 @@ struct ConvPlan {
   bool halo = false, pix_on_n = false;
   BoxShape bx{};
   int imgs = 1;  // pixN: whole images per pixel tile (small planes)
+  bool flat = false;  // pixN: flat-row tiles (see TcArgs::flat)
   int num_m = 0, num_n = 0;
 };
 
@@ -1784,9 +1811,29 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
       c.imgs = 4;
       c.bx = BoxShape{8, 8, 8, 1, 1};
     }
+    // Flat rows: full-width boxes whose height divides OH tile N*OH rows
+    // with no per-image row padding (28 x 28: 2 x 4 rows x 28 = 224 pixels,
+    // where any per-image box pads 28 rows to 32).
+    if (c.pix_on_n && c.imgs == 1 && c.bx.wb != 0 && !(force && std::string(force) == "pixn1")) {
+      const double waste = (double)c.bx.tiles_w * c.bx.wb * c.bx.tiles_h * c.bx.tileH /
+                           ((double)g.OW * g.OH);
+      int best_bh = 0;
+      for (int bh = 1; bh <= g.OH; ++bh) {
+        const int P = c.cg * bh * g.OW;
+        if (g.OH % bh || P > 256 || P < 64 || P % (16 * c.cg) || g.OW * g.stride > 256 ||
+            bh * g.stride > 256)
+          continue;
+        best_bh = bh;  // the largest qualifying box
+      }
+      if (best_bh && waste > 1.02) {
+        c.flat = true;
+        c.bx = BoxShape{g.OW, c.cg * best_bh, best_bh, 1, 1};
+      }
+    }
     if (c.bx.wb == 0) return c;  // reported by the launcher
     const long long pix_tiles =
-        ((long long)g.N + c.imgs - 1) / c.imgs * c.bx.tiles_w * c.bx.tiles_h;
+        c.flat ? ((long long)g.N * g.OH + c.bx.tileH - 1) / c.bx.tileH
+               : ((long long)g.N + c.imgs - 1) / c.imgs * c.bx.tiles_w * c.bx.tiles_h;
     if (c.pix_on_n) {
       c.num_m = (g.K + kRows * c.cg - 1) / (kRows * c.cg);
       c.num_n = (int)pix_tiles;
@@ -2071,7 +2118,10 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   p.stride = g.stride;
   p.imgs = plan.imgs;
   p.Nimg = g.N;
-  const int pix_tiles = (g.N + plan.imgs - 1) / plan.imgs * bx.tiles_w * bx.tiles_h;
+  p.flat = plan.flat ? 1 : 0;
+  const int pix_tiles =
+      plan.flat ? (int)(((long long)g.N * g.OH + bx.tileH - 1) / bx.tileH)
+                : (g.N + plan.imgs - 1) / plan.imgs * bx.tiles_w * bx.tiles_h;
   if (pix_on_n) {
     p.BN = bx.wb * bx.tileH * plan.imgs;
     p.M = g.K;
