@@ -510,6 +510,8 @@ void conv_dev(const tilekit::ConvShape& s, const tk_conv_params* p, int precisio
       return;
     case 3: {
       const int m = check_winograd(s, p);
+      if (precision == TK_PREC_3XTF32)
+        fail(TK_ERR_CAPABILITY, "conv2d_winograd: 3xTF32 is provided on the im2col path only");
       winograd_dev(g, m, precision, in, filt, out, ws, st, phase);
       return;
     }

@@ -1128,8 +1128,85 @@ void dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& m
 }
 
 void require_tc(int precision) {
-  if (precision != TK_PREC_TF32 && precision != TK_PREC_BF16)
-    fail(TK_ERR_CAPABILITY, "tensor-core path: precision must be TF32 or BF16 in this version");
+  if (precision != TK_PREC_TF32 && precision != TK_PREC_BF16 && precision != TK_PREC_3XTF32)
+    fail(TK_ERR_CAPABILITY, "tensor-core path: precision must be TF32, BF16 or 3xTF32");
+}
+
+// ---- 3xTF32 (split precision) ------------------------------------------------
+// x = hi + lo with hi = x truncated to TF32 (what the tensor core reads from
+// an fp32 operand) and lo = x - hi (exact in fp32).  A product sum then runs
+// as one TF32 contraction over a tripled depth:
+//   sum_k a_k b_k ~= sum_k (a_hi b_hi + a_hi b_lo + a_lo b_hi)
+// by concatenating [a, a, a_lo] against [b_hi, b_lo, b_hi] along K; the
+// dropped a_lo b_lo term is below 2^-22 relative.
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+
+// rows x [kp] K-major fp32 -> rows x [3 kp]: pattern 0 = (x, x, lo), 1 = (hi, lo, hi).
+__global__ void __launch_bounds__(256) split3_rows_kernel(const float* __restrict__ src,
+                                                          long long rows, long long kp,
+                                                          float* __restrict__ dst, int pattern) {
+  const long long n = rows * kp;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / kp, k = i - r * kp;
+    const float x = src[i], hi = tf32_hi(x), lo = x - hi;
+    float* d = dst + r * 3 * kp + k;
+    if (pattern == 0) {
+      d[0] = x;
+      d[kp] = x;
+      d[2 * kp] = lo;
+    } else {
+      d[0] = hi;
+      d[kp] = lo;
+      d[2 * kp] = hi;
+    }
+  }
+}
+
+void split3_rows(const float* src, long long rows, long long kp, float* dst, int pattern,
+                 cudaStream_t st) {
+  const long long n = rows * kp;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sm_count() * 16);
+  split3_rows_kernel<<<blocks, 256, 0, st>>>(src, rows, kp, dst, pattern);
+  note_launch();
+  TKB_CUDA(cudaGetLastError());
+}
+
+// NHWC [P][C] -> [P][3C] = [x | x | lo] (activations; the tensor core
+// truncates the first two copies to hi).
+__global__ void __launch_bounds__(256) split3_channels_kernel(const float* __restrict__ src,
+                                                              long long pix, int C,
+                                                              float* __restrict__ dst) {
+  const long long n = pix * C;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long q = i / C;
+    const int c = (int)(i - q * C);
+    const float x = src[i];
+    float* d = dst + q * 3 * C + c;
+    d[0] = x;
+    d[C] = x;
+    d[2 * C] = x - tf32_hi(x);
+  }
+}
+
+// HWCK [R*S][C][K] -> [R*S][3C][K] = [hi | lo | hi] along C.
+__global__ void __launch_bounds__(256) split3_filter_kernel(const float* __restrict__ src,
+                                                            long long taps, int C, int K,
+                                                            float* __restrict__ dst) {
+  const long long n = taps * C * K;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long t = i / ((long long)C * K);
+    const long long rem = i - t * C * K;  // c*K + k
+    const float x = src[i], hi = tf32_hi(x);
+    float* d = dst + t * 3 * C * K + rem;
+    d[0] = hi;
+    d[(long long)C * K] = x - hi;
+    d[2LL * C * K] = hi;
+  }
 }
 
 // TMA tensor maps and the vectorised pack/convert kernels address global
@@ -1585,6 +1662,39 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
                              bool tb, const float* a, const float* b, const float* c, float* d,
                              int precision, int tile_n, cudaStream_t st) {
   require_tc(precision);
+  if (precision == TK_PREC_3XTF32) {
+    // Pack both operands K-major (fp32, unrounded), expand to the split
+    // triple along K, run one TF32 GEMM of depth 3 kp.
+    const long long kp = (long long)((k + 3) / 4 * 4);
+    float *pa = nullptr, *pb = nullptr, *a3 = nullptr, *b3 = nullptr;
+    TKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pa), (size_t)m * kp * 4, st));
+    TKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pb), (size_t)n * kp * 4, st));
+    TKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a3), (size_t)m * kp * 12, st));
+    TKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b3), (size_t)n * kp * 12, st));
+    if (ta) pack_kmajor<float>(a, (long long)k, 1, (long long)m, (long long)k, kp, pa, false, st);
+    else pack_kmajor<float>(a, 1, (long long)m, (long long)m, (long long)k, kp, pa, false, st);
+    if (tb) pack_kmajor<float>(b, 1, (long long)n, (long long)n, (long long)k, kp, pb, false, st);
+    else pack_kmajor<float>(b, (long long)k, 1, (long long)n, (long long)k, kp, pb, false, st);
+    split3_rows(pa, (long long)m, kp, a3, 0, st);
+    split3_rows(pb, (long long)n, kp, b3, 1, st);
+    TcGemm g;
+    g.M = (int)m;
+    g.N = (int)n;
+    g.K = (int)(3 * kp);
+    g.a = a3;
+    g.b = b3;
+    g.d = d;
+    g.c = c;
+    g.d_sm = 1;
+    g.d_sn = (long long)m;
+    g.alpha = alpha;
+    g.beta = beta;
+    g.precision = TK_PREC_TF32;
+    g.tile_n = tile_n;
+    launch_tc_gemm(g, st);
+    for (float* q : {pa, pb, a3, b3}) cudaFreeAsync(q, st);
+    return;
+  }
   const bool tf32 = precision == TK_PREC_TF32;
   const long long kp = tf32 ? (long long)((k + 3) / 4 * 4) : (long long)((k + 7) / 8 * 8);
   // TF32 operands already K-major with 16-byte rows are used in place;
@@ -1947,7 +2057,19 @@ void launch_pointwise(const ConvGeom& g, const ConvPlan& c, const float* in, con
 
 }  // namespace
 
+namespace {
+ConvGeom tripled(const ConvGeom& g) {
+  ConvGeom t = g;
+  t.C = 3 * g.C;
+  return t;
+}
+size_t split3_bytes_in(const ConvGeom& g) { return align256((size_t)g.N * g.H * g.W * g.C * 12); }
+size_t split3_bytes_filt(const ConvGeom& g) { return align256((size_t)g.R * g.S * g.C * g.K * 12); }
+}  // namespace
+
 size_t tc_conv_workspace(const ConvGeom& g, int precision) {
+  if (precision == TK_PREC_3XTF32)
+    return split3_bytes_in(g) + split3_bytes_filt(g) + tc_conv_workspace(tripled(g), TK_PREC_TF32);
   const ConvPlan c = plan_conv(g, precision);
   return c.filt_bytes + c.in_bytes + c.part_bytes + align256(c.tail.bytes);
 }
@@ -1956,6 +2078,34 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
                     int precision, void* ws, cudaStream_t st, int phase) {
   require_tc(precision);
   const bool prep = (phase & kConvPrepare) != 0, run = (phase & kConvRun) != 0;
+  if (precision == TK_PREC_3XTF32) {
+    // The same convolution over 3C channels: [x | x | x_lo] against
+    // [f_hi | f_lo | f_hi], as one TF32 convolution (see split3_*).
+    const ConvGeom g3 = tripled(g);
+    char* w = static_cast<char*>(ws);
+    float* x3 = reinterpret_cast<float*>(w);
+    float* f3 = reinterpret_cast<float*>(w + split3_bytes_in(g));
+    void* inner = w + split3_bytes_in(g) + split3_bytes_filt(g);
+    if (prep) {
+      require_aligned(filt, "the filter");
+      const long long n = (long long)g.R * g.S * g.C * g.K;
+      const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sm_count() * 16);
+      split3_filter_kernel<<<blocks, 256, 0, st>>>(filt, (long long)g.R * g.S, g.C, g.K, f3);
+      note_launch();
+      TKB_CUDA(cudaGetLastError());
+      launch_tc_conv(g3, nullptr, f3, nullptr, TK_PREC_TF32, inner, st, kConvPrepare);
+    }
+    if (run) {
+      const long long pix = (long long)g.N * g.H * g.W;
+      const long long n = pix * g.C;
+      const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sm_count() * 16);
+      split3_channels_kernel<<<blocks, 256, 0, st>>>(in, pix, g.C, x3);
+      note_launch();
+      TKB_CUDA(cudaGetLastError());
+      launch_tc_conv(g3, x3, f3, out, TK_PREC_TF32, inner, st, kConvRun);
+    }
+    return;
+  }
   if (prep) require_aligned(filt, "the filter");
   if (run) {
     require_aligned(in, "the input");

@@ -177,3 +177,53 @@ def test_graph_captured_stack_matches_direct_calls(tk, prec):
         torch.cuda.synchronize()
         for s, x, f, ref, ws, out in layers:
             assert torch.equal(out.view(torch.int32), ref.view(torch.int32)), s
+
+
+TOL_3XTF32 = 5e-5  # split-precision TF32: near-FP32; at K >= 1024 the FP32
+# accumulation order (tensor-core tree vs the reference's sequential sum) alone
+# reaches ~1e-5, so the bar is set at 5e-5 with a >= 20x margin over TF32.
+
+
+@pytest.mark.parametrize("m,n,k,ta,tb", [(256, 512, 384, 0, 0), (33, 29, 21, 1, 1), (1024, 1024, 1024, 1, 0)])
+def test_3xtf32_gemm(tk, oracle, m, n, k, ta, tb):
+    import torch
+    a = oracle.fill_random(m * k, 11)
+    b = oracle.fill_random(k * n, 12)
+    c = oracle.fill_random(m * n, 13)
+    want = oracle.gemm_naive(m, n, k, 1.5, -0.5, ta, tb, a, b, c)
+    da, db, dc = (torch.from_numpy(v).cuda() for v in (a, b, c))
+    out = torch.full((m * n,), float("nan"), device="cuda")
+    shape = tk.GemmShape(m, n, k, 1.5, -0.5, "t" if ta else "n", "t" if tb else "n")
+    tk.gemm_dev(da, db, dc, out, shape, precision="3xtf32")
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    err = oracle.max_scaled_error(got, want)
+    # and clearly better than plain TF32 on the same inputs
+    out2 = torch.full((m * n,), float("nan"), device="cuda")
+    tk.gemm_dev(da, db, dc, out2, shape, precision="tf32")
+    torch.cuda.synchronize()
+    err_tf32 = oracle.max_scaled_error(out2.cpu().numpy(), want)
+    assert err <= TOL_3XTF32, err
+    assert err < err_tf32 / 20, (err, err_tf32)
+
+
+@pytest.mark.parametrize("shape", [(2, 14, 14, 32, 128), (1, 9, 9, 3, 16), (2, 28, 28, 64, 64),
+                                   (2, 14, 14, 256, 512), (2, 16, 16, 64, 256, 1)])
+def test_3xtf32_conv(tk, oracle, shape):
+    N, H, W, C, K = shape[:5]
+    R = shape[5] if len(shape) > 5 else 3
+    s = tk.ConvShape(N, H, W, C, K, R, R, 1, True)
+    conv = oracle.Conv(N, H, W, C, K, R, R, 1, True)
+    x = oracle.fill_random(int(np.prod(conv.in_shape)), 14).reshape(conv.in_shape)
+    f = oracle.fill_random(int(np.prod(conv.filt_shape)), 15).reshape(conv.filt_shape)
+    want = oracle.conv2d_naive(conv, x, f)
+    got = dev_conv(tk, x, f, s, "im2col", precision="3xtf32")
+    assert oracle.max_scaled_error(got, want) <= TOL_3XTF32
+
+
+def test_3xtf32_winograd_is_a_capability_error(tk, oracle):
+    s = tk.ConvShape(1, 8, 8, 32, 32, 3, 3, 1, True)
+    x = np.zeros(s.in_shape, np.float32)
+    f = np.zeros(s.filt_shape, np.float32)
+    with pytest.raises(tk.CapabilityError):
+        dev_conv(tk, x, f, s, "winograd_t2x2", precision="3xtf32")
