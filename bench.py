@@ -370,6 +370,7 @@ def main():
     torch.cuda.synchronize()
     launches0 = tk.launch_count()
     times = []
+    extra_steps = 0
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush.zero_()
@@ -379,7 +380,17 @@ def main():
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
-    launches = tk.launch_count() - launches0
+        timed_samples = len(clocks.lines)
+        launches = tk.launch_count() - launches0
+        # A short timed region (small --steps) can end between two 20 ms
+        # samples: keep the same step running, untimed, until three samples
+        # under this load exist (reported as samples_after_timed).
+        t_end = time.time() + 2.0
+        while len(clocks.lines) < 3 and clocks.proc is not None and time.time() < t_end:
+            flush.zero_()
+            run_step()
+            torch.cuda.synchronize()
+            extra_steps += 1
     if launches_per_step is not None:
         launches = launches_per_step * args.steps
     torch.cuda.synchronize()
@@ -487,6 +498,50 @@ def main():
             secondary[f"vgg16_{p_}"] = {"value": round(step_flops / (ms * 1e-3) / 1e9, 1),
                                          "unit": "GFLOP/s", "ms_per_step": round(ms, 3),
                                          "bit_exact": p_ == "fp32"}
+        # BASELINE configs[1] at batch 1: the 13 VGG16 layers on one image
+        # (latency-bound: 13 launches of small grids), TF32, as one graph.
+        b1 = []
+        for name, hh, cc, kk, mult in VGG16:
+            shp = tk.ConvShape(1, hh, hh, cc, kk, 3, 3, 1, True)
+            for _ in range(mult):
+                b1.append((shp, torch.rand(shp.in_shape, device=dev, generator=gen) * 2 - 1,
+                           torch.rand(shp.filt_shape, device=dev, generator=gen) * 2 - 1,
+                           torch.empty(shp.out_shape, device=dev),
+                           torch.empty(tk.conv2d_workspace_size(shp, tk.parse_conv_params("im2col"),
+                                                                prec) // 4 + 1, device=dev)))
+        b1_flops = sum(shp.flops() for shp, *_ in b1)
+
+        def b1_pass(st_):
+            for shp, x, f, y, ws in b1:
+                tk.conv2d_dev(x, f, y, shp, tk.parse_conv_params("im2col"), precision=prec,
+                              workspace=ws, stream=st_)
+        b1_pass(stream)
+        torch.cuda.synchronize()
+        g_b1 = None
+        if not args.no_graph:
+            cap = torch.cuda.Stream(device=dev)
+            cap.wait_stream(stream)
+            g_b1 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_b1, stream=cap):
+                b1_pass(cap)
+            g_b1.replay()
+            torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            if g_b1 is not None:
+                g_b1.replay()
+            else:
+                b1_pass(stream)
+            b_.record(stream)
+            b_.synchronize()
+            ts.append(a_.elapsed_time(b_))
+        ms = float(np.median(ts))
+        secondary[f"vgg16_batch1_{prec}"] = {"value": round(b1_flops / (ms * 1e-3) / 1e9, 1),
+                                             "unit": "GFLOP/s", "ms_per_step": round(ms, 4),
+                                             "note": "L2-warm (inputs fit in L2)"}
+
         # BASELINE configs[2]: ResNet-50 conv stack (53 layers) at batch 32.
         rn = []
         for name, r, stv, h, c, k, mult in RESNET50:
@@ -624,7 +679,10 @@ def main():
                        "precision": prec, "step_gflop": round(step_flops / 1e9, 2),
                        "l2": "flushed between steps (256 MiB write, outside events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches), "clocks": clocks.summary(), "layers": layer_rows,
+            "gpu_launches": int(launches),
+            "clocks": dict(clocks.summary(), samples_in_timed=timed_samples,
+                           samples_after_timed=len(clocks.lines) - timed_samples),
+            "layers": layer_rows,
             "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
