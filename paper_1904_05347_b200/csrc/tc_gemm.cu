@@ -2128,7 +2128,10 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     if (prep) pack_filter<float>(filt, (int)K, g.K, (int)kp, ft, true, st);
     if (!run) return;
     const int pixels = g.N * g.OH * g.OW;
-    const int cg = 2;
+    // One SM per tile (cta_group::1): the gather producers then signal their
+    // own CTA's barrier -- no cross-CTA release on every K-slab.
+    int cg = 1;
+    if (const char* e = getenv("TK_GATHER_CG")) cg = atoi(e) == 2 ? 2 : 1;
     TcArgs p{};
     p.M = pixels;
     p.N = g.K;
