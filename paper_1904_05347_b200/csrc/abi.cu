@@ -7,6 +7,8 @@
 // GPU: there is no CPU fallback, and without an sm_100 device every compute
 // entry point fails with TK_ERR_CUDA.
 #include <atomic>
+#include <map>
+#include <memory>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -547,10 +549,16 @@ struct HostPipe {
   }
 };
 
+// One set of streams/events per (host thread, device): streams belong to
+// the device current when they were created.
 HostPipe& host_pipe() {
   host_stream();  // device + pool checks
-  thread_local HostPipe pipe;
-  return pipe;
+  int dev = 0;
+  TKB_CUDA(cudaGetDevice(&dev));
+  thread_local std::map<int, std::unique_ptr<HostPipe>> pipes;
+  std::unique_ptr<HostPipe>& p = pipes[dev];
+  if (!p) p = std::make_unique<HostPipe>();
+  return *p;
 }
 
 // Number of equal batch chunks: the largest divisor of the batch <= 8 that
