@@ -33,6 +33,7 @@ enum class TcMode {
   PixM = TK_TC_PIXM,
   Gather = TK_TC_GATHER,
   Pointwise = TK_TC_POINTWISE,
+  Im2col = TK_TC_IM2COL,
 };
 
 struct ExecOptions {
@@ -56,7 +57,7 @@ struct ExecOptions {
 
   // Config-name suffix of the non-default knobs, e.g. "_n128_s4_c1_halo".
   std::string suffix() const {
-    static const char* modes[] = {"", "_halo", "_pixn", "_pixm", "_gather", "_pointwise"};
+    static const char* modes[] = {"", "_halo", "_pixn", "_pixm", "_gather", "_pointwise", "_im2col"};
     std::string s;
     if (tc_tile_n) s += "_n" + std::to_string(tc_tile_n);
     if (tc_stages) s += "_s" + std::to_string(tc_stages);

@@ -129,7 +129,8 @@ enum tk_tc_mode {
   TK_TC_PIXN = 2,      /* features on the MMA M side, pixel boxes on N     */
   TK_TC_PIXM = 3,      /* pixels on M, features on N                       */
   TK_TC_GATHER = 4,    /* producer warps build the pixel operand           */
-  TK_TC_POINTWISE = 5  /* 1x1: plain GEMM on the NHWC input                */
+  TK_TC_POINTWISE = 5, /* 1x1: plain GEMM on the NHWC input                */
+  TK_TC_IM2COL = 6     /* pixels on M gathered by im2col-mode TMA          */
 };
 
 /* ---- library --------------------------------------------------------- */

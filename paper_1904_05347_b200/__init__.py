@@ -406,7 +406,7 @@ def parse_conv_params(text: str) -> ConvAlgoParams:
     raise ParseError(f'conv params "{text}": unrecognized name')
 
 
-TC_MODES = {"auto": 0, "halo": 1, "pixn": 2, "pixm": 3, "gather": 4, "pointwise": 5}
+TC_MODES = {"auto": 0, "halo": 1, "pixn": 2, "pixm": 3, "gather": 4, "pointwise": 5, "im2col": 6}
 
 
 def exec_options(precision="fp32", tile_n=0, stages=0, cluster=0, mode="auto",
@@ -522,35 +522,42 @@ def _stream(stream) -> C.c_void_p:
 
 
 def conv2d_dev(inp, filt, out, shape: ConvShape, params: ConvAlgoParams, precision="fp32",
-               workspace=None, stream=None, tile_n=0) -> None:
+               workspace=None, stream=None, tile_n=0, options=None) -> None:
+    """options: an exec_options(...) record (tensor-core knobs); overrides
+    precision / tile_n when given."""
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    opts = options if options is not None else exec_options(precision, tile_n)
     _check(lib().tk_conv2d_dev(C.byref(shape.c()), C.byref(params.c()),
-                               C.byref(exec_options(precision, tile_n)), _dptr(inp), _dptr(filt),
+                               C.byref(opts), _dptr(inp), _dptr(filt),
                                _dptr(out), _dptr(workspace), ws_bytes, _stream(stream)))
 
 
 def conv2d_prepare_dev(filt, shape: ConvShape, params: ConvAlgoParams, workspace,
-                       precision="fp32", stream=None) -> None:
+                       precision="fp32", stream=None, options=None) -> None:
     """Filter-side phase of conv2d_dev (may run on its own stream)."""
     ws_bytes = workspace.numel() * workspace.element_size()
+    opts = options if options is not None else exec_options(precision)
     _check(lib().tk_conv2d_prepare_dev(C.byref(shape.c()), C.byref(params.c()),
-                                       C.byref(exec_options(precision)), _dptr(filt),
+                                       C.byref(opts), _dptr(filt),
                                        _dptr(workspace), ws_bytes, _stream(stream)))
 
 
 def conv2d_run_dev(inp, filt, out, shape: ConvShape, params: ConvAlgoParams, workspace,
-                   precision="fp32", stream=None) -> None:
+                   precision="fp32", stream=None, options=None) -> None:
     """Input-side phase of conv2d_dev; ordered after conv2d_prepare_dev."""
     ws_bytes = workspace.numel() * workspace.element_size()
+    opts = options if options is not None else exec_options(precision)
     _check(lib().tk_conv2d_run_dev(C.byref(shape.c()), C.byref(params.c()),
-                                   C.byref(exec_options(precision)), _dptr(inp), _dptr(filt),
+                                   C.byref(opts), _dptr(inp), _dptr(filt),
                                    _dptr(out), _dptr(workspace), ws_bytes, _stream(stream)))
 
 
-def conv2d_workspace_size(shape: ConvShape, params: ConvAlgoParams, precision="fp32") -> int:
+def conv2d_workspace_size(shape: ConvShape, params: ConvAlgoParams, precision="fp32",
+                          options=None) -> int:
     n = C.c_size_t(0)
+    opts = options if options is not None else exec_options(precision)
     _check(lib().tk_conv2d_workspace_size(C.byref(shape.c()), C.byref(params.c()),
-                                          C.byref(exec_options(precision)), C.byref(n)))
+                                          C.byref(opts), C.byref(n)))
     return int(n.value)
 
 

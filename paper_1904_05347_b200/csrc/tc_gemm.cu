@@ -58,7 +58,19 @@ constexpr int kAccCols = 256;  // TMEM: 2 x 256 fp32 columns allocated
 constexpr int kMaxAcc = 8;     // accumulator slots when BN <= 64 (512 / 64)
 constexpr int kMaxStages = 8;
 
-enum TcMode : int { kPlain = 0, kConvPixN = 1, kConvPixM = 2, kConvGather = 3, kConvHalo = 4 };
+enum TcMode : int {
+  kPlain = 0,
+  kConvPixN = 1,
+  kConvPixM = 2,
+  kConvGather = 3,
+  kConvHalo = 4,
+  kConvIm2col = 5  // plain GEMM whose A rows are output pixels loaded by im2col-mode TMA
+};
+// Modes with the plain GEMM's unit decode, split-K partials and tail pieces.
+template <int MODE>
+constexpr bool plain_like() {
+  return MODE == kPlain || MODE == kConvIm2col;
+}
 
 #ifndef TKB_GATHER_GROUPS
 #define TKB_GATHER_GROUPS 2
@@ -550,6 +562,16 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         const Unit u = decode_unit(p, t);
         const int m_blk = u.m_blk, n_blk = u.n_blk, z = u.z;
         PixTile pt{0, 0, 0};
+        int i2c_w = 0, i2c_h = 0, i2c_n = 0;  // im2col: traversal start of the CTA's rows
+        if constexpr (MODE == kConvIm2col) {
+          const int m0 = m_blk * BM + rank * kRows;
+          const int plane = p.OH * p.OW;
+          i2c_n = m0 / plane;
+          const int r = m0 - i2c_n * plane;
+          const int oh = r / p.OW;
+          i2c_h = oh * p.stride - p.pad_t;
+          i2c_w = (r - oh * p.OW) * p.stride - p.pad_l;
+        }
         if constexpr (MODE == kConvPixN) pt = pix_tile(p, n_blk);
         if constexpr (MODE == kConvPixM) pt = pix_tile(p, m_blk);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
@@ -572,6 +594,14 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           if constexpr (MODE == kPlain) {
             ptx::tma3<CG>(sa, &map_a, fb, k0, m_blk * BM + rank * kRows, z);
             ptx::tma3<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows, z);
+          } else if constexpr (MODE == kConvIm2col) {
+            // 128 consecutive output pixels (across rows and images) from
+            // the traversal start of this CTA's first pixel, shifted by the tap.
+            const int tap = kb / p.cchunks;
+            const int ty = tap % p.S;
+            ptx::tma4_im2col<CG>(sa, &map_a, fb, c0, i2c_w, i2c_h, i2c_n, (uint16_t)ty,
+                                 (uint16_t)(tap / p.S));
+            ptx::tma2<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows);
           } else if constexpr (MODE == kConvPixN) {
             ptx::tma2<CG>(sa, &map_a, fb, k0, m_blk * BM + rank * kRows);
             if (p.flat) {
@@ -679,7 +709,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       if (local == kTraceUnit && warp == 2 && lane == 0) trace_mark(p, 13);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * p.acc_cols;
 
-      if ((MODE == kPlain || MODE == kConvPixN) && u.slot >= 0) {
+      if ((plain_like<MODE>() || MODE == kConvPixN) && u.slot >= 0) {
         store_tail_piece(p, taddr, u.slot, rank, CG, row);
         ptx::tc_fence_before();
         ptx::named_sync(1, 128);
@@ -703,7 +733,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
                                &tmem_empty[acc], &map_d, n_blk * p.BN, m_blk * BM + rank * kRows,
                                0, 0, 3);
         continue;
-      } else if constexpr (MODE == kPlain) {
+      } else if constexpr (plain_like<MODE>()) {
         const int m = m_blk * BM + rank * kRows + row;
         float* dz = p.d + (long long)z * p.d_batch;
         const float* cz = p.read_c ? p.c + (long long)z * p.d_batch : nullptr;
@@ -835,6 +865,27 @@ CUtensorMap make_map(const void* base, int esize, int rank, const cuuint64_t* di
   return m;
 }
 
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                    cuuint32_t, cuuint32_t, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(ptr);
+  });
+  if (!fn) fail(TK_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable from the driver");
+  return fn;
+}
+
 // [batch][rows][K] K-major operand, box {slab, box_rows, 1}.
 CUtensorMap map_rows(const void* base, int esize, long long K, long long rows, long long batch,
                      long long batch_stride, int box_rows) {
@@ -865,6 +916,38 @@ CUtensorMap map_nhwc(const void* base, int esize, const ConvGeom& g, int wb, int
                        (cuuint32_t)(hb * stride), (cuuint32_t)nb};
   const cuuint32_t trav[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
   return make_map(base, esize, 4, dims, strides, box, stride > 1 ? trav : nullptr);
+}
+
+// NHWC activations in im2col mode: each load is `pixels` consecutive output
+// pixels x one slab of channels.  The bounding box of filter origins runs
+// from -pad (lower corner) to the last origin a window visits (upper corner
+// = pad_after - (R-1)); the traversal steps by the stride in W and H and
+// wraps across rows and images, so a tile is any run of output pixels in
+// NHW order -- no per-image box padding.  Order of the corner arrays: W, H.
+CUtensorMap map_nhwc_im2col(const void* base, int esize, const ConvGeom& g, int pixels) {
+  cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+  cuuint64_t strides[3] = {(cuuint64_t)g.C * esize, (cuuint64_t)g.W * g.C * esize,
+                           (cuuint64_t)g.H * g.W * g.C * esize};
+  const int pad_b = (g.OH - 1) * g.stride + g.R - g.H - g.pad_t;
+  const int pad_r = (g.OW - 1) * g.stride + g.S - g.W - g.pad_l;
+  const int lower[2] = {-g.pad_l, -g.pad_t};
+  const int upper[2] = {pad_r - (g.S - 1), pad_b - (g.R - 1)};
+  const cuuint32_t trav[4] = {1, (cuuint32_t)g.stride, (cuuint32_t)g.stride, 1};
+  CUtensorMap m;
+  const CUresult r = encode_im2col_fn()(
+      &m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+      const_cast<void*>(base), dims, strides, lower, upper, (cuuint32_t)(kSlabBytes / esize),
+      (cuuint32_t)pixels, trav, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(TK_ERR_CUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string(r) + ")");
+  // Same driver workaround as CUTLASS's im2col descriptors (drivers <= 13.1,
+  // tensors under 128 KiB): clear bit 21 of the second descriptor word.
+  int drv = 0;
+  if (cudaDriverGetVersion(&drv) == cudaSuccess && drv <= 13010 &&
+      (size_t)g.N * g.H * g.W * g.C * esize < 131072)
+    reinterpret_cast<uint64_t*>(&m)[1] &= ~(1ull << 21);
+  return m;
 }
 
 int sm_count() {
@@ -1026,7 +1109,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     if (forced == 2 || forced == 4 || forced == 8) p.acc_slots = std::min(p.acc_slots, forced);
     p.acc_cols = 2 * kAccCols / p.acc_slots;
   }
-  if (p.splits < 1 || (MODE != kPlain && MODE != kConvPixN)) {
+  if (p.splits < 1 || (!plain_like<MODE>() && MODE != kConvPixN)) {
     p.splits = 1;
     p.kb_per = p.num_kb;
   }
@@ -1037,11 +1120,11 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     }();
     const long long units_all = (long long)p.num_m * p.num_n * p.batch * p.splits;
     // Grouping only pays once tiles queue up behind the resident wave.
-    p.raster = ((MODE == kPlain || MODE == kConvPixN) && units_all > 2LL * (sm_count() / CG))
+    p.raster = ((plain_like<MODE>() || MODE == kConvPixN) && units_all > 2LL * (sm_count() / CG))
                    ? raster
                    : 0;
   }
-  if (p.tail_q > 1 && (p.splits > 1 || (MODE != kPlain && MODE != kConvPixN))) p.tail_q = 0;
+  if (p.tail_q > 1 && (p.splits > 1 || (!plain_like<MODE>() && MODE != kConvPixN))) p.tail_q = 0;
   const long long total =
       p.tail_q > 1 ? (long long)p.tail_start + (total_tiles_of(p) - p.tail_start) * p.tail_q
                    : (long long)p.num_m * p.num_n * p.batch * p.splits;
@@ -1078,7 +1161,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   }
   TKB_CUDA(cudaLaunchKernelEx(&cfg, fn, ma, mb, md, p));
   note_launch();
-  if constexpr (MODE == kPlain || MODE == kConvPixN) {
+  if constexpr (plain_like<MODE>() || MODE == kConvPixN) {
     if (p.tail_q > 1) {
       const long long rem = total_tiles_of(p) - p.tail_start;
       const long long blocks = rem * CG * ((p.BN + 7) / 8);
@@ -1758,7 +1841,10 @@ size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 //                  NHWC input itself (stride 1, TF32) or on a compacted /
 //                  converted copy (stride 2, BF16), split over K when the
 //                  output has too few tiles to fill the SMs
-enum PlanKind : int { kGatherPlan = 0, kBoxPlan = 1, kPointwisePlan = 2 };
+//   kIm2colPlan    C a whole number of slabs: a plain GEMM whose A rows are
+//                  output pixels loaded by im2col-mode TMA (runs of 128
+//                  pixels in NHW order, one tap per K-slab), filter on N
+enum PlanKind : int { kGatherPlan = 0, kBoxPlan = 1, kPointwisePlan = 2, kIm2colPlan = 3 };
 
 struct ConvPlan {
   int kind = kGatherPlan;
@@ -1826,6 +1912,13 @@ void finish_splits(ConvPlan& c, int num_kb, int splits, size_t out_bytes, long l
   if (c.splits > 1) c.part_bytes = align256((size_t)c.splits * out_bytes);
 }
 
+// Automatic choice of the im2col plan (see plan_conv_impl).
+bool prefer_im2col(const ConvGeom& g, int precision) {
+  (void)g;
+  (void)precision;
+  return false;
+}
+
 ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
   ConvPlan c;
   const long long K = (long long)g.R * g.S * g.C;
@@ -1843,12 +1936,10 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
   const bool pointwise = g.R == 1 && g.S == 1 && g.pad_t == 0 && g.pad_l == 0 && g.C % 8 == 0 &&
                          g.K % 4 == 0 && !(force && std::string(force) != "plain") &&
                          (mode == TK_TC_AUTO || mode == TK_TC_POINTWISE) && !strided_box;
-  if (pointwise) {
-    c.kind = kPointwisePlan;
-    c.tf32 = tf32;
-    c.kp = (g.C + ek - 1) / ek * ek;
-    c.filt_bytes = align256((size_t)g.K * c.kp * esize);
-    c.in_bytes = (g.stride != 1 || !tf32) ? align256((size_t)pix * g.C * esize) : 0;
+  // Pixels-on-M GEMM sizing shared by the pointwise and im2col plans: SM
+  // pair tiles of 256 pixels x bn features, split over K when the tiles
+  // cannot fill the pairs, the last partial wave cut into K-pieces.
+  auto size_pixels_gemm = [&](ConvPlan& c) {
     c.cg = pix > kRows ? 2 : 1;
     const int step = 16 * c.cg;
     c.bn = g.K >= 256 ? 256 : (g.K + step - 1) / step * step;
@@ -1871,6 +1962,26 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
                                 96ull << 20),
                   out_bytes, (long long)c.num_m * c.num_n);
     if (c.splits == 1) c.tail = plan_tail((long long)c.num_m * c.num_n, c.num_kb, c.cg, c.bn);
+  };
+  const bool im2col = conv_boxable(g, precision) && g.K % 4 == 0 &&
+                      (mode == TK_TC_IM2COL || (force && std::string(force) == "im2col") ||
+                       (mode == TK_TC_AUTO && !force && prefer_im2col(g, precision)));
+  if (im2col) {
+    c.kind = kIm2colPlan;
+    c.tf32 = tf32;
+    c.kp = K;
+    c.filt_bytes = align256((size_t)g.K * K * esize);
+    c.in_bytes = tf32 ? 0 : align256((size_t)g.N * g.H * g.W * g.C * 2);
+    size_pixels_gemm(c);
+    return c;
+  }
+  if (pointwise) {
+    c.kind = kPointwisePlan;
+    c.tf32 = tf32;
+    c.kp = (g.C + ek - 1) / ek * ek;
+    c.filt_bytes = align256((size_t)g.K * c.kp * esize);
+    c.in_bytes = (g.stride != 1 || !tf32) ? align256((size_t)pix * g.C * esize) : 0;
+    size_pixels_gemm(c);
     return c;
   }
   if (conv_boxable(g, precision) && mode != TK_TC_GATHER) {
@@ -1982,7 +2093,8 @@ ConvPlan plan_conv(const ConvGeom& g, int precision) {
                   (mode == TK_TC_GATHER && c.kind == kGatherPlan) ||
                   (mode == TK_TC_HALO && c.kind == kBoxPlan && c.halo) ||
                   (mode == TK_TC_PIXN && c.kind == kBoxPlan && !c.halo && c.pix_on_n) ||
-                  (mode == TK_TC_PIXM && c.kind == kBoxPlan && !c.halo && !c.pix_on_n);
+                  (mode == TK_TC_PIXM && c.kind == kBoxPlan && !c.halo && !c.pix_on_n) ||
+                  (mode == TK_TC_IM2COL && c.kind == kIm2colPlan);
   if (!ok) fail(TK_ERR_CAPABILITY, "tc_conv: operand path " + std::to_string(mode) +
                                        " does not apply to this convolution");
   if (cluster != 0 && cluster != c.cg)  // only the pixN plan takes the cluster knob
@@ -2058,6 +2170,76 @@ void launch_pointwise(const ConvGeom& g, const ConvPlan& c, const float* in, con
 }  // namespace
 
 namespace {
+
+// Implicit-GEMM convolution with im2col-mode TMA (see kIm2colPlan): A =
+// output pixels [N*OH*OW][R*S*C] gathered by the TMA unit slab by slab (tap
+// (x, y), channel chunk), B = the packed filter [Kout][R*S*C], the output
+// [pixels][Kout] (NHWC) leaves through the TMA-store epilogue.
+void launch_im2col_conv(const ConvGeom& g, const ConvPlan& c, const float* in, const float* filt,
+                        float* out, char* ws, cudaStream_t st, bool prep, bool run) {
+  const int esize = c.tf32 ? 4 : 2, ek = kSlabBytes / esize;
+  const long long K = (long long)g.R * g.S * g.C;
+  char* cursor = ws;
+  void* ft = cursor;
+  cursor += c.filt_bytes;
+  float* part = reinterpret_cast<float*>(ws + c.filt_bytes + c.in_bytes);
+  if (prep) {
+    if (c.tf32) pack_filter<float>(filt, (int)K, g.K, (int)c.kp, (float*)ft, tf32_filter_rounding(), st);
+    else pack_filter<__nv_bfloat16>(filt, (int)K, g.K, (int)c.kp, (__nv_bfloat16*)ft, false, st);
+  }
+  if (!run) return;
+  const long long pix = (long long)g.N * g.OH * g.OW;
+  const void* a = in;
+  if (!c.tf32) {
+    to_bf16(in, (__nv_bfloat16*)cursor, (long long)g.N * g.H * g.W * g.C, st);
+    a = cursor;
+  }
+  float* dst = c.splits > 1 ? part : out;
+  if (pix > 2147483647ll) fail(TK_ERR_CAPABILITY, "tc_conv: too many output pixels");
+  TcArgs p{};
+  p.M = (int)pix;
+  p.N = g.K;
+  p.K = (int)c.kp;
+  p.BN = c.bn;
+  p.ek = ek;
+  p.num_m = c.num_m;
+  p.num_n = c.num_n;
+  p.batch = 1;
+  p.num_kb = c.num_kb;
+  p.splits = c.splits;
+  p.kb_per = c.kb_per;
+  p.d = out;
+  p.d_sm = g.K;
+  p.d_sn = 1;
+  p.part = part;
+  p.part_stride = pix * g.K;
+  p.alpha = 1.0f;
+  p.OH = g.OH;
+  p.OW = g.OW;
+  p.Kout = g.K;
+  p.S = g.S;
+  p.stride = g.stride;
+  p.pad_t = g.pad_t;
+  p.pad_l = g.pad_l;
+  p.cchunks = g.C / ek;
+  if (c.tail.q > 1) {
+    p.tail_start = c.tail.start;
+    p.tail_q = c.tail.q;
+    p.tail_kb = c.tail.kb;
+    p.tail_part = reinterpret_cast<float*>(reinterpret_cast<char*>(part) + c.part_bytes);
+  }
+  const CUtensorMap ma = map_nhwc_im2col(a, esize, g, kRows);
+  const CUtensorMap mb = map_rows2d(ft, esize, c.kp, g.K, c.bn / c.cg);
+  cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)pix, (cuuint64_t)c.splits};
+  cuuint64_t strides[2] = {(cuuint64_t)g.K * 4, (cuuint64_t)(pix * g.K * 4)};
+  cuuint32_t box[3] = {32, (cuuint32_t)kRows, 1};
+  const CUtensorMap md = make_map(dst, 4, 3, dims, strides, box);
+  p.store_tma = 1;
+  p.epi_bufs = 2;
+  dispatch<kConvIm2col>(ma, mb, md, p, c.cg, c.tf32, st);
+  if (c.splits > 1) splitk_reduce(part, pix * g.K, c.splits, out, st);
+}
+
 ConvGeom tripled(const ConvGeom& g) {
   ConvGeom t = g;
   t.C = 3 * g.C;
@@ -2117,6 +2299,10 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   char* cursor = static_cast<char*>(ws);
   if (plan.kind == kPointwisePlan) {
     launch_pointwise(g, plan, in, filt, out, cursor, st, prep, run);
+    return;
+  }
+  if (plan.kind == kIm2colPlan) {
+    launch_im2col_conv(g, plan, in, filt, out, cursor, st, prep, run);
     return;
   }
 

@@ -277,6 +277,30 @@ __device__ __forceinline__ void tma4(void* dst, const CUtensorMap* m, uint32_t b
         : "memory");
 }
 
+// Im2col-mode TMA over an NHWC tensor map (cuTensorMapEncodeIm2col): loads
+// pixelsPerColumn consecutive output pixels of the (w, h, n) traversal that
+// starts at input coordinate (w, h, n), each shifted by the filter tap
+// (off_w, off_h); channels [c, c + channelsPerPixel).  Taps outside the input
+// are zero-filled.
+template <int CG>
+__device__ __forceinline__ void tma4_im2col(void* dst, const CUtensorMap* m, uint32_t bar, int c,
+                                            int w, int h, int n, uint16_t off_w, uint16_t off_h) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};\n" ::"r"(smem(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n),
+        "h"(off_w), "h"(off_h)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.4d.im2col.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};\n" ::"r"(smem(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n),
+        "h"(off_w), "h"(off_h)
+        : "memory");
+}
+
 template <int CG, uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_cg(uint32_t* dst_smem) {
   if constexpr (CG == 1) {

@@ -1,0 +1,98 @@
+"""GPU parity of the im2col-mode TMA convolution path (tk_exec_options.tc_mode
+= TK_TC_IM2COL): output pixels on the MMA M side, loaded 128 at a time in
+NHW order by cp.async.bulk.tensor.*.im2col, one filter tap per K-slab.
+
+Checked against the CPU oracle's conv2d_naive (conv.hpp:74-113) with the
+tolerances of test_gpu_tc.py (TF32 <= 1e-3, BF16 <= 5e-3 max_scaled_error,
+numeric.hpp:39-56); runs are deterministic bit for bit.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"tf32": 1e-3, "bf16": 5e-3}
+
+
+def run_mode(tk, x, f, shape, prec, mode="im2col", split=0):
+    import torch
+    dx, df = torch.from_numpy(x).cuda(), torch.from_numpy(f).cuda()
+    dy = torch.full(shape.out_shape, float("nan"), device="cuda")
+    opts = tk.exec_options(prec, mode=mode, split=split)
+    p = tk.parse_conv_params("im2col")
+    ws = torch.empty(max(tk.conv2d_workspace_size(shape, p, options=opts), 4) // 4 + 1,
+                     device="cuda")
+    tk.conv2d_dev(dx, df, dy, shape, p, workspace=ws, options=opts)
+    torch.cuda.synchronize()
+    return dy.cpu().numpy()
+
+
+def case(oracle, N, H, W, C, K, R, stride, same, seed=11):
+    conv = oracle.Conv(N, H, W, C, K, R, R, stride, same)
+    x = oracle.fill_random(int(np.prod(conv.in_shape)), seed).reshape(conv.in_shape)
+    f = oracle.fill_random(int(np.prod(conv.filt_shape)), seed + 1).reshape(conv.filt_shape)
+    return conv, x, f, oracle.conv2d_naive(conv, x, f)
+
+
+SHAPES = [
+    # N, H, W, C, K, R, stride, same
+    (2, 14, 14, 64, 256, 3, 1, True),     # 14x14 planes: tiles cross image boundaries
+    (3, 7, 7, 128, 128, 3, 1, True),      # 7x7 planes (ResNet res5 geometry)
+    (1, 28, 28, 32, 128, 3, 1, True),
+    (2, 17, 23, 32, 96, 3, 1, True),      # ragged plane, features not a multiple of 32
+    (2, 20, 18, 32, 64, 3, 1, False),     # Valid
+    (2, 20, 18, 64, 64, 3, 2, True),      # stride 2, Same (pad smaller first)
+    (2, 21, 19, 32, 128, 3, 2, False),    # stride 2, Valid, odd plane
+    (2, 16, 16, 64, 128, 1, 1, True),     # 1x1
+    (2, 15, 15, 64, 128, 1, 2, True),     # 1x1 stride 2
+    (2, 12, 12, 64, 64, 5, 1, True),      # 5x5
+    (1, 20, 20, 64, 64, 7, 2, True),      # 7x7 / 2
+    (1, 4, 4, 64, 32, 3, 1, True),        # tiny tensor (< 128 KiB descriptor workaround)
+    (1, 1, 1, 64, 64, 3, 1, True),        # one-pixel plane
+]
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_im2col_tma_matches_oracle(tk, oracle, shape, prec):
+    N, H, W, C, K, R, stride, same = shape
+    if prec == "bf16" and C % 64:
+        pytest.skip("BF16 slabs hold 64 channels")
+    conv, x, f, want = case(oracle, *shape)
+    s = tk.ConvShape(N, H, W, C, K, R, R, stride, same)
+    got = run_mode(tk, x, f, s, prec)
+    assert not np.isnan(got).any()
+    err = oracle.max_scaled_error(got, want)
+    assert err <= TOL[prec], err
+
+
+@pytest.mark.parametrize("split", [1, 3])
+def test_im2col_tma_split_k_and_determinism(tk, oracle, split):
+    shape = (4, 14, 14, 128, 256, 3, 1, True)
+    conv, x, f, want = case(oracle, *shape, seed=21)
+    s = tk.ConvShape(*shape[:5], 3, 3, 1, True)
+    a = run_mode(tk, x, f, s, "tf32", split=split)
+    b = run_mode(tk, x, f, s, "tf32", split=split)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert oracle.max_scaled_error(a, want) <= TOL["tf32"]
+
+
+def test_im2col_tma_matches_box_path(tk, oracle):
+    """Same convolution through the tiled-box path and the im2col path."""
+    shape = (4, 28, 28, 128, 128, 3, 1, True)
+    conv, x, f, want = case(oracle, *shape, seed=31)
+    s = tk.ConvShape(*shape[:5], 3, 3, 1, True)
+    a = run_mode(tk, x, f, s, "tf32", mode="im2col")
+    b = run_mode(tk, x, f, s, "tf32", mode="auto")
+    assert oracle.max_scaled_error(a, want) <= TOL["tf32"]
+    assert oracle.max_scaled_error(b, want) <= TOL["tf32"]
+    # both truncate the same TF32 operands: differences are summation order only
+    assert oracle.max_scaled_error(a, b) <= 2e-5
+
+
+def test_im2col_mode_rejects_unboxable_channels(tk, oracle):
+    import torch
+    s = tk.ConvShape(1, 8, 8, 3, 16, 3, 3, 1, True)
+    opts = tk.exec_options("tf32", mode="im2col")
+    with pytest.raises(tk.CapabilityError):
+        tk.conv2d_workspace_size(s, tk.parse_conv_params("im2col"), options=opts)

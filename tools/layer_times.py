@@ -21,6 +21,8 @@ ap.add_argument("prec", nargs="?", default="tf32")
 ap.add_argument("batch", nargs="?", type=int, default=32)
 ap.add_argument("--only", default="")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--mode", default="auto", help="tensor-core operand path (tk.TC_MODES)")
+ap.add_argument("--split", type=int, default=0)
 ap.add_argument("--flush", default="read", choices=["read", "write"],
                 help="evict L2 by reading (clean lines) or writing (dirty lines whose "
                      "write-back then lands on the timed kernel) a 256 MiB buffer")
@@ -45,12 +47,18 @@ for name, r, s, h, c, k in rows:
     x = torch.rand(shp.in_shape, device="cuda") * 2 - 1
     f = torch.rand(shp.filt_shape, device="cuda") * 2 - 1
     y = torch.empty(shp.out_shape, device="cuda")
-    ws = torch.empty(max(tk.conv2d_workspace_size(shp, p, a.prec), 4) // 4 + 1, device="cuda")
-    tk.conv2d_prepare_dev(f, shp, p, ws, precision=a.prec, stream=st)
+    opts = tk.exec_options(a.prec, mode=a.mode, split=a.split)
+    try:
+        ws = torch.empty(max(tk.conv2d_workspace_size(shp, p, options=opts), 4) // 4 + 1,
+                         device="cuda")
+    except tk.CapabilityError:
+        print(f"{name:18s} {'n/a':>8s}")
+        continue
+    tk.conv2d_prepare_dev(f, shp, p, ws, stream=st, options=opts)
     st.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=st):
-        tk.conv2d_run_dev(x, f, y, shp, p, ws, precision=a.prec, stream=st)
+        tk.conv2d_run_dev(x, f, y, shp, p, ws, stream=st, options=opts)
     ts = []
     for i in range(a.reps + 2):
         if a.flush == "write":

@@ -50,7 +50,7 @@ int main(int argc, char** argv) {
   space.tc_stages = {0, 4};
   space.tc_clusters = {0, 1};
   space.tc_modes = {b200::TcMode::Auto, b200::TcMode::Halo, b200::TcMode::PixN,
-                    b200::TcMode::PixM, b200::TcMode::Pointwise};
+                    b200::TcMode::PixM, b200::TcMode::Pointwise, b200::TcMode::Im2col};
   BenchOptions opts;
   opts.warmup = 2;
   opts.samples = 5;
