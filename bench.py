@@ -301,6 +301,7 @@ def main():
     # value.  gpu_launches counts the kernels inside the graph.
     graph = None
     launches_per_step = None
+    join_each = os.environ.get("BENCH_JOIN_EACH", "0") == "1"  # A/B of the graph's join structure
     if not args.no_graph:
         cap = torch.cuda.Stream(device=dev)
         cap.wait_stream(stream)
@@ -311,17 +312,29 @@ def main():
             # Filter-side work (prepare: tensor-core filter repack) depends only
             # on the filters: fork it to a side stream so it overlaps earlier
             # layers; each layer's run joins on its own prepare.
+            # Two joins only: the first layer waits for its own prepare, the
+            # second for all of them (done long before the first layer ends);
+            # layers 2..13 then follow each other in plain stream order, so
+            # every launch keeps its programmatic (PDL) edge to the previous
+            # layer -- an event join per layer would turn each of those into a
+            # full dependency (~8 us per layer boundary measured).
             side.wait_stream(cap)
             ready = []
             with torch.cuda.stream(side):
-                for L in layers:
+                for i, L in enumerate(layers):
                     tk.conv2d_prepare_dev(L["f"], L["shape"], L["algo"], L["ws"], precision=prec,
                                           stream=side)
-                    ev = torch.cuda.Event()
-                    ev.record(side)
-                    ready.append(ev)
-            for L, ev in zip(layers, ready):
-                cap.wait_event(ev)
+                    if i == 0 or i == len(layers) - 1 or join_each:
+                        ev = torch.cuda.Event()
+                        ev.record(side)
+                        ready.append(ev)
+            for i, L in enumerate(layers):
+                if join_each:
+                    cap.wait_event(ready[i])
+                elif i == 0:
+                    cap.wait_event(ready[0])
+                elif i == 1:
+                    cap.wait_event(ready[-1])
                 tk.conv2d_run_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], L["ws"],
                                   precision=prec, stream=cap)
             cap.wait_stream(side)
@@ -336,33 +349,63 @@ def main():
         else:
             step()
 
-    # Per-layer device times (same stream, CUDA events), for the roofline.
-    # (each layer replayed from its own graph so host launch latency does not
-    # pad the small layers; median of 3)
+    # Per-layer device times of the conv kernels (same stream, CUDA events),
+    # for the roofline.  With graphs: one graph replays R x [L2 flush, the
+    # layer's run phase] and a second R x [L2 flush]; the layer's kernel time
+    # is their difference / R -- L2-cold like the step, without the graph
+    # launch latency (~4-6 us) that an event pair around one replay adds.
+    # The filter prepare (tiny, overlapped in the step) is not included.
     per_layer = []
-    for L in layers:
-        lg = None
-        if not args.no_graph:
-            cap = torch.cuda.Stream(device=dev)
-            cap.wait_stream(stream)
-            lg = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(lg, stream=cap):
-                tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=prec,
-                              workspace=L["ws"], stream=cap)
+    reps = 4
+
+    def timed(fn, n=3, pre=None):
         ts = []
-        for _ in range(3):
+        for _ in range(n):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-            flush.zero_()
+            if pre is not None:
+                pre()
+            torch.cuda.synchronize()
             ev[0].record(stream)
-            if lg is not None:
-                lg.replay()
-            else:
-                tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=prec,
-                              workspace=L["ws"], stream=stream)
+            fn()
             ev[1].record(stream)
             torch.cuda.synchronize()
             ts.append(ev[0].elapsed_time(ev[1]))
-        per_layer.append(float(np.median(ts)))
+        return float(np.median(ts))
+
+    flush_ms = None
+    if not args.no_graph:
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(stream)
+        fg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(fg, stream=cap):
+            for _ in range(reps):
+                flush.zero_()
+        with torch.cuda.stream(stream):
+            flush_ms = timed(fg.replay)
+
+    def kernel_ms(run_on):
+        """Device time of run_on(stream) (a prepared layer's run phase),
+        L2-cold, without launch latency (graph of reps x [flush, run])."""
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(stream)
+        lg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(lg, stream=cap):
+            for _ in range(reps):
+                flush.zero_()
+                run_on(cap)
+        with torch.cuda.stream(stream):
+            return max(timed(lg.replay) - flush_ms, 1e-6) / reps
+
+    for L in layers:
+        if not args.no_graph:
+            per_layer.append(kernel_ms(
+                lambda st, L=L: tk.conv2d_run_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"],
+                                                  L["ws"], precision=prec, stream=st)))
+        else:
+            def one(L=L):
+                tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=prec,
+                              workspace=L["ws"], stream=stream)
+            per_layer.append(timed(one, pre=flush.zero_))
 
     # Timed steps.
     if world > 1:
@@ -617,6 +660,20 @@ def main():
                                             "unit": "GFLOP/s", "ms_per_step": round(ms, 3),
                                             "step_gflop": round(rn_flops / 1e9, 2),
                                             "batch_per_gpu": N}
+            if not args.no_graph and p_ == prec:
+                # Kernel time per distinct layer shape (first instance, its
+                # filter prepared by the pass above), as the VGG layers.
+                pk = peaks["bf16_tflops"] / (2.0 if p_ == "tf32" else 1.0)
+                rows, k0 = [], 0
+                for (name, *_rest), (shp, x, f, y, ws, mult, fl) in zip(RESNET50, rn):
+                    _, _, _, _, ws0 = inst[k0]
+                    k0 += mult
+                    kms = kernel_ms(lambda st, shp=shp, x=x, f=f, y=y, ws0=ws0: tk.conv2d_run_dev(
+                        x, f, y, shp, im2col, ws0, precision=p_, stream=st))
+                    rows.append({"layer": name, "ms": round(kms, 4),
+                                 "tflops": round(fl / (kms * 1e-3) / 1e12, 1),
+                                 "frac_of_peak": round(fl / (kms * 1e-3) / 1e12 / pk, 3)})
+                secondary[f"resnet50_{p_}"]["layers"] = rows
         del rn
         # BASELINE configs[3]: large square GEMMs on the tensor cores
         # (column-major nn through tk_gemm_dev; operands in HBM, > L2 from 4096).

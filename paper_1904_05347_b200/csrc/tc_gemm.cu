@@ -97,6 +97,7 @@ struct TcArgs {
   int store_tma;               // epilogue via swizzled smem tile + TMA store
   int epi_bytes;               // bytes of epilogue staging
   int epi_bufs;                // staging buffers for the TMA-store epilogue
+  int epi_ring;                // > 0: staging halves of epi_ring 32-column chunks (tma_store_epilogue)
   // TMEM accumulator ring: acc_slots slots of acc_cols columns (512 / slots);
   // more slots for narrow tiles let the MMA run further ahead of the
   // epilogue, decoupling their per-tile handshakes.
@@ -128,12 +129,17 @@ struct TcArgs {
   // L2-aware raster (plain / pixN): tiles are visited in groups of `raster`
   // M-blocks, N-blocks within a group, so a wave of CTAs shares A and B tiles.
   int raster;
-  // Wave-quantisation tail (plain / pixN, splits == 1): tiles >= tail_start
-  // (the last partial wave) are cut into tail_q K-pieces of tail_kb slabs so
-  // the final wave spreads over every SM pair; each piece stores its
-  // partial tile column-major (tile-local, [BN][128] per CTA) in tail_part,
-  // and tail_reduce sums the pieces in order into the output.
-  int tail_start, tail_q, tail_kb;
+  // Balanced tail (plain / pixN, splits == 1; stream-K over the last partial
+  // wave): the tail_W = (tiles - tail_start) x num_kb slab-steps of the
+  // tiles >= tail_start are dealt to the tail_P SM pairs as equal contiguous
+  // ranges [p W / P, (p+1) W / P) in (tile, slab) order.  Pair p's range is
+  // cut at tile boundaries into at most tail_kb segments, visited as units
+  // tail_start + j P + p.  A tile covered by one segment is stored directly;
+  // otherwise every segment stores its partial tile column-major (tile-
+  // local, [BN][128] per CTA) in slot tile * tail_q + piece of tail_part, and
+  // tail_reduce sums the pieces in order into the output (deterministic).
+  int tail_start, tail_q, tail_kb, tail_P;
+  long long tail_W;
   float* tail_part;
   // Timeline probe (TK_TC_TRACE=1, experiments only): per CTA, globaltimer
   // stamps of kTraceEvents milestones.
@@ -156,16 +162,10 @@ struct Unit {
   int slot;  // tail piece slot (-1: a whole tile)
 };
 
-__device__ __forceinline__ Unit decode_unit(const TcArgs& p, int t) {
+// Tile t -> (m_blk, n_blk, z, split) with the split's K-slab range.
+__device__ __forceinline__ Unit decode_tile(const TcArgs& p, int t) {
   Unit u;
   u.slot = -1;
-  int piece = -1;
-  if (p.tail_q > 1 && t >= p.tail_start) {
-    const int d = t - p.tail_start;
-    piece = d % p.tail_q;
-    u.slot = d;
-    t = p.tail_start + d / p.tail_q;
-  }
   const int per = p.num_m * p.num_n;
   int rest = t / per;
   const int t2 = t - rest * per;
@@ -185,11 +185,39 @@ __device__ __forceinline__ Unit decode_unit(const TcArgs& p, int t) {
   u.sp = rest / p.batch;
   u.kb0 = u.sp * p.kb_per;
   u.kb1 = min(p.num_kb, u.kb0 + p.kb_per);
-  if (piece >= 0) {
-    u.kb0 = piece * p.tail_kb;
-    u.kb1 = min(p.num_kb, u.kb0 + p.tail_kb);
-  }
   return u;
+}
+
+// Balanced tail: the pair whose range holds slab-step s (ranges [b_p,
+// b_{p+1}), b_p = floor(p W / P)) is ceil((s + 1) P / W) - 1.
+__device__ __forceinline__ int tail_owner(const TcArgs& p, long long s) {
+  return (int)(((s + 1) * p.tail_P + p.tail_W - 1) / p.tail_W) - 1;
+}
+
+// Unit t -> tile and K-slab range; tail units may be empty (kb0 == kb1).
+__device__ __forceinline__ Unit decode_unit(const TcArgs& p, int t) {
+  if (p.tail_q > 1 && t >= p.tail_start) {
+    const int d = t - p.tail_start;
+    const int pr = d % p.tail_P, j = d / p.tail_P;
+    const long long nk = p.num_kb;
+    const long long b1 = (long long)(pr + 1) * p.tail_W / p.tail_P;
+    long long s = (long long)pr * p.tail_W / p.tail_P;
+    for (int i = 0; i < j && s < b1; ++i) s = (s / nk + 1) * nk;
+    if (s >= b1) {
+      Unit e = decode_tile(p, p.tail_start);
+      e.kb0 = e.kb1 = 0;
+      return e;
+    }
+    const int r = (int)(s / nk);
+    const long long e = min(b1, (long long)(r + 1) * nk);
+    Unit u = decode_tile(p, p.tail_start + r);
+    u.kb0 = (int)(s - r * nk);
+    u.kb1 = (int)(e - r * nk);
+    const int p0 = tail_owner(p, r * nk), p1 = tail_owner(p, (r + 1) * nk - 1);
+    u.slot = p0 == p1 ? -1 : r * p.tail_q + (pr - p0);
+    return u;
+  }
+  return decode_tile(p, t);
 }
 
 // Tail piece epilogue: this thread's accumulator row (TMEM lane `row`) into
@@ -237,11 +265,56 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
                                                    int srow,
                                                    uint32_t empty_cluster_addr, uint64_t* empty_local,
                                                    const CUtensorMap* map_d, int c0, int c1, int c2,
-                                                   int c3, int rank_dims) {
+                                                   int c3, int rank_dims, int& ring) {
   const int nchunks = (p.BN + 31) / 32;
+  const bool issuer = warp == 2 && lane == 0;
+  if (p.epi_ring) {
+    // Staging in two halves of epi_ring 32-column chunks each (as little as
+    // 2 x 16 KiB whatever the tile width): the chunks go out in batches of
+    // epi_ring, each batch one bulk group; a batch waits only for the batch
+    // before the previous one to have been read.  epi_ring >= nchunks is the
+    // whole-tile double buffer.
+    const int bs = p.epi_ring;
+    for (int j0 = 0; j0 < nchunks; j0 += bs) {
+      const int nb = min(bs, nchunks - j0);
+      uint8_t* half = stage + (ring & 1) * bs * kRows * kSlabBytes;
+      ++ring;
+      if (issuer) ptx::bulk_wait_read<1>();
+      ptx::named_sync(1, 128);
+      for (int jj = 0; jj < nb; ++jj) {
+        float v[32];
+        ptx::tmem_ld32(taddr + (j0 + jj) * 32, v);
+        if (srow < 0) continue;
+        const uint32_t rowp = ptx::smem(half + jj * kRows * kSlabBytes + srow * kSlabBytes);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(rowp + ((c ^ (srow & 7)) << 4)),
+                       "f"(p.alpha * v[4 * c]), "f"(p.alpha * v[4 * c + 1]),
+                       "f"(p.alpha * v[4 * c + 2]), "f"(p.alpha * v[4 * c + 3])
+                       : "memory");
+        }
+      }
+      const bool last = j0 + nb == nchunks;
+      if (last) ptx::tc_fence_before();
+      ptx::fence_proxy_async();
+      ptx::named_sync(1, 128);
+      if (issuer) {
+        if (last) {
+          if constexpr (CG == 2) ptx::mbar_arrive_remote(empty_cluster_addr);
+          else ptx::mbar_arrive(empty_local);
+        }
+        for (int jj = 0; jj < nb; ++jj) {
+          const uint8_t* src = half + jj * kRows * kSlabBytes;
+          if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + 32 * (j0 + jj), c1, c2, c3);
+          else ptx::tma_store_3d(map_d, src, c0 + 32 * (j0 + jj), c1, c2);
+        }
+        ptx::bulk_commit();
+      }
+    }
+    return;
+  }
   const int buf_bytes = nchunks * kRows * kSlabBytes;
   uint8_t* sbuf = stage + (p.epi_bufs > 1 ? (local & 1) : 0) * buf_bytes;
-  const bool issuer = warp == 2 && lane == 0;
   if (issuer) {
     if (p.epi_bufs > 1) ptx::bulk_wait_read<1>();
     else ptx::bulk_wait_read<0>();
@@ -448,9 +521,8 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   ptx::griddep_wait();
   if (threadIdx.x == 0) trace_mark(p, 1);  // barriers + TMEM ready
 
-  const int total = p.tail_q > 1
-                        ? p.tail_start + (p.num_m * p.num_n * p.batch - p.tail_start) * p.tail_q
-                        : p.num_m * p.num_n * p.batch * p.splits;
+  const int total = p.tail_q > 1 ? p.tail_start + p.tail_kb * p.tail_P
+                                  : p.num_m * p.num_n * p.batch * p.splits;
   const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
 
   if (MODE == kConvHalo && warp == 0) {
@@ -634,15 +706,17 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       const uint64_t kdesc = ptx::desc_sw128(0);
       int stage = 0;
       uint32_t phase = 0;
-      int local = 0;
-      for (int t = unit; t < total; t += nunits, ++local) {
+      int nlocal = 0;
+      for (int t = unit; t < total; t += nunits) {
+        const Unit u = decode_unit(p, t);
+        if (u.kb0 >= u.kb1) continue;  // empty tail segment
+        const int local = nlocal++;
         const int acc = local % p.acc_slots;
         const uint32_t acc_phase = (uint32_t)(local / p.acc_slots) & 1u;
         ptx::mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         if (local == kTraceUnit && lane == 0) trace_mark(p, 10);
         const uint32_t d_tmem = tmem_base + acc * p.acc_cols;
-        const Unit u = decode_unit(p, t);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
@@ -696,9 +770,12 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
     const int row = q * 32 + lane;
     uint32_t empty_base = ptx::smem(&tmem_empty[0]);
     if constexpr (CG == 2) empty_base = ptx::map_to_rank(empty_base, 0);
-    int local = 0;
-    for (int t = unit; t < total; t += nunits, ++local) {
+    int nlocal = 0;
+    int ering = 0;  // staging chunk sequence (chunk-ring epilogue)
+    for (int t = unit; t < total; t += nunits) {
       const Unit u = decode_unit(p, t);
+      if (u.kb0 >= u.kb1) continue;  // empty tail segment
+      const int local = nlocal++;
       const int m_blk = u.m_blk, n_blk = u.n_blk, z = u.z;
       const int acc = local % p.acc_slots;
       const uint32_t acc_phase = (uint32_t)(local / p.acc_slots) & 1u;
@@ -726,12 +803,12 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         const int srow = w < p.TW ? h * p.TW + w : -1;
         tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, srow,
                                empty_base + 8u * acc, &tmem_empty[acc], &map_d, hn * p.BN, pt.ow0,
-                               pt.oh0 + rank * p.TH, pt.img, 4);
+                               pt.oh0 + rank * p.TH, pt.img, 4, ering);
         continue;
       } else if constexpr (MODE == kConvGather) {
         tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, row, empty_base + 8u * acc,
                                &tmem_empty[acc], &map_d, n_blk * p.BN, m_blk * BM + rank * kRows,
-                               0, 0, 3);
+                               0, 0, 3, ering);
         continue;
       } else if constexpr (plain_like<MODE>()) {
         const int m = m_blk * BM + rank * kRows + row;
@@ -740,7 +817,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         if (p.store_tma) {
           tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, row, empty_base + 8u * acc,
                                  &tmem_empty[acc], &map_d, n_blk * p.BN,
-                                 m_blk * BM + rank * kRows, u.sp * p.batch + z, 0, 3);
+                                 m_blk * BM + rank * kRows, u.sp * p.batch + z, 0, 3, ering);
           continue;
         }
         for (int col = 0; col < p.BN; col += 32) {
@@ -800,7 +877,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         const PixTile pt = pix_tile(p, m_blk);
         tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, row, empty_base + 8u * acc,
                                &tmem_empty[acc], &map_d, n_blk * p.BN, pt.ow0,
-                               pt.oh0 + rank * p.boxH, pt.img, 4);
+                               pt.oh0 + rank * p.boxH, pt.img, 4, ering);
         continue;
       }
       ptx::tc_fence_before();
@@ -976,12 +1053,15 @@ __global__ void __launch_bounds__(256) tail_reduce_kernel(TcArgs p) {
   const int col = (rem - rank * col_blocks) * 8 + threadIdx.x / 32;
   const int row = (threadIdx.x % 32) * 4;
   if (col >= p.BN) return;
-  const Unit u = decode_unit(p, p.tail_start + r * p.tail_q);
+  const long long nk = p.num_kb;
+  const int pieces = tail_owner(p, (r + 1) * nk - 1) - tail_owner(p, r * nk) + 1;
+  if (pieces < 2) return;  // stored directly by its only segment
+  const Unit u = decode_tile(p, p.tail_start + r);
   const long long tile = (long long)p.BN * 128;
   const float* src =
       p.tail_part + ((long long)r * p.tail_q * CG + rank) * tile + (long long)col * 128 + row;
   float4 a = __ldcs(reinterpret_cast<const float4*>(src));
-  for (int q = 1; q < p.tail_q; ++q) {
+  for (int q = 1; q < pieces; ++q) {
     const float4 b = __ldcs(reinterpret_cast<const float4*>(src + (long long)q * CG * tile));
     a.x += b.x;
     a.y += b.y;
@@ -1027,15 +1107,33 @@ __global__ void __launch_bounds__(256) tail_reduce_kernel(TcArgs p) {
 inline long long total_tiles_of(const TcArgs& p) { return (long long)p.num_m * p.num_n * p.batch; }
 
 struct TailPlan {
-  int start = 0, q = 0, kb = 0;
+  int start = 0, q = 0, kb = 0, P = 0;  // q: max pieces per tile, kb: segments per pair
+  long long W = 0;
   size_t bytes = 0;
+  double cost_us = 0;                   // modelled time of the whole launch with this tail
 };
 
-// Wave-quantisation tail: with T tiles on P SM pairs, the last T % P tiles
-// would run as a partial wave as long as a full one; cut each into q <= P /
-// (T % P) K-pieces instead when the cost model (same constants as
-// choose_splits: per-slab max(MMA, operand feed), ~1 us per unit, the
-// reduction pass at ~4 TB/s + launch) says the shorter final round pays.
+// Per-slab time of an SM pair (us): max(MMA, operand feed) -- the constants
+// of choose_splits.
+inline double slab_time_us(int cg, int bn) {
+  const int bm = kRows * cg;
+  const double mma_clk = 4.0 * (double)bm * bn * 8 / 3782.0;
+  const double feed_clk = (double)(bm / 2 + bn / 2) * 128 / 70.0;
+  return std::max(mma_clk, feed_clk) / 1900.0;
+}
+
+// Modelled time (us) of `tiles` whole tiles of num_kb slabs in waves.
+inline double waves_cost_us(long long tiles, int num_kb, int cg, int bn) {
+  const long long pairs = sm_count() / cg;
+  return (double)((tiles + pairs - 1) / pairs) * (num_kb * slab_time_us(cg, bn) + 1.0);
+}
+
+// Wave-quantisation tail, stream-K style: with T tiles on P SM pairs the
+// last T % P tiles (all of them when T < P) would run as a partial wave as
+// long as a full one; instead their slab-steps are dealt evenly to all P
+// pairs (see TcArgs::tail_*).  Taken when the cost model (per-slab max(MMA,
+// operand feed), ~1 us per unit, the reduction pass over the partial tiles
+// at ~4 TB/s + launch) says it pays.
 TailPlan plan_tail(long long tiles, int num_kb, int cg, int bn) {
   TailPlan t;
   static const bool off = [] {
@@ -1044,27 +1142,39 @@ TailPlan plan_tail(long long tiles, int num_kb, int cg, int bn) {
   }();
   const long long pairs = sm_count() / cg;
   const long long rem = tiles % pairs, full = tiles / pairs;
-  if (off || tc_knobs().split == 1 || rem == 0 || full < 1 || num_kb < 8) return t;
-  const int bm = kRows * cg;
-  const double mma_clk = 4.0 * (double)bm * bn * 8 / 3782.0;
-  const double feed_clk = (double)(bm / 2 + bn / 2) * 128 / 70.0;
-  const double slab_us = std::max(mma_clk, feed_clk) / 1900.0;
-  const double tile_bytes = (double)bm * bn * 4;
-  const double base = num_kb * slab_us + 1.0;
-  double best = base * 0.85;  // demand a clear win
-  for (int q = 2; q <= pairs / rem && num_kb / q >= 4; ++q) {
-    const int kb = (num_kb + q - 1) / q;
-    const double cost = kb * slab_us + 1.0 + 2.0 + (q + 1) * rem * tile_bytes / 4.0e6;
-    if (cost < best) {
-      best = cost;
-      t.q = (num_kb + kb - 1) / kb;
-      t.kb = kb;
-    }
-  }
-  if (t.q < 2) return TailPlan{};
+  const double base = waves_cost_us(tiles, num_kb, cg, bn);
+  t.cost_us = base;
+  if (off || tc_knobs().split == 1 || rem == 0 || num_kb < 4) return t;
+  const long long W = rem * (long long)num_kb;
+  if (W < 2 * pairs) return t;  // every pair needs >= 2 slab-steps
+  const double slab = slab_time_us(cg, bn);
+  const double tile_bytes = (double)kRows * cg * bn * 4;
+  const long long per = (W + pairs - 1) / pairs;
+  const int segs = (int)((per + num_kb - 1) / num_kb) + 1;
+  const int q = (int)((num_kb * pairs + W - 1) / W) + 1;  // pieces per tile, upper bound
+  // pieces written: ~ one per pair plus one per tile; read once, tiles written once
+  const double red_bytes = (double)(pairs + rem) * tile_bytes * 2 + (double)rem * tile_bytes;
+  const double cost = (double)full * (num_kb * slab + 1.0) + per * slab + 1.0 * segs + 2.0 +
+                      red_bytes / 4.0e6;
+  if (cost >= base * 0.9) return t;  // demand a clear win
   t.start = (int)(tiles - rem);
+  t.q = std::max(q, 2);
+  t.kb = segs;
+  t.P = (int)pairs;
+  t.W = W;
   t.bytes = (size_t)rem * t.q * cg * bn * 128 * 4;
+  t.cost_us = cost;
   return t;
+}
+
+void apply_tail(TcArgs& p, const TailPlan& t, float* buf) {
+  if (t.q < 2) return;
+  p.tail_start = t.start;
+  p.tail_q = t.q;
+  p.tail_kb = t.kb;
+  p.tail_P = t.P;
+  p.tail_W = t.W;
+  p.tail_part = buf;
 }
 
 template <int MODE, int CG, bool TF32>
@@ -1081,14 +1191,37 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   if (tc_knobs().stages > 0) stages_req = tc_knobs().stages;
   if (const char* e = getenv("TK_TC_STAGES")) stages_req = atoi(e);
   if (const char* e = getenv("TK_TC_EPI")) p.epi_bufs = std::min(p.epi_bufs, atoi(e));
+  {
+    // Chunk-ring staging (32 KiB) for tiles wider than one chunk.
+    static const bool ring_on = [] {
+      const char* e = getenv("TK_EPI_RING");
+      return !(e && e[0] == '0');
+    }();
+    p.epi_ring = (p.store_tma && ring_on && p.BN > 32) ? 1 : 0;
+  }
   // Double-buffered TMA-store staging when it leaves room for >= 3 stages.
   if (p.store_tma && p.epi_bufs > 1 &&
       232448 - 2048 - ktab_bytes0 - 2 * ((p.BN + 31) / 32) * kRows * kSlabBytes < 3 * stage_bytes)
     p.epi_bufs = 1;
-  const int epi_bytes =
-      p.store_tma ? p.epi_bufs * ((p.BN + 31) / 32) * kRows * kSlabBytes : 0;
-  p.epi_bytes = epi_bytes;
   const int ktab_bytes = MODE == kConvGather ? p.num_kb * 32 * 8 : 0;
+  constexpr int kChunkBytes = kRows * kSlabBytes;
+  if (p.epi_ring) {
+    // Batch size: whole tiles double-buffered (two syncs per tile) when the
+    // operand ring still gets every stage a unit can use, else smaller
+    // batches down to single chunks.
+    const int nchunks = (p.BN + 31) / 32;
+    const int room = 232448 - 1024 - 1024 - ktab_bytes - fres_bytes;
+    const int kb_unit = std::max(1, std::min(p.num_kb, p.splits > 1 ? p.kb_per : p.num_kb));
+    const int want = std::min(kMaxStages, std::max(3, kb_unit + 1));
+    int bs = (room - want * stage_bytes) / (2 * kChunkBytes);
+    bs = std::max(1, std::min(nchunks, bs));
+    if (const char* e = getenv("TK_EPI_RING_N")) bs = std::max(1, std::min(nchunks, atoi(e)));
+    p.epi_ring = bs;
+  }
+  const int epi_bytes = !p.store_tma ? 0
+                       : p.epi_ring ? 2 * p.epi_ring * kChunkBytes
+                                    : p.epi_bufs * ((p.BN + 31) / 32) * kChunkBytes;
+  p.epi_bytes = epi_bytes;
   const int budget = 232448 - 1024 - 1024 - epi_bytes - ktab_bytes - fres_bytes;
   int stages = budget / stage_bytes;
   if (stages > kMaxStages) stages = kMaxStages;
@@ -1125,9 +1258,8 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
                    : 0;
   }
   if (p.tail_q > 1 && (p.splits > 1 || (!plain_like<MODE>() && MODE != kConvPixN))) p.tail_q = 0;
-  const long long total =
-      p.tail_q > 1 ? (long long)p.tail_start + (total_tiles_of(p) - p.tail_start) * p.tail_q
-                   : (long long)p.num_m * p.num_n * p.batch * p.splits;
+  const long long total = p.tail_q > 1 ? (long long)p.tail_start + (long long)p.tail_kb * p.tail_P
+                                       : (long long)p.num_m * p.num_n * p.batch * p.splits;
   const int units = sm_count() / CG;
   int used = (int)(total < units ? total : units);
   // Halo mode with a resident filter: every CTA must keep one feature block.
@@ -1731,10 +1863,7 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
     const TailPlan tp = plan_tail((long long)p.num_m * p.num_n * p.batch, p.num_kb, cg, bn);
     if (tp.q > 1) {
       TKB_CUDA(cudaMallocAsync(&tail_buf, tp.bytes, st));
-      p.tail_start = tp.start;
-      p.tail_q = tp.q;
-      p.tail_kb = tp.kb;
-      p.tail_part = static_cast<float*>(tail_buf);
+      apply_tail(p, tp, static_cast<float*>(tail_buf));
     }
   }
   dispatch<kPlain>(ma, mb, md, p, cg, tf32, st);
@@ -1888,7 +2017,8 @@ int choose_splits(long long units, int num_kb, long long pairs, int bm, int bn,
     return t;
   };
   int best = 1;
-  double best_t = cost(1);
+  // No split leaves the balanced tail (plan_tail) to even out the last wave.
+  double best_t = std::min(cost(1), plan_tail(units, num_kb, bm / kRows, bn).cost_us);
   for (int s = 2; s <= 16 && num_kb / s >= 4; ++s) {
     if ((size_t)s * out_bytes > cap) break;
     const double t = cost(s);
@@ -2149,12 +2279,7 @@ void launch_pointwise(const ConvGeom& g, const ConvPlan& c, const float* in, con
   p.part = part;
   p.part_stride = pix * g.K;
   p.alpha = 1.0f;
-  if (c.tail.q > 1) {
-    p.tail_start = c.tail.start;
-    p.tail_q = c.tail.q;
-    p.tail_kb = c.tail.kb;
-    p.tail_part = reinterpret_cast<float*>(reinterpret_cast<char*>(part) + c.part_bytes);
-  }
+  apply_tail(p, c.tail, reinterpret_cast<float*>(reinterpret_cast<char*>(part) + c.part_bytes));
   const CUtensorMap ma = map_rows(a, esize, g.C, pix, 1, 0, kRows);
   const CUtensorMap mb = map_rows(ft, esize, c.kp, g.K, 1, 0, c.bn / c.cg);
   cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)pix, (cuuint64_t)c.splits};
@@ -2222,12 +2347,7 @@ void launch_im2col_conv(const ConvGeom& g, const ConvPlan& c, const float* in, c
   p.pad_t = g.pad_t;
   p.pad_l = g.pad_l;
   p.cchunks = g.C / ek;
-  if (c.tail.q > 1) {
-    p.tail_start = c.tail.start;
-    p.tail_q = c.tail.q;
-    p.tail_kb = c.tail.kb;
-    p.tail_part = reinterpret_cast<float*>(reinterpret_cast<char*>(part) + c.part_bytes);
-  }
+  apply_tail(p, c.tail, reinterpret_cast<float*>(reinterpret_cast<char*>(part) + c.part_bytes));
   const CUtensorMap ma = map_nhwc_im2col(a, esize, g, kRows);
   const CUtensorMap mb = map_rows2d(ft, esize, c.kp, g.K, c.bn / c.cg);
   cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)pix, (cuuint64_t)c.splits};
@@ -2471,12 +2591,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     p.kb_per = plan.kb_per;
     p.part = part;
     p.part_stride = (long long)g.N * g.OH * g.OW * g.K;
-    if (plan.tail.q > 1) {
-      p.tail_start = plan.tail.start;
-      p.tail_q = plan.tail.q;
-      p.tail_kb = plan.tail.kb;
-      p.tail_part = reinterpret_cast<float*>(reinterpret_cast<char*>(part) + plan.part_bytes);
-    }
+    apply_tail(p, plan.tail, reinterpret_cast<float*>(reinterpret_cast<char*>(part) + plan.part_bytes));
     const CUtensorMap ma = map_rows2d(fa, esize, kp, g.K, kRows);
     const CUtensorMap mb =
         plan.imgs > 1 ? map_nhwc(xin, esize, g, bx.wb, bx.tileH, g.stride, plan.imgs / cg)

@@ -96,3 +96,27 @@ def test_im2col_mode_rejects_unboxable_channels(tk, oracle):
     opts = tk.exec_options("tf32", mode="im2col")
     with pytest.raises(tk.CapabilityError):
         tk.conv2d_workspace_size(s, tk.parse_conv_params("im2col"), options=opts)
+
+
+# Gather mode (channel counts that are not whole slabs: VGG conv1_1, the
+# ResNet stem): producer warps stage the input rows of each 128-pixel run in
+# shared memory and build the K-slabs from there.
+GATHER_SHAPES = [
+    # N, H, W, C, K, R, stride, same
+    (2, 224, 224, 3, 64, 3, 1, True),    # conv1_1 geometry (runs cross rows)
+    (2, 224, 224, 3, 64, 7, 2, True),    # ResNet stem
+    (3, 13, 13, 3, 16, 3, 1, True),      # a run spans ~10 rows and 3 images
+    (1, 129, 127, 5, 32, 3, 1, False),   # Valid, ragged rows
+    (2, 40, 33, 7, 48, 5, 2, True),      # stride 2, 5x5
+    (1, 1, 1, 3, 16, 3, 1, True),        # one pixel
+]
+
+
+@pytest.mark.parametrize("shape", GATHER_SHAPES)
+def test_gather_mode_matches_oracle(tk, oracle, shape):
+    N, H, W, C, K, R, stride, same = shape
+    conv, x, f, want = case(oracle, *shape, seed=41)
+    s = tk.ConvShape(N, H, W, C, K, R, R, stride, same)
+    got = run_mode(tk, x, f, s, "tf32", mode="gather")
+    assert not np.isnan(got).any()
+    assert oracle.max_scaled_error(got, want) <= TOL["tf32"]
