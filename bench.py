@@ -102,7 +102,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("BENCH_SMI_MS", "20")], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
             t0 = time.time()
@@ -301,7 +301,11 @@ def main():
     # value.  gpu_launches counts the kernels inside the graph.
     graph = None
     launches_per_step = None
-    join_each = os.environ.get("BENCH_JOIN_EACH", "0") == "1"  # A/B of the graph's join structure
+    # Per-layer device time inside the timed steps: timing event-record nodes
+    # in the step graph between consecutive layer launches on the main stream.
+    in_step_events = not args.no_graph and os.environ.get("BENCH_STEP_EVENTS", "0") == "1"
+    lay_ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(layers) + 1)]
+    in_step = np.zeros(len(layers))
     if not args.no_graph:
         cap = torch.cuda.Stream(device=dev)
         cap.wait_stream(stream)
@@ -312,31 +316,23 @@ def main():
             # Filter-side work (prepare: tensor-core filter repack) depends only
             # on the filters: fork it to a side stream so it overlaps earlier
             # layers; each layer's run joins on its own prepare.
-            # Two joins only: the first layer waits for its own prepare, the
-            # second for all of them (done long before the first layer ends);
-            # layers 2..13 then follow each other in plain stream order, so
-            # every launch keeps its programmatic (PDL) edge to the previous
-            # layer -- an event join per layer would turn each of those into a
-            # full dependency (~8 us per layer boundary measured).
             side.wait_stream(cap)
             ready = []
             with torch.cuda.stream(side):
-                for i, L in enumerate(layers):
+                for L in layers:
                     tk.conv2d_prepare_dev(L["f"], L["shape"], L["algo"], L["ws"], precision=prec,
                                           stream=side)
-                    if i == 0 or i == len(layers) - 1 or join_each:
-                        ev = torch.cuda.Event()
-                        ev.record(side)
-                        ready.append(ev)
-            for i, L in enumerate(layers):
-                if join_each:
-                    cap.wait_event(ready[i])
-                elif i == 0:
-                    cap.wait_event(ready[0])
-                elif i == 1:
-                    cap.wait_event(ready[-1])
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    ready.append(ev)
+            for i, (L, ev) in enumerate(zip(layers, ready)):
+                cap.wait_event(ev)
+                if in_step_events:
+                    lay_ev[i].record(cap)
                 tk.conv2d_run_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], L["ws"],
                                   precision=prec, stream=cap)
+            if in_step_events:
+                lay_ev[-1].record(cap)
             cap.wait_stream(side)
         launches_per_step = tk.launch_count() - l0
         for _ in range(2):
@@ -349,9 +345,48 @@ def main():
         else:
             step()
 
-    # Per-layer device times of the conv kernels (same stream, CUDA events),
-    # for the roofline.  With graphs: one graph replays R x [L2 flush, the
-    # layer's run phase] and a second R x [L2 flush]; the layer's kernel time
+    # Timed steps.
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = tk.launch_count()
+    times = []
+    extra_steps = 0
+    step_flush = os.environ.get("BENCH_STEP_FLUSH", "1") == "1"
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            if step_flush:
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run_step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            if in_step_events:
+                in_step += [lay_ev[i].elapsed_time(lay_ev[i + 1]) for i in range(len(layers))]
+        timed_samples = len(clocks.lines)
+        launches = tk.launch_count() - launches0
+        # A short timed region (small --steps) can end between two 20 ms
+        # samples: keep the same step running, untimed, until three samples
+        # under this load exist (reported as samples_after_timed).
+        t_end = time.time() + 2.0
+        while len(clocks.lines) < 3 and clocks.proc is not None and time.time() < t_end:
+            flush.zero_()
+            run_step()
+            torch.cuda.synchronize()
+            extra_steps += 1
+    if launches_per_step is not None:
+        launches = launches_per_step * args.steps
+    torch.cuda.synchronize()
+    total_ms = shard.max_over_ranks(float(sum(times)), device=dev)
+    ms_per_step = total_ms / args.steps
+    value = step_flops * world / (ms_per_step * 1e-3) / 1e9
+
+    # Per-layer device times of the conv kernels (after the timed steps; same
+    # stream, CUDA events),
+    # for the roofline.  With graphs: one graph replays R x [L2 eviction, the
+    # layer's run phase] and a second R x [L2 eviction]; the layer's kernel time
     # is their difference / R -- L2-cold like the step, without the graph
     # launch latency (~4-6 us) that an event pair around one replay adds.
     # The filter prepare (tiny, overlapped in the step) is not included.
@@ -372,6 +407,19 @@ def main():
             ts.append(ev[0].elapsed_time(ev[1]))
         return float(np.median(ts))
 
+    # The per-layer eviction reads the 256 MiB buffer (clean lines): a write
+    # flush would leave ~126 MB of dirty lines whose write-back then lands on
+    # the timed layer.
+    flush_sink = torch.empty((), device=dev)
+
+    evict_read = os.environ.get("BENCH_EVICT", "read") == "read"
+
+    def evict():
+        if evict_read:
+            torch.sum(flush, dim=0, out=flush_sink)
+        else:
+            flush.zero_()
+
     flush_ms = None
     if not args.no_graph:
         cap = torch.cuda.Stream(device=dev)
@@ -379,7 +427,7 @@ def main():
         fg = torch.cuda.CUDAGraph()
         with torch.cuda.graph(fg, stream=cap):
             for _ in range(reps):
-                flush.zero_()
+                evict()
         with torch.cuda.stream(stream):
             flush_ms = timed(fg.replay)
 
@@ -391,7 +439,7 @@ def main():
         lg = torch.cuda.CUDAGraph()
         with torch.cuda.graph(lg, stream=cap):
             for _ in range(reps):
-                flush.zero_()
+                evict()
                 run_on(cap)
         with torch.cuda.stream(stream):
             return max(timed(lg.replay) - flush_ms, 1e-6) / reps
@@ -405,41 +453,8 @@ def main():
             def one(L=L):
                 tk.conv2d_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"], precision=prec,
                               workspace=L["ws"], stream=stream)
-            per_layer.append(timed(one, pre=flush.zero_))
+            per_layer.append(timed(one, pre=evict))
 
-    # Timed steps.
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = tk.launch_count()
-    times = []
-    extra_steps = 0
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            run_step()
-            e1.record(stream)
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1))
-        timed_samples = len(clocks.lines)
-        launches = tk.launch_count() - launches0
-        # A short timed region (small --steps) can end between two 20 ms
-        # samples: keep the same step running, untimed, until three samples
-        # under this load exist (reported as samples_after_timed).
-        t_end = time.time() + 2.0
-        while len(clocks.lines) < 3 and clocks.proc is not None and time.time() < t_end:
-            flush.zero_()
-            run_step()
-            torch.cuda.synchronize()
-            extra_steps += 1
-    if launches_per_step is not None:
-        launches = launches_per_step * args.steps
-    torch.cuda.synchronize()
-    total_ms = shard.max_over_ranks(float(sum(times)), device=dev)
-    ms_per_step = total_ms / args.steps
-    value = step_flops * world / (ms_per_step * 1e-3) / 1e9
 
     # End-to-end through the host-buffer C ABI (pinned host memory).
     e2e = None
@@ -490,7 +505,10 @@ def main():
     peaks, peaks_kind = load_peaks()
     # Dominant kernel: the implicit-GEMM conv (tc_gemm_kernel) -- its share
     # is the whole step except the tiny filter-pack launches.
-    lay_ms = float(sum(per_layer))
+    # Per-layer times inside the timed steps (event nodes in the step graph,
+    # averaged over the K steps) when available, else the isolated kernels.
+    step_layer = list(in_step / max(1, args.steps)) if in_step_events else list(per_layer)
+    lay_ms = float(sum(step_layer))
     achieved_tf = step_flops / (lay_ms * 1e-3) / 1e12
     if prec == "bf16":
         peak_tf = peaks["bf16_tflops"]
@@ -524,8 +542,8 @@ def main():
                 "peak_source": peak_note}
 
     layer_rows = []
-    for L, ms in zip(layers, per_layer):
-        layer_rows.append({"layer": L["name"], "ms": round(ms, 4),
+    for L, ms, kms in zip(layers, step_layer, per_layer):
+        layer_rows.append({"layer": L["name"], "ms": round(ms, 4), "kernel_ms": round(kms, 4),
                            "tflops": round(L["flops"] / (ms * 1e-3) / 1e12, 2)})
 
     peaks, peaks_kind = load_peaks()
@@ -751,6 +769,9 @@ def main():
             "gpu_launches": int(launches),
             "clocks": dict(clocks.summary(), samples_in_timed=timed_samples,
                            samples_after_timed=len(clocks.lines) - timed_samples),
+            "step_ms": {"min": round(float(np.min(times)), 4),
+                        "median": round(float(np.median(times)), 4),
+                        "max": round(float(np.max(times)), 4)},
             "layers": layer_rows,
             "secondary": secondary,
         }

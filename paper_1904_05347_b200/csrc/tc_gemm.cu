@@ -2511,7 +2511,15 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     p.ek = ek;
     p.cchunks = g.C / ek;
     p.num_kb = p.cchunks;
-    p.BN = g.K <= 32 ? 32 : 64;
+    // Feature tile: 128 wide when the features come in 128s (N = 128 MMAs
+    // and half the units of N = 64: VGG conv2_1 105 -> 91 us, ResNet
+    // res3a/res4a_branch2b 27 -> 25 us, same-box A/B); two operand stages
+    // (halo 22.5 KiB + 9 filter taps x 8 KiB each) still fit.
+    p.BN = g.K <= 32 ? 32 : (g.K % 128 == 0 ? 128 : 64);
+    if (const char* e = getenv("TK_HALO_BN")) {  // experiment knob
+      const int b = atoi(e);
+      if ((b == 64 || b == 128) && g.K % b == 0) p.BN = b;
+    }
     p.Wb = p.TW;
     p.tileH = cg * p.TH;
     p.tiles_w = (g.OW + p.TW - 1) / p.TW;

@@ -13,9 +13,9 @@ out = []
 for f in re.split(r"\n\s*Function : ", txt)[1:]:
     name = f.split("\n", 1)[0].strip()
     c = collections.Counter()
-    for k in re.findall(r"\b(UTC\w*MMA\w*|UTMALDG\w*|UTMASTG\w*|UBLKCP\w*|LDTM\w*|STTM\w*|"
+    for k in re.findall(r"\b(UTC\w*MMA\w*|UTMALDG(?:\.\w+)*|UTMASTG\w*|UBLKCP\w*|LDTM\w*|STTM\w*|"
                         r"HMMA\w*|FFMA|FMUL|FADD|LDGSTS\w*|SYNCS\.\w+)", f):
-        c[k if k.startswith("SYNCS") else k.split(".")[0]] += 1
+        c[k if k.startswith("SYNCS") else (k if k.startswith("UTMALDG") else k.split(".")[0])] += 1
     out.append((name, c))
 dem = subprocess.run(["c++filt"], input="\n".join(n for n, _ in out), capture_output=True,
                      text=True).stdout.split("\n")
