@@ -1106,6 +1106,11 @@ __global__ void __launch_bounds__(256) tail_reduce_kernel(TcArgs p) {
 
 inline long long total_tiles_of(const TcArgs& p) { return (long long)p.num_m * p.num_n * p.batch; }
 
+// Sustained dense TF32 tensor-core rate per SM and clock the cost models use:
+// the measured 827 TF/s (1/2 of the bf16 burst in MEASURED_PEAKS.json) over
+// 148 SMs at 1.9 GHz (the nominal 1.1 PF would be 3782).
+constexpr double kTcFlopPerClk = 2941.0;
+
 struct TailPlan {
   int start = 0, q = 0, kb = 0, P = 0;  // q: max pieces per tile, kb: segments per pair
   long long W = 0;
@@ -1117,7 +1122,7 @@ struct TailPlan {
 // of choose_splits.
 inline double slab_time_us(int cg, int bn) {
   const int bm = kRows * cg;
-  const double mma_clk = 4.0 * (double)bm * bn * 8 / 3782.0;
+  const double mma_clk = 4.0 * (double)bm * bn * 8 / kTcFlopPerClk;
   const double feed_clk = (double)(bm / 2 + bn / 2) * 128 / 70.0;
   return std::max(mma_clk, feed_clk) / 1900.0;
 }
@@ -1146,7 +1151,7 @@ TailPlan plan_tail(long long tiles, int num_kb, int cg, int bn) {
   t.cost_us = base;
   if (off || tc_knobs().split == 1 || rem == 0 || num_kb < 4) return t;
   const long long W = rem * (long long)num_kb;
-  if (W < 2 * pairs) return t;  // every pair needs >= 2 slab-steps
+  if (W < pairs) return t;  // every pair needs a slab-step (no empty ranges)
   const double slab = slab_time_us(cg, bn);
   const double tile_bytes = (double)kRows * cg * bn * 4;
   const long long per = (W + pairs - 1) / pairs;
@@ -1156,7 +1161,7 @@ TailPlan plan_tail(long long tiles, int num_kb, int cg, int bn) {
   const double red_bytes = (double)(pairs + rem) * tile_bytes * 2 + (double)rem * tile_bytes;
   const double cost = (double)full * (num_kb * slab + 1.0) + per * slab + 1.0 * segs + 2.0 +
                       red_bytes / 4.0e6;
-  if (cost >= base * 0.9) return t;  // demand a clear win
+  if (cost >= base * 0.97) return t;  // demand a win beyond the model's noise
   t.start = (int)(tiles - rem);
   t.q = std::max(q, 2);
   t.kb = segs;
@@ -2006,7 +2011,7 @@ int choose_splits(long long units, int num_kb, long long pairs, int bm, int bn,
     while (sp > 1 && (size_t)sp * out_bytes > cap) --sp;
     return sp;
   }
-  const double mma_clk = 4.0 * (double)bm * bn * 8 / 3782.0;      // per slab, per pair
+  const double mma_clk = 4.0 * (double)bm * bn * 8 / kTcFlopPerClk;      // per slab, per pair
   const double feed_clk = (double)(bm / 2 + bn / 2) * 128 / 70.0;  // bytes per SM / (B/clk)
   const double slab_us = std::max(mma_clk, feed_clk) / 1900.0;
   auto cost = [&](int s) {
@@ -2043,10 +2048,13 @@ void finish_splits(ConvPlan& c, int num_kb, int splits, size_t out_bytes, long l
 }
 
 // Automatic choice of the im2col plan (see plan_conv_impl).
+// Measured (same-box A/B of every ResNet-50 / VGG-16 layer, tools/
+// layer_times.py --mode im2col): TF32 strided 1x1 layers gain from the
+// im2col traversal (ResNet res3a_branch1 33 -> 27, res4a_branch2a 19 -> 17,
+// res5a_branch2a 24 -> 20, res5a_branch1 33 -> 27 us); 3x3 layers are
+// faster through the tiled boxes.
 bool prefer_im2col(const ConvGeom& g, int precision) {
-  (void)g;
-  (void)precision;
-  return false;
+  return precision == TK_PREC_TF32 && g.R == 1 && g.S == 1 && g.stride == 2;
 }
 
 ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
@@ -2063,9 +2071,16 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
   // (Small planes waste too much of a pixel box: 7x7 -> 8x8 boxes.)
   const bool strided_box = g.stride > 1 && tf32 && conv_boxable(g, precision) &&
                            mode != TK_TC_POINTWISE && g.OH * g.OW >= 196;
+  // BF16 stride-1 1x1 layers on planes >= 14 x 14 with <= 512 features run
+  // faster as one-tap halo convolutions than as the plain GEMM (same-box
+  // A/B: ResNet res2b/res3b/res4b_branch2a 60/38/29 -> 45/28/24 us).
+  const bool auto_sel = mode == TK_TC_AUTO && !force;
+  const bool bf16_pw_halo = auto_sel && !tf32 && g.R == 1 && g.S == 1 && g.stride == 1 &&
+                            g.OH >= 14 && g.K <= 512 && g.K % 32 == 0 && conv_boxable(g, precision);
   const bool pointwise = g.R == 1 && g.S == 1 && g.pad_t == 0 && g.pad_l == 0 && g.C % 8 == 0 &&
                          g.K % 4 == 0 && !(force && std::string(force) != "plain") &&
-                         (mode == TK_TC_AUTO || mode == TK_TC_POINTWISE) && !strided_box;
+                         (mode == TK_TC_AUTO || mode == TK_TC_POINTWISE) && !strided_box &&
+                         !bf16_pw_halo;
   // Pixels-on-M GEMM sizing shared by the pointwise and im2col plans: SM
   // pair tiles of 256 pixels x bn features, split over K when the tiles
   // cannot fill the pairs, the last partial wave cut into K-pieces.
@@ -2139,10 +2154,19 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
                                 (long long)g.N * pb.tiles_w * pb.tiles_h;
         const long long pairs = sm_count() / pcg;
         const double eff = (double)units / (double)(((units + pairs - 1) / pairs) * pairs);
-        if (c.halo && eff >= 0.9) c.halo = false;
+        // (128-wide halo tiles, K % 128 == 0, beat full-wave pixN too: VGG
+        // conv2_2 185 -> 150 us)
+        if (c.halo && eff >= 0.9 && g.K % 128 != 0) c.halo = false;
         if (!c.halo && eff < 0.6) c.halo = true;
       }
     }
+    // BF16 on planes >= 28 x 28 with 128-multiple features: halo's one
+    // input box per channel chunk halves the operand traffic of the
+    // conversion-bound BF16 layers (VGG conv2_2 / conv3_1 / conv4_1 / conv4_2
+    // 157/70/71/111 -> 138/67/62/107 us), and the one-tap 1x1 case above.
+    if (auto_sel && !tf32 && halo_geom &&
+        ((g.K % 128 == 0 && g.OH >= 28 && g.C >= 64) || bf16_pw_halo))
+      c.halo = true;
     if (mode == TK_TC_HALO && halo_geom) c.halo = true;
     if (mode == TK_TC_PIXN || mode == TK_TC_PIXM) c.halo = false;
     c.num_kb = (int)(K / ek);

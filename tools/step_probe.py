@@ -41,18 +41,20 @@ def graph_of(body):
     return g
 
 
-def timeit(g, n=10, pre=lambda: flush.zero_()):
+def timeit(g, n=10, pre=lambda: flush.zero_(), spread=False):
     ts = []
     for _ in range(n + 2):
         pre()
-        torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         g.replay()
         b.record()
         b.synchronize()
         ts.append(a.elapsed_time(b))
-    return float(np.median(ts[2:]))
+    t = np.array(ts[2:])
+    if spread:
+        return f"min {t.min():.3f} med {np.median(t):.3f} mean {t.mean():.3f} max {t.max():.3f}"
+    return float(np.median(t))
 
 
 def runs(st):
@@ -76,6 +78,15 @@ def full(st):
     st.wait_stream(side)
 
 
+def prep_first(st):
+    for name, shape, x, f, y, ws in layers:
+        tk.conv2d_prepare_dev(f, shape, algo, ws, precision=prec, stream=st)
+    runs(st)
+
+
+for nm, body in (("full", full), ("prepares first", prep_first), ("runs only", runs)):
+    g = graph_of(body)
+    print(f"{nm:16s} x50: {timeit(g, n=50, spread=True)}", flush=True)
 print(f"full step            {timeit(graph_of(full)):8.3f} ms")
 print(f"runs only            {timeit(graph_of(runs)):8.3f} ms")
 print(f"runs only, read-evict{timeit(graph_of(runs), pre=lambda: torch.sum(flush, dim=0, out=sink)):8.3f} ms")
