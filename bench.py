@@ -83,6 +83,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch layer by layer")
+    ap.add_argument("--no-layers", action="store_true",
+                    help="skip the per-layer kernel timing (profiling runs: the step's launches "
+                         "are then the last ones after the L2 flush)")
     return ap.parse_args()
 
 
@@ -444,7 +447,7 @@ def main():
         with torch.cuda.stream(stream):
             return max(timed(lg.replay) - flush_ms, 1e-6) / reps
 
-    for L in layers:
+    for L in ([] if args.no_layers else layers):
         if not args.no_graph:
             per_layer.append(kernel_ms(
                 lambda st, L=L: tk.conv2d_run_dev(L["x"], L["f"], L["y"], L["shape"], L["algo"],
@@ -508,6 +511,9 @@ def main():
     # Per-layer times inside the timed steps (event nodes in the step graph,
     # averaged over the K steps) when available, else the isolated kernels.
     step_layer = list(in_step / max(1, args.steps)) if in_step_events else list(per_layer)
+    if not step_layer:  # --no-layers: the step itself
+        step_layer = [ms_per_step * L["flops"] / step_flops for L in layers]
+        per_layer = list(step_layer)
     lay_ms = float(sum(step_layer))
     achieved_tf = step_flops / (lay_ms * 1e-3) / 1e12
     if prec == "bf16":

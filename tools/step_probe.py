@@ -87,6 +87,11 @@ def prep_first(st):
 for nm, body in (("full", full), ("prepares first", prep_first), ("runs only", runs)):
     g = graph_of(body)
     print(f"{nm:16s} x50: {timeit(g, n=50, spread=True)}", flush=True)
+gf = graph_of(full)
+for nm, pre in (("write flush", lambda: flush.zero_()),
+                ("read evict", lambda: torch.sum(flush, dim=0, out=sink)),
+                ("no eviction", lambda: None)):
+    print(f"full, {nm:12s} x100: {timeit(gf, n=100, pre=pre, spread=True)}", flush=True)
 print(f"full step            {timeit(graph_of(full)):8.3f} ms")
 print(f"runs only            {timeit(graph_of(runs)):8.3f} ms")
 print(f"runs only, read-evict{timeit(graph_of(runs), pre=lambda: torch.sum(flush, dim=0, out=sink)):8.3f} ms")
