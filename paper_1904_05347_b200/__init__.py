@@ -21,7 +21,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtilekit_b200.so")
+LIB_PATH = os.environ.get("TK_LIB_PATH") or os.path.join(HERE, "libtilekit_b200.so")  # (TK_LIB_PATH: A/B builds)
 
 # ---------------------------------------------------------------------------
 # Errors: one class per reference exception (errors.hpp:9-59)
