@@ -129,6 +129,10 @@ struct TcArgs {
   // L2-aware raster (plain / pixN): tiles are visited in groups of `raster`
   // M-blocks, N-blocks within a group, so a wave of CTAs shares A and B tiles.
   int raster;
+  // Plain TF32 GEMM with A MN-major (TcGemm::a_mn): A stages are 4 boxes of
+  // 32 M x 32 K (box {32, 32, 4} of the view {32, K, M/32}), 4 KiB apart,
+  // 128B_ATOM_32B-swizzled (ptx::desc_sw128_mn).
+  int a_mn;
   // Balanced tail (plain / pixN, splits == 1; stream-K over the last partial
   // wave): the tail_W = (tiles - tail_start) x num_kb slab-steps of the
   // tiles >= tail_start are dealt to the tail_P SM pairs as equal contiguous
@@ -664,7 +668,8 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
             dx = tap / p.S - p.pad_t;
           }
           if constexpr (MODE == kPlain) {
-            ptx::tma3<CG>(sa, &map_a, fb, k0, m_blk * BM + rank * kRows, z);
+            if (p.a_mn) ptx::tma3<CG>(sa, &map_a, fb, 0, k0, (m_blk * BM + rank * kRows) / 32);
+            else ptx::tma3<CG>(sa, &map_a, fb, k0, m_blk * BM + rank * kRows, z);
             ptx::tma3<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows, z);
           } else if constexpr (MODE == kConvIm2col) {
             // 128 consecutive output pixels (across rows and images) from
@@ -702,8 +707,10 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader CTA) ----------------
     if (leader) {
-      const uint32_t idesc = ptx::idesc(BM, p.BN, TF32);
+      const bool a_mn = MODE == kPlain && p.a_mn;
+      const uint32_t idesc = ptx::idesc(BM, p.BN, TF32) | (a_mn ? (1u << 15) : 0u);
       const uint64_t kdesc = ptx::desc_sw128(0);
+      const uint64_t kdesc_mn = ptx::desc_sw128_mn(0, 4096, 512);
       int stage = 0;
       uint32_t phase = 0;
       int nlocal = 0;
@@ -725,11 +732,12 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           if (local == kTraceUnit && kb == u.kb0 && lane == 0) trace_mark(p, 11);
           if (ptx::elect_one()) {
             const uint32_t sa = ptx::smem(base + stage * stage_bytes);
-            const uint64_t ad = kdesc + (sa >> 4);
+            const uint64_t ad = (a_mn ? kdesc_mn : kdesc) + (sa >> 4);
             const uint64_t bd = kdesc + ((sa + (uint32_t)a_bytes) >> 4);
+            const uint64_t a_step = a_mn ? 64 : 2;  // K = 8: one 1 KiB atom / 32 bytes
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              ptx::mma_cg<CG, TF32>(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc,
+              ptx::mma_cg<CG, TF32>(d_tmem, ad + a_step * kk, bd + 2 * kk, idesc,
                                     (kb != u.kb0 || kk != 0));
             ptx::commit_cg<CG>(&empty[stage]);
             if (kb == u.kb1 - 1) ptx::commit_cg<CG>(&tmem_full[acc]);
@@ -927,7 +935,8 @@ EncodeTiledFn encode_fn() {
 // esize: 4 (fp32 / tf32) or 2 (bf16).  dims[0] is the contiguous K axis.
 CUtensorMap make_map(const void* base, int esize, int rank, const cuuint64_t* dims,
                      const cuuint64_t* strides, const cuuint32_t* box,
-                     const cuuint32_t* traversal = nullptr) {
+                     const cuuint32_t* traversal = nullptr,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   cuuint32_t elem_strides[5] = {1, 1, 1, 1, 1};
   if (traversal)
@@ -935,7 +944,7 @@ CUtensorMap make_map(const void* base, int esize, int rank, const cuuint64_t* di
   const CUresult r = encode_fn()(
       &m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
       (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, elem_strides,
-      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
@@ -1859,7 +1868,19 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
   p.alpha = g.alpha;
   p.beta = g.beta;
   p.read_c = g.c != nullptr && g.beta != 0.0f;
-  const CUtensorMap ma = map_rows(g.a, esize, g.K, g.M, g.batch, g.a_batch, kRows);
+  CUtensorMap ma;
+  if (g.a_mn) {
+    if (!tf32 || g.batch != 1 || g.M % 32 != 0 || (g.lda * 4) % 16 != 0)
+      fail(TK_ERR_CAPABILITY, "tc_gemm: MN-major A needs TF32, batch 1, M % 32 == 0");
+    // view {32 (M inner), K (stride lda), M / 32 (stride 128 B)}, box {32, 32, 4}
+    cuuint64_t dims[3] = {32, (cuuint64_t)g.K, (cuuint64_t)(g.M / 32)};
+    cuuint64_t strides[2] = {(cuuint64_t)g.lda * 4, 128};
+    cuuint32_t box[3] = {32, 32, (cuuint32_t)(kRows / 32)};
+    ma = make_map(g.a, 4, 3, dims, strides, box, nullptr, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    p.a_mn = 1;
+  } else {
+    ma = map_rows(g.a, esize, g.K, g.M, g.batch, g.a_batch, kRows);
+  }
   const CUtensorMap mb = map_rows(g.b, esize, g.K, g.N, g.batch, g.b_batch, bn / cg);
   // Row-major output (d_sn == 1): stage through smem and TMA-store it.
   CUtensorMap md = ma;
@@ -1930,16 +1951,23 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool a_ok = tf32 && ta && kp == (long long)k && aligned(a);
   const bool b_ok = tf32 && !tb && kp == (long long)k && aligned(b);
+  // Column-major, untransposed A is MN-major: the tensor core reads it in
+  // place (no transpose pass) when M is a multiple of 32.
+  static const bool mn_on = [] {
+    const char* e = getenv("TK_A_MN");
+    return !(e && e[0] == '0');
+  }();
+  const bool a_mn = mn_on && tf32 && !ta && m % 32 == 0 && aligned(a) && m <= (1ull << 31);
   const size_t esz = tf32 ? 4 : 2;
   void* pa = nullptr;
   void* pb = nullptr;
-  if (!a_ok) TKB_CUDA(cudaMallocAsync(&pa, (size_t)m * kp * esz, st));
+  if (!a_ok && !a_mn) TKB_CUDA(cudaMallocAsync(&pa, (size_t)m * kp * esz, st));
   if (!b_ok) TKB_CUDA(cudaMallocAsync(&pb, (size_t)n * kp * esz, st));
   auto pack = [&](const float* src, long long rs, long long ks, long long rows, void* dst) {
     if (tf32) pack_kmajor<float>(src, rs, ks, rows, (long long)k, kp, (float*)dst, false, st);
     else pack_kmajor<__nv_bfloat16>(src, rs, ks, rows, (long long)k, kp, (__nv_bfloat16*)dst, false, st);
   };
-  if (!a_ok) {
+  if (!a_ok && !a_mn) {
     if (ta) pack(a, (long long)k, 1, (long long)m, pa);
     else pack(a, 1, (long long)m, (long long)m, pa);
   }
@@ -1951,7 +1979,9 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
   g.M = (int)m;
   g.N = (int)n;
   g.K = (int)kp;
-  g.a = a_ok ? a : (const float*)pa;
+  g.a = (a_ok || a_mn) ? a : (const float*)pa;
+  g.a_mn = a_mn;
+  g.lda = (long long)m;
   g.b = b_ok ? b : (const float*)pb;
   g.d = d;
   g.c = c;

@@ -25,6 +25,10 @@ struct TcGemm {
   float alpha = 1.0f, beta = 0.0f;
   int precision = 1;
   int tile_n = 0;  // 0 = auto
+  // TF32, batch 1: A given MN-major instead -- column-major [K][lda] with M
+  // contiguous (M % 32 == 0), read by the tensor core as is (no transpose).
+  bool a_mn = false;
+  long long lda = 0;
 };
 
 void launch_tc_gemm(const TcGemm& g, cudaStream_t st);

@@ -187,6 +187,22 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// MN-major tf32 operand: the only layout UMMA takes for it is
+// SWIZZLE_128B_BASE32B (layout type 1; TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+// 32-byte chunks permuted within 128-byte rows over 4-row periods): 32 tf32 of
+// M per 128-byte row, K rows 128 B apart in 4-row atoms `sbo` bytes apart,
+// M blocks of 32 `lbo` bytes apart.  One K = 8 MMA reads two atoms.
+__device__ __forceinline__ uint64_t desc_sw128_mn(uint32_t smem_addr, uint32_t lbo,
+                                                  uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;
+  return d;
+}
+
 // Instruction descriptor: fp32 accumulate, K-major A and B, M x N.
 // a/b format: kind::tf32 -> 2 (TF32); kind::f16 -> 1 (BF16).
 __host__ __device__ constexpr uint32_t idesc(int m, int n, bool tf32) {

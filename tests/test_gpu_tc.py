@@ -29,7 +29,12 @@ def dev_conv(tk, x, f, shape, algo, precision="tf32"):
 @pytest.mark.parametrize("prec", ["tf32", "bf16"])
 @pytest.mark.parametrize("m,n,k,ta,tb", [(128, 128, 32, 1, 0), (256, 512, 128, 1, 0),
                                          (1024, 1024, 1024, 0, 0), (33, 29, 21, 0, 1),
-                                         (300, 200, 100, 1, 1), (1000, 70, 64, 0, 0)])
+                                         (300, 200, 100, 1, 1), (1000, 70, 64, 0, 0),
+                                         # untransposed A with M % 32 == 0: read MN-major in
+                                         # place by the TF32 path (K tails, thin N, tall M)
+                                         (256, 256, 256, 0, 0), (512, 96, 100, 0, 1),
+                                         (4096, 128, 64, 0, 0), (64, 1000, 2048, 0, 0),
+                                         (96, 32, 7, 0, 0)])
 def test_tc_gemm_colmajor(tk, oracle, m, n, k, ta, tb, prec):
     import torch
     a = oracle.fill_random(m * k, 1)
