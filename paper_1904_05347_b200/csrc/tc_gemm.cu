@@ -2090,12 +2090,25 @@ void finish_splits(ConvPlan& c, int num_kb, int splits, size_t out_bytes, long l
 
 // Automatic choice of the im2col plan (see plan_conv_impl).
 // Measured (same-box A/B of every ResNet-50 / VGG-16 layer, tools/
-// layer_times.py --mode im2col): TF32 strided 1x1 layers gain from the
-// im2col traversal (ResNet res3a_branch1 33 -> 27, res4a_branch2a 19 -> 17,
-// res5a_branch2a 24 -> 20, res5a_branch1 33 -> 27 us); 3x3 layers are
-// faster through the tiled boxes.
+// layer_times.py --mode im2col, confirmed by the tuner's DB
+// profiles/r01_tune_*_knobs.ndjson):
+//  * TF32 strided 1x1 layers gain from the im2col traversal (ResNet
+//    res3a_branch1 33 -> 27, res4a_branch2a 19 -> 17, res5a_branch2a 24 ->
+//    20, res5a_branch1 33 -> 27 us);
+//  * 3x3 layers with >= 128 channels, >= 256 features on planes >= 28 x 28,
+//    both precisions, once the two-half epilogue staging left the 256 x 256
+//    tiles six operand stages (VGG conv4_1 99 -> 86, conv4_2 170 -> 151,
+//    conv3_1 95 -> 90 us TF32; BF16 conv3_2/conv4_2 119/107 -> 112/97 us);
+//    smaller planes and feature counts stay on halo / pixel boxes;
+//  * BF16 stride-1 1x1 layers that expand the features (K >= 2C) or run on
+//    7 x 7 planes (res2a_branch2c 40 -> 36, res5b_branch2a 29 -> 25 us).
 bool prefer_im2col(const ConvGeom& g, int precision) {
-  return precision == TK_PREC_TF32 && g.R == 1 && g.S == 1 && g.stride == 2;
+  const bool tf32 = precision == TK_PREC_TF32;
+  if (tf32 && g.R == 1 && g.S == 1 && g.stride == 2) return true;
+  if (g.R == 3 && g.S == 3 && g.stride == 1 && g.C >= 128 && g.K >= 256 && g.OH >= 28)
+    return true;
+  if (!tf32 && g.R == 1 && g.S == 1 && g.stride == 1 && (g.K >= 2 * g.C || g.OH <= 7)) return true;
+  return false;
 }
 
 ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
