@@ -699,6 +699,45 @@ def main():
                                  "frac_of_peak": round(fl / (kms * 1e-3) / 1e12 / pk, 3)})
                 secondary[f"resnet50_{p_}"]["layers"] = rows
         del rn
+        # BASELINE configs[1]'s algorithm comparison: every distinct VGG16
+        # layer at batch 32 through each conv algorithm of the selector
+        # (direct / tiled / im2col are one exact-FP32 kernel -- the same
+        # ascending (x, y, c) sum -- so "tiled" stands for them; im2col and
+        # Winograd F(2x2) / F(4x4) on the tensor cores in TF32, Winograd F(2x2)
+        # also exact FP32).  Whole conv2d_dev calls (filter transform
+        # included, as the reference's conv2d does) from a graph, L2-cold,
+        # launch latency removed as for the layers.  GFLOP/s count the
+        # direct-equivalent conv_flops for every algorithm (tuner.hpp:442).
+        if not args.no_graph:
+            algos = [("tiled_fp32", "tiled_t4x5_v4x2", "fp32"), ("im2col_tf32", "im2col", "tf32"),
+                     ("winograd_t2x2_tf32", "winograd_t2x2", "tf32"),
+                     ("winograd_t4x4_tf32", "winograd_t4x4", "tf32"),
+                     ("winograd_t2x2_fp32", "winograd_t2x2", "fp32")]
+            table = {}
+            for name, h, c, k, _mult in VGG16:
+                shp = tk.ConvShape(N, h, h, c, k, 3, 3, 1, True)
+                x = torch.rand((N, h, h, c), device=dev, generator=gen) * 2 - 1
+                f = torch.rand((3, 3, c, k), device=dev, generator=gen) * 2 - 1
+                y = torch.empty(shp.out_shape, device=dev)
+                row = {}
+                for key, algo_name, p_ in algos:
+                    algo = tk.parse_conv_params(algo_name)
+                    try:
+                        wsz = tk.conv2d_workspace_size(shp, algo, p_)
+                    except tk.TilekitError:
+                        continue
+                    ws = torch.empty(max(wsz, 4) // 4 + 1, device=dev)
+                    run = (lambda st, algo=algo, p_=p_, ws=ws: tk.conv2d_dev(
+                        x, f, y, shp, algo, precision=p_, workspace=ws, stream=st))
+                    run(stream)  # warm (allocator, descriptors)
+                    torch.cuda.synchronize()
+                    ms = kernel_ms(run)
+                    row[key] = {"ms": round(ms, 4),
+                                "gflops": round(shp.flops() / (ms * 1e-3) / 1e9, 1)}
+                    del ws
+                table[name] = row
+                del x, f, y
+            secondary["vgg16_algorithms_b32"] = table
         # BASELINE configs[3]: large square GEMMs on the tensor cores
         # (column-major nn through tk_gemm_dev; operands in HBM, > L2 from 4096).
         for n in (2048, 4096, 8192):
