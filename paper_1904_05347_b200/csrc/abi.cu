@@ -453,20 +453,22 @@ void winograd_dev(const ConvGeom& g, int m, int precision, const float* in, cons
     p.tx_on_m = 0;
     launch_exact(p, exact_auto((long long)w.tiles * spots, w.K), false, spots, st);
   } else {
-    // P[tile][k] = sum_c Ut[k][c] * V[tile][c]: features on the MMA M side
-    // so the epilogue stores coalesce along k.
+    // P[tile][k] = sum_c V[tile][c] * Ut[k][c]: tiles on the MMA M side,
+    // features on N, so P's rows (k contiguous) leave through the TMA-store
+    // epilogue (features on M stored column by column from registers: the
+    // F(4x4) batched GEMM of VGG conv4_2 ran 109 us that way).
     TcGemm t{};
-    t.M = w.K;
-    t.N = w.tiles;
+    t.M = w.tiles;
+    t.N = w.K;
     t.K = w.C;
     t.batch = spots;
-    t.a = u;
-    t.a_batch = (long long)w.C * w.K;
-    t.b = v;
-    t.b_batch = (long long)w.tiles * w.C;
+    t.a = v;
+    t.a_batch = (long long)w.tiles * w.C;
+    t.b = u;
+    t.b_batch = (long long)w.C * w.K;
     t.d = prod;
-    t.d_sm = 1;
-    t.d_sn = w.K;
+    t.d_sm = w.K;
+    t.d_sn = 1;
     t.d_batch = (long long)w.tiles * w.K;
     // The transform-domain operands are fp32 scratch: the batched GEMM runs
     // kind::tf32 for every tensor-core precision request.

@@ -123,15 +123,18 @@ __global__ void __launch_bounds__(256) wino_input_kernel(WinoGeom g, const float
 }
 
 // Stage 2 (winograd.hpp:239-259): one thread per (channel, feature).
-// k_major = 0 writes U[s][c][k]; 1 writes Ut[s][k][c].
+// k_major = 0 writes U[s][c][k]; 1 writes Ut[s][k][c].  The index order
+// follows the written layout (feature fastest for U, channel fastest for
+// Ut): the T^2 = 16 / 36 stores per thread coalesce, the 9 filter reads are
+// the strided side.
 template <class Plan>
 __global__ void __launch_bounds__(256) wino_filter_kernel(WinoGeom g, const float* __restrict__ filt,
                                                           float* __restrict__ u, int k_major) {
   constexpr int T = Plan::T;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)g.C * g.K) return;
-  const int k = (int)(idx % g.K);
-  const int c = (int)(idx / g.K);
+  const int k = k_major ? (int)(idx / g.C) : (int)(idx % g.K);
+  const int c = k_major ? (int)(idx % g.C) : (int)(idx / g.K);
   float w[9];
 #pragma unroll
   for (int x = 0; x < 3; ++x)
