@@ -120,3 +120,27 @@ def test_gather_mode_matches_oracle(tk, oracle, shape):
     got = run_mode(tk, x, f, s, "tf32", mode="gather")
     assert not np.isnan(got).any()
     assert oracle.max_scaled_error(got, want) <= TOL["tf32"]
+
+
+# Automatic operand-path rules (plan_conv): each shape lands on a different
+# path in BF16 / TF32; all must agree with the oracle.
+AUTO_SHAPES = [
+    # N, H, W, C, K, R, stride, same       path (bf16 / tf32)
+    (2, 16, 16, 64, 128, 1, 1, True),      # im2col (K >= 2C) / pointwise
+    (2, 16, 16, 128, 128, 1, 1, True),     # one-tap halo / pointwise
+    (4, 7, 7, 256, 128, 1, 1, True),       # im2col (7 x 7) / pointwise
+    (2, 28, 28, 128, 256, 3, 1, True),     # im2col (wide 3x3, plane >= 28) / im2col
+    (2, 28, 28, 64, 128, 3, 1, True),      # halo (128-wide tiles)
+    (2, 30, 30, 256, 128, 1, 2, True),     # strided 1x1: compacting GEMM / im2col
+]
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("shape", AUTO_SHAPES)
+def test_auto_paths_match_oracle(tk, oracle, shape, prec):
+    N, H, W, C, K, R, stride, same = shape
+    conv, x, f, want = case(oracle, *shape, seed=51)
+    s = tk.ConvShape(N, H, W, C, K, R, R, stride, same)
+    got = run_mode(tk, x, f, s, prec, mode="auto")
+    assert not np.isnan(got).any()
+    assert oracle.max_scaled_error(got, want) <= TOL[prec]

@@ -23,6 +23,7 @@ ap.add_argument("--only", default="")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--mode", default="auto", help="tensor-core operand path (tk.TC_MODES)")
 ap.add_argument("--split", type=int, default=0)
+ap.add_argument("--algo", default="im2col", help="conv algorithm (parse_conv_params grammar)")
 ap.add_argument("--flush", default="read", choices=["read", "write"],
                 help="evict L2 by reading (clean lines) or writing (dirty lines whose "
                      "write-back then lands on the timed kernel) a 256 MiB buffer")
@@ -37,7 +38,7 @@ peaks, _ = bench.load_peaks()
 peak = peaks["bf16_tflops"] / (2.0 if a.prec == "tf32" else 1.0)
 flush = torch.ones(64 << 20, device="cuda")
 flush_sink = torch.empty((), device="cuda")
-p = tk.parse_conv_params("im2col")
+p = tk.parse_conv_params(a.algo)
 st = torch.cuda.Stream()
 print(f"{'layer':18s} {'us':>8s} {'TF/s':>8s} {'%peak':>6s}  ({a.prec}, batch {a.batch}, peak {peak:.0f})")
 for name, r, s, h, c, k in rows:
