@@ -1048,6 +1048,36 @@ int sm_count() {
   return n;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TK_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Launch of a helper kernel (reductions, conversions) as a programmatic
+// dependent of the previous kernel in the stream: its CTAs may be scheduled
+// while that kernel drains (they block in griddep_wait before touching
+// memory), and they release their own dependents at once, so the next
+// tensor-core kernel's prologue overlaps them too.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  TKB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  note_launch();
+}
+
 // Sum the tail pieces of each tail tile in piece order into the output.
 // Block = (tail tile r, CTA rank, 8 columns); thread = one column x 4 rows
 // (float4 along the column-major partial).  pixN: row = output feature,
@@ -1055,6 +1085,8 @@ int sm_count() {
 // stores); plain: row = M index, column = N index.
 template <int MODE, int CG>
 __global__ void __launch_bounds__(256) tail_reduce_kernel(TcArgs p) {
+  ptx::griddep_wait();
+  ptx::griddep_launch_dependents();
   const int col_blocks = (p.BN + 7) / 8;
   const int r = blockIdx.x / (CG * col_blocks);
   const int rem = blockIdx.x - r * CG * col_blocks;
@@ -1311,9 +1343,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     if (p.tail_q > 1) {
       const long long rem = total_tiles_of(p) - p.tail_start;
       const long long blocks = rem * CG * ((p.BN + 7) / 8);
-      tail_reduce_kernel<MODE, CG><<<(unsigned)blocks, 256, 0, st>>>(p);
-      note_launch();
-      TKB_CUDA(cudaGetLastError());
+      launch_pdl(tail_reduce_kernel<MODE, CG>, (unsigned)blocks, 256, st, p);
     }
   }
   if (trace) {
@@ -1669,6 +1699,8 @@ void pack_filter(const float* filt, int K, int Kout, int kp, T* dst, bool tf32_r
 __global__ void __launch_bounds__(256) to_bf16_kernel(const float4* __restrict__ src,
                                                       __nv_bfloat162* __restrict__ dst,
                                                       long long n4) {
+  ptx::griddep_wait();
+  ptx::griddep_launch_dependents();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     const float4 v = src[i];
@@ -1681,10 +1713,8 @@ void to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st)
   if (n % 4 != 0) fail(TK_ERR_CAPABILITY, "bf16 conversion needs a multiple of 4 elements");
   const long long n4 = n / 4;
   const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)sm_count() * 8);
-  to_bf16_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(src),
-                                         reinterpret_cast<__nv_bfloat162*>(dst), n4);
-  note_launch();
-  TKB_CUDA(cudaGetLastError());
+  launch_pdl(to_bf16_kernel, (unsigned)blocks, 256, st, reinterpret_cast<const float4*>(src),
+             reinterpret_cast<__nv_bfloat162*>(dst), n4);
 }
 
 // out[i] = sum_s part[s*stride + i] in split order (deterministic), 4
@@ -1693,6 +1723,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __rest
                                                             long long stride4, int splits,
                                                             float4* __restrict__ out, long long n4) {
   constexpr int kMaxSplits = 16;
+  ptx::griddep_wait();
+  ptx::griddep_launch_dependents();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     float4 v[kMaxSplits];  // every split's load in flight before the ordered sum
@@ -1716,10 +1748,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __rest
 void splitk_reduce(const float* part, long long n, int splits, float* out, cudaStream_t st) {
   const long long n4 = n / 4;
   const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)sm_count() * 8);
-  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(part), n4, splits,
-                                               reinterpret_cast<float4*>(out), n4);
-  note_launch();
-  TKB_CUDA(cudaGetLastError());
+  launch_pdl(splitk_reduce_kernel, (unsigned)blocks, 256, st, reinterpret_cast<const float4*>(part),
+             n4, splits, reinterpret_cast<float4*>(out), n4);
 }
 
 // Pointwise (1x1) conv operand: the input pixels the strided window visits,
