@@ -429,10 +429,53 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
 
+# Operand checks before any pointer crosses the C ABI (the reference raises
+# ShapeError from check_gemm_operands / check_conv_operands, gemm.hpp:165-186,
+# conv.hpp:30-66): an undersized buffer must never be read past its end.
+def _need_size(arr, count: int, what: str) -> None:
+    n = int(arr.size) if isinstance(arr, np.ndarray) else int(arr.numel())
+    if n != count:
+        raise ShapeError(f"{what} has {n} elements, expected {count}")
+
+
+def _gemm_sizes(shape: "GemmShape"):
+    return shape.m * shape.k, shape.k * shape.n, shape.m * shape.n
+
+
+def _need_shape(arr, want, what: str) -> None:
+    got = tuple(arr.shape)
+    if got != tuple(want):
+        if int(np.prod(got)) == int(np.prod(want)) and len(got) == 1:
+            return  # flat buffer of the right size
+        raise ShapeError(f"conv2d: {what} is {'x'.join(map(str, got))}, expected "
+                         f"{'x'.join(map(str, want))}")
+
+
+def _need_dev(t, what: str, count: Optional[int] = None, dtype_f32: bool = True) -> None:
+    """Device operand: a contiguous CUDA tensor (float32 unless a workspace)
+    holding exactly `count` elements (at least, for workspaces: count=None)."""
+    if t is None:
+        return
+    if not getattr(t, "is_cuda", False):
+        raise ContractError(f"{what} must be a CUDA tensor")
+    if dtype_f32:
+        import torch
+        if t.dtype != torch.float32:
+            raise ContractError(f"{what} must be float32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ContractError(f"{what} must be contiguous")
+    if count is not None and t.numel() != count:
+        raise ShapeError(f"{what} has {t.numel()} elements, expected {count}")
+
+
 def gemm_tiled(a, b, c, shape: GemmShape, cfg: GemmConfig, dev: DeviceSpec) -> np.ndarray:
     """gemm_tiled (gemm.hpp:308): flat column-major operands, returns m*n."""
     a, b = _f32(a).ravel(), _f32(b).ravel()
     c = _f32(c).ravel() if c is not None else np.zeros(shape.m * shape.n, np.float32)
+    na, nb, nc = _gemm_sizes(shape)
+    _need_size(a, na, "gemm: operand A")
+    _need_size(b, nb, "gemm: operand B")
+    _need_size(c, nc, "gemm: operand C")
     out = np.empty(shape.m * shape.n, np.float32)
     _check(lib().tk_gemm_tiled(C.byref(shape.c()), C.byref(cfg.c()), C.byref(dev.c()),
                                _ptr(a), _ptr(b), _ptr(c), _ptr(out)))
@@ -442,6 +485,10 @@ def gemm_tiled(a, b, c, shape: GemmShape, cfg: GemmConfig, dev: DeviceSpec) -> n
 def gemm_naive(a, b, c, shape: GemmShape) -> np.ndarray:
     a, b = _f32(a).ravel(), _f32(b).ravel()
     c = _f32(c).ravel() if c is not None else np.zeros(shape.m * shape.n, np.float32)
+    na, nb, nc = _gemm_sizes(shape)
+    _need_size(a, na, "gemm: operand A")
+    _need_size(b, nb, "gemm: operand B")
+    _need_size(c, nc, "gemm: operand C")
     out = np.empty(shape.m * shape.n, np.float32)
     _check(lib().tk_gemm_naive(C.byref(shape.c()), _ptr(a), _ptr(b), _ptr(c), _ptr(out)))
     return out
@@ -450,6 +497,8 @@ def gemm_naive(a, b, c, shape: GemmShape) -> np.ndarray:
 def gemm_batched_strided(a, b, batch, m, n, k):
     """C_g = A_g B_g over packed column-major members; returns (c, multiplies)."""
     a, b = _f32(a).ravel(), _f32(b).ravel()
+    _need_size(a, batch * m * k, "gemm_batched_strided: operand A")
+    _need_size(b, batch * k * n, "gemm_batched_strided: operand B")
     c = np.zeros(batch * m * n, np.float32)
     cnt = C.c_uint64(0)
     _check(lib().tk_gemm_batched_strided(_ptr(a), m * k, _ptr(b), k * n, _ptr(c), m * n,
@@ -460,6 +509,8 @@ def gemm_batched_strided(a, b, batch, m, n, k):
 def conv2d(inp, filt, shape: ConvShape, params: ConvAlgoParams, precision="fp32") -> np.ndarray:
     """conv2d selector (winograd.hpp:304); precision != fp32 uses tensor cores."""
     inp, filt = _f32(inp), _f32(filt)
+    _need_shape(inp, shape.in_shape, "input")
+    _need_shape(filt, shape.filt_shape, "filter")
     out = np.empty(shape.out_shape, np.float32)
     if precision == "fp32":
         rc = lib().tk_conv2d(C.byref(shape.c()), C.byref(params.c()), _ptr(inp), _ptr(filt),
@@ -474,6 +525,8 @@ def conv2d(inp, filt, shape: ConvShape, params: ConvAlgoParams, precision="fp32"
 
 def conv2d_im2col(inp, filt, shape: ConvShape, cfg: GemmConfig, dev: DeviceSpec) -> np.ndarray:
     inp, filt = _f32(inp), _f32(filt)
+    _need_shape(inp, shape.in_shape, "input")
+    _need_shape(filt, shape.filt_shape, "filter")
     out = np.empty(shape.out_shape, np.float32)
     _check(lib().tk_conv2d_im2col(C.byref(shape.c()), C.byref(cfg.c()), C.byref(dev.c()),
                                   _ptr(inp), _ptr(filt), _ptr(out)))
@@ -482,6 +535,8 @@ def conv2d_im2col(inp, filt, shape: ConvShape, cfg: GemmConfig, dev: DeviceSpec)
 
 def conv2d_winograd(inp, filt, shape: ConvShape, params: ConvAlgoParams):
     inp, filt = _f32(inp), _f32(filt)
+    _need_shape(inp, shape.in_shape, "input")
+    _need_shape(filt, shape.filt_shape, "filter")
     out = np.empty(shape.out_shape, np.float32)
     mults, tiles = C.c_uint64(0), C.c_size_t(0)
     _check(lib().tk_conv2d_winograd(C.byref(shape.c()), C.byref(params.c()), _ptr(inp),
@@ -491,6 +546,7 @@ def conv2d_winograd(inp, filt, shape: ConvShape, params: ConvAlgoParams):
 
 def im2col(inp, shape: ConvShape) -> np.ndarray:
     inp = _f32(inp)
+    _need_shape(inp, shape.in_shape, "input")
     rows = shape.batch * shape.out_rows * shape.out_cols
     cols = shape.window_rows * shape.window_cols * shape.channels
     out = np.empty(rows * cols, np.float32)
@@ -521,10 +577,18 @@ def _stream(stream) -> C.c_void_p:
     return C.c_void_p(s.cuda_stream)
 
 
+def _need_conv_dev(shape: ConvShape, inp, filt, out, workspace) -> None:
+    _need_dev(inp, "conv2d: input", int(np.prod(shape.in_shape)))
+    _need_dev(filt, "conv2d: filter", int(np.prod(shape.filt_shape)))
+    _need_dev(out, "conv2d: output", int(np.prod(shape.out_shape)))
+    _need_dev(workspace, "conv2d: workspace", None, dtype_f32=False)
+
+
 def conv2d_dev(inp, filt, out, shape: ConvShape, params: ConvAlgoParams, precision="fp32",
                workspace=None, stream=None, tile_n=0, options=None) -> None:
     """options: an exec_options(...) record (tensor-core knobs); overrides
     precision / tile_n when given."""
+    _need_conv_dev(shape, inp, filt, out, workspace)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     opts = options if options is not None else exec_options(precision, tile_n)
     _check(lib().tk_conv2d_dev(C.byref(shape.c()), C.byref(params.c()),
@@ -535,6 +599,7 @@ def conv2d_dev(inp, filt, out, shape: ConvShape, params: ConvAlgoParams, precisi
 def conv2d_prepare_dev(filt, shape: ConvShape, params: ConvAlgoParams, workspace,
                        precision="fp32", stream=None, options=None) -> None:
     """Filter-side phase of conv2d_dev (may run on its own stream)."""
+    _need_conv_dev(shape, None, filt, None, workspace)
     ws_bytes = workspace.numel() * workspace.element_size()
     opts = options if options is not None else exec_options(precision)
     _check(lib().tk_conv2d_prepare_dev(C.byref(shape.c()), C.byref(params.c()),
@@ -545,6 +610,7 @@ def conv2d_prepare_dev(filt, shape: ConvShape, params: ConvAlgoParams, workspace
 def conv2d_run_dev(inp, filt, out, shape: ConvShape, params: ConvAlgoParams, workspace,
                    precision="fp32", stream=None, options=None) -> None:
     """Input-side phase of conv2d_dev; ordered after conv2d_prepare_dev."""
+    _need_conv_dev(shape, inp, filt, out, workspace)
     ws_bytes = workspace.numel() * workspace.element_size()
     opts = options if options is not None else exec_options(precision)
     _check(lib().tk_conv2d_run_dev(C.byref(shape.c()), C.byref(params.c()),
@@ -563,10 +629,21 @@ def conv2d_workspace_size(shape: ConvShape, params: ConvAlgoParams, precision="f
 
 def gemm_dev(a, b, c, out, shape: GemmShape, cfg: Optional[GemmConfig] = None,
              precision="fp32", stream=None, tile_n=0) -> None:
+    na, nb, nc = _gemm_sizes(shape)
+    _need_dev(a, "gemm: operand A", na)
+    _need_dev(b, "gemm: operand B", nb)
+    if shape.beta != 0.0:
+        if c is None:
+            raise ContractError("gemm: beta != 0 needs operand C")
+        _need_dev(c, "gemm: operand C", nc)
+    _need_dev(out, "gemm: output", nc)
     cfg_c = C.byref(cfg.c()) if cfg is not None else None
     _check(lib().tk_gemm_dev(C.byref(shape.c()), cfg_c, C.byref(exec_options(precision, tile_n)),
                              _dptr(a), _dptr(b), _dptr(c), _dptr(out), _stream(stream)))
 
 
 def im2col_dev(inp, out, shape: ConvShape, stream=None) -> None:
+    _need_dev(inp, "conv2d: input", int(np.prod(shape.in_shape)))
+    _need_dev(out, "im2col: patches", shape.batch * shape.out_rows * shape.out_cols *
+              shape.window_rows * shape.window_cols * shape.channels)
     _check(lib().tk_im2col_dev(C.byref(shape.c()), _dptr(inp), _dptr(out), _stream(stream)))

@@ -587,22 +587,31 @@ void conv_host(const tilekit::ConvShape& s, const tk_conv_params* p, int precisi
   {
     DevBuf din(4 * in_elems(g), st), dfl(4 * filt_elems(g), st), dout(4 * out_elems(g), st);
     DevBuf ws(conv_workspace(cg, p, precision), st);
-    h2d(dfl.p, filt, 4 * filt_elems(g), st);
-    conv_dev(cs, p, precision, nullptr, dfl.f(), nullptr, ws.p, st, kConvPrepare);
-    TKB_CUDA(cudaEventRecord(hp.ready, st));  // allocations exist from here on
-    TKB_CUDA(cudaStreamWaitEvent(hp.copy_in, hp.ready, 0));
-    for (int i = 0; i < chunks; ++i) {
-      h2d(din.f() + i * in_chunk, in + i * in_chunk, 4 * in_chunk, hp.copy_in);
-      TKB_CUDA(cudaEventRecord(hp.in_done[i], hp.copy_in));
-      TKB_CUDA(cudaStreamWaitEvent(st, hp.in_done[i], 0));
-      conv_dev(cs, p, precision, din.f() + i * in_chunk, dfl.f(), dout.f() + i * out_chunk, ws.p,
-               st, kConvRun);
-      TKB_CUDA(cudaEventRecord(hp.run_done[i], st));
-      TKB_CUDA(cudaStreamWaitEvent(hp.copy_out, hp.run_done[i], 0));
-      d2h(out + i * out_chunk, dout.f() + i * out_chunk, 4 * out_chunk, hp.copy_out);
+    try {
+      h2d(dfl.p, filt, 4 * filt_elems(g), st);
+      conv_dev(cs, p, precision, nullptr, dfl.f(), nullptr, ws.p, st, kConvPrepare);
+      TKB_CUDA(cudaEventRecord(hp.ready, st));  // allocations exist from here on
+      TKB_CUDA(cudaStreamWaitEvent(hp.copy_in, hp.ready, 0));
+      for (int i = 0; i < chunks; ++i) {
+        h2d(din.f() + i * in_chunk, in + i * in_chunk, 4 * in_chunk, hp.copy_in);
+        TKB_CUDA(cudaEventRecord(hp.in_done[i], hp.copy_in));
+        TKB_CUDA(cudaStreamWaitEvent(st, hp.in_done[i], 0));
+        conv_dev(cs, p, precision, din.f() + i * in_chunk, dfl.f(), dout.f() + i * out_chunk,
+                 ws.p, st, kConvRun);
+        TKB_CUDA(cudaEventRecord(hp.run_done[i], st));
+        TKB_CUDA(cudaStreamWaitEvent(hp.copy_out, hp.run_done[i], 0));
+        d2h(out + i * out_chunk, dout.f() + i * out_chunk, 4 * out_chunk, hp.copy_out);
+      }
+      TKB_CUDA(cudaEventRecord(hp.out_done, hp.copy_out));
+      TKB_CUDA(cudaStreamWaitEvent(st, hp.out_done, 0));  // frees are ordered after the copies
+    } catch (...) {
+      // No queued copy may touch the caller's host buffers (or the device
+      // buffers freed below) after the error is reported.
+      cudaStreamSynchronize(hp.copy_in);
+      cudaStreamSynchronize(st);
+      cudaStreamSynchronize(hp.copy_out);
+      throw;
     }
-    TKB_CUDA(cudaEventRecord(hp.out_done, hp.copy_out));
-    TKB_CUDA(cudaStreamWaitEvent(st, hp.out_done, 0));  // frees are ordered after the copies
   }
   finish(st);
 }
@@ -793,6 +802,8 @@ int tk_gemm_batched_strided(const float* a, size_t sa, const float* b, size_t sb
   return guarded([&] {
     if (multiplies) *multiplies = (uint64_t)batch * m * n * k;
     if (batch == 0 || m == 0 || n == 0) return;
+    if (m > 2147483647ull || n > 2147483647ull || k > 2147483647ull || batch > 65535ull)
+      fail(TK_ERR_CAPABILITY, "gemm_batched_strided: dimensions exceed the 32-bit index range");
     cudaStream_t st = host_stream();
     // Span of each operand: the last batch member's end.
     const size_t ea = (batch - 1) * sa + m * k, eb = (batch - 1) * sb + k * n,
@@ -837,6 +848,9 @@ int tk_gemm_batched_strided_dev(const float* d_a, size_t sa, const float* d_b, s
     require_gpu();
     if (precision_of(opts) != TK_PREC_FP32_EXACT)
       fail(TK_ERR_CAPABILITY, "gemm_batched_strided: column-major batched GEMM is FP32-exact only");
+    if (batch == 0 || m == 0 || n == 0) return;  // nothing to write (reference: 0 multiplies)
+    if (m > 2147483647ull || n > 2147483647ull || k > 2147483647ull || batch > 65535ull)
+      fail(TK_ERR_CAPABILITY, "gemm_batched_strided: dimensions exceed the 32-bit index range");
     ExactArgs p{};
     p.M = (int)m;
     p.N = (int)n;

@@ -57,6 +57,7 @@ constexpr int kThreads = 192;
 constexpr int kAccCols = 256;  // TMEM: 2 x 256 fp32 columns allocated
 constexpr int kMaxAcc = 8;     // accumulator slots when BN <= 64 (512 / 64)
 constexpr int kMaxStages = 8;
+constexpr int kMaxSplits = 16;  // split-K partials summed by splitk_reduce
 
 enum TcMode : int {
   kPlain = 0,
@@ -1722,12 +1723,11 @@ void to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st)
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __restrict__ part,
                                                             long long stride4, int splits,
                                                             float4* __restrict__ out, long long n4) {
-  constexpr int kMaxSplits = 16;
   ptx::griddep_wait();
   ptx::griddep_launch_dependents();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
-    float4 v[kMaxSplits];  // every split's load in flight before the ordered sum
+    float4 v[kMaxSplits];  // every split's load in flight before the ordered sum (host: splits <= kMaxSplits)
 #pragma unroll
     for (int s = 0; s < kMaxSplits; ++s)
       if (s < splits) v[s] = __ldcs(part + s * stride4 + i);
@@ -1746,6 +1746,9 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __rest
 }
 
 void splitk_reduce(const float* part, long long n, int splits, float* out, cudaStream_t st) {
+  if (splits < 1 || splits > kMaxSplits)
+    fail(TK_ERR_CAPABILITY, "split-K: " + std::to_string(splits) + " splits (at most " +
+                                std::to_string(kMaxSplits) + ")");
   const long long n4 = n / 4;
   const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)sm_count() * 8);
   launch_pdl(splitk_reduce_kernel, (unsigned)blocks, 256, st, reinterpret_cast<const float4*>(part),
@@ -1903,7 +1906,8 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
     if (!tf32 || g.batch != 1 || g.M % 32 != 0 || (g.lda * 4) % 16 != 0)
       fail(TK_ERR_CAPABILITY, "tc_gemm: MN-major A needs TF32, batch 1, M % 32 == 0");
     // view {32 (M inner), K (stride lda), M / 32 (stride 128 B)}, box {32, 32, 4}
-    cuuint64_t dims[3] = {32, (cuuint64_t)g.K, (cuuint64_t)(g.M / 32)};
+    const long long ak = g.a_k > 0 ? std::min<long long>(g.a_k, g.K) : g.K;
+    cuuint64_t dims[3] = {32, (cuuint64_t)ak, (cuuint64_t)(g.M / 32)};
     cuuint64_t strides[2] = {(cuuint64_t)g.lda * 4, 128};
     cuuint32_t box[3] = {32, 32, (cuuint32_t)(kRows / 32)};
     ma = make_map(g.a, 4, 3, dims, strides, box, nullptr, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
@@ -2012,6 +2016,7 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
   g.a = (a_ok || a_mn) ? a : (const float*)pa;
   g.a_mn = a_mn;
   g.lda = (long long)m;
+  g.a_k = (long long)k;  // A holds k columns; the padded K tail reads as zeros
   g.b = b_ok ? b : (const float*)pb;
   g.d = d;
   g.c = c;
@@ -2078,7 +2083,8 @@ int choose_splits(long long units, int num_kb, long long pairs, int bm, int bn,
   const int forced = tc_knobs().split;
   if (forced == 1) return 1;
   if (forced > 1) {
-    int sp = std::min(forced, std::max(1, num_kb / 2));
+    // splitk_reduce sums at most kMaxSplits partials.
+    int sp = std::min(std::min(forced, kMaxSplits), std::max(1, num_kb / 2));
     while (sp > 1 && (size_t)sp * out_bytes > cap) --sp;
     return sp;
   }

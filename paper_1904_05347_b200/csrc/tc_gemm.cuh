@@ -29,6 +29,9 @@ struct TcGemm {
   // contiguous (M % 32 == 0), read by the tensor core as is (no transpose).
   bool a_mn = false;
   long long lda = 0;
+  // MN-major A: its true K extent (K may be padded for B); the TMA zero-fills
+  // past it instead of reading beyond the end of A.  0 = K.
+  long long a_k = 0;
 };
 
 void launch_tc_gemm(const TcGemm& g, cudaStream_t st);

@@ -98,3 +98,36 @@ def test_b200_device_spec(tk):
     assert d.compute_units in (148, 132, 160) or d.compute_units > 0
     ok, _ = tk.validate_config(tk.parse_gemm_config("8x8_16x16_loc_db"), d)
     assert ok
+
+
+def test_undersized_operands_raise_shape_error(tk):
+    """the Python wrappers check buffer sizes before any pointer
+    reaches the C ABI (reference check_gemm_operands / check_conv_operands,
+    gemm.hpp:165-186, conv.hpp:30-66)."""
+    g = tk.GemmShape(8, 8, 8)
+    cfg = tk.parse_gemm_config("4x4_8x8_noloc")
+    dev = tk.find_device("mali")
+    z, small = np.zeros(64, np.float32), np.zeros(63, np.float32)
+    with pytest.raises(tk.ShapeError, match="operand A"):
+        tk.gemm_tiled(small, z, z, g, cfg, dev)
+    with pytest.raises(tk.ShapeError, match="operand B"):
+        tk.gemm_naive(z, small, z, g)
+    with pytest.raises(tk.ShapeError, match="operand C"):
+        tk.gemm_naive(z, z, small, g)
+    with pytest.raises(tk.ShapeError, match="operand A"):
+        tk.gemm_batched_strided(small, z, 1, 8, 8, 8)
+    s = tk.ConvShape(1, 8, 8, 4, 2, 3, 3)
+    x = np.zeros(s.in_shape, np.float32)
+    w = np.zeros(s.filt_shape, np.float32)
+    with pytest.raises(tk.ShapeError, match="input"):
+        tk.conv2d(x[:, :7], w, s, tk.parse_conv_params("naive"))
+    with pytest.raises(tk.ShapeError, match="filter"):
+        tk.conv2d(x, w[..., :1], s, tk.parse_conv_params("im2col"))
+    with pytest.raises(tk.ShapeError, match="input"):
+        tk.im2col(x[:, :, :7], s)
+    import torch
+    with pytest.raises(tk.ContractError, match="CUDA tensor"):
+        tk.conv2d_dev(torch.zeros(s.in_shape), torch.zeros(s.filt_shape),
+                      torch.zeros(s.out_shape), s, tk.parse_conv_params("im2col"))
+    with pytest.raises(tk.ContractError, match="CUDA tensor"):
+        tk.gemm_dev(torch.zeros(64), torch.zeros(64), None, torch.zeros(64), g)

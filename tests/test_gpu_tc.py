@@ -232,3 +232,24 @@ def test_3xtf32_winograd_is_a_capability_error(tk, oracle):
     f = np.zeros(s.filt_shape, np.float32)
     with pytest.raises(tk.CapabilityError):
         dev_conv(tk, x, f, s, "winograd_t2x2", precision="3xtf32")
+
+
+@pytest.mark.parametrize("m,n,k", [(96, 32, 7), (256, 64, 30), (128, 128, 1)])
+def test_tc_gemm_mn_major_a_never_reads_past_a(tk, oracle, m, n, k):
+    """an untransposed A with k % 4 != 0 is read MN-major in
+    place; its TMA K extent must be the true k, so the padded K tail is
+    zero-filled rather than read from whatever follows A (NaN here)."""
+    import torch
+    a = oracle.fill_random(m * k, 1)
+    b = oracle.fill_random(k * n, 2)
+    want = oracle.gemm_naive(m, n, k, 1.0, 0.0, 0, 0, a, b, np.zeros(m * n, np.float32))
+    big = torch.full((m * k + 64 * 1024,), float("nan"), device="cuda")
+    big[:m * k] = torch.from_numpy(a).cuda()
+    da = big[:m * k]
+    db = torch.from_numpy(b).cuda()
+    out = torch.full((m * n,), float("nan"), device="cuda")
+    tk.gemm_dev(da, db, None, out, tk.GemmShape(m, n, k), precision="tf32")
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert not np.isnan(got).any()
+    assert oracle.max_scaled_error(got, want) <= TOL_TF32
