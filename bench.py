@@ -67,6 +67,24 @@ def load_peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
+def plan_str(tk, shape, algo, prec):
+    """Compact tk_conv2d_plan_info: kernel/effective precision, CTA group,
+    tile, split-K and stream-K tail (e.g. "tc_im2col/tf32 cg2 256x256")."""
+    d = tk.conv2d_plan_info(shape, algo, prec)
+    s = f"{d['kernel']}/{d['precision']} cg{d['cta_group']} {d['tile_m']}x{d['tile_n']}"
+    if d["splits"] > 1:
+        s += f" split{d['splits']}"
+    if d["tail_pieces"]:
+        s += f" tail{d['tail_pieces']}"
+    if d["imgs"] > 1:
+        s += f" imgs{d['imgs']}"
+    if d["flat"]:
+        s += " flat"
+    if d["precision"] != d["requested_precision"]:
+        s += f" (requested {d['requested_precision']})"
+    return s
+
+
 def conv_flops(n, h, c, k):
     return 2 * n * h * h * k * 9 * c
 
@@ -550,7 +568,8 @@ def main():
     layer_rows = []
     for L, ms, kms in zip(layers, step_layer, per_layer):
         layer_rows.append({"layer": L["name"], "ms": round(ms, 4), "kernel_ms": round(kms, 4),
-                           "tflops": round(L["flops"] / (ms * 1e-3) / 1e12, 2)})
+                           "tflops": round(L["flops"] / (ms * 1e-3) / 1e12, 2),
+                           "plan": plan_str(tk, L["shape"], L["algo"], prec)})
 
     peaks, peaks_kind = load_peaks()
     # Secondary lines (same run, same resident inputs): the other precisions
@@ -696,7 +715,8 @@ def main():
                         x, f, y, shp, im2col, ws0, precision=p_, stream=st))
                     rows.append({"layer": name, "ms": round(kms, 4),
                                  "tflops": round(fl / (kms * 1e-3) / 1e12, 1),
-                                 "frac_of_peak": round(fl / (kms * 1e-3) / 1e12 / pk, 3)})
+                                 "frac_of_peak": round(fl / (kms * 1e-3) / 1e12 / pk, 3),
+                                 "plan": plan_str(tk, shp, im2col, p_)})
                 secondary[f"resnet50_{p_}"]["layers"] = rows
         del rn
         # BASELINE configs[1]'s algorithm comparison: every distinct VGG16

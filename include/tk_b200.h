@@ -133,6 +133,40 @@ enum tk_tc_mode {
   TK_TC_IM2COL = 6     /* pixels on M gathered by im2col-mode TMA          */
 };
 
+/* Kernel family a convolution call runs (tk_conv_plan_info.kernel); the
+ * tensor-core values equal the tk_tc_mode of the operand path. */
+enum tk_kernel_kind {
+  TK_KERNEL_EXACT = 0,        /* FP32 SIMT implicit GEMM, bit-exact          */
+  TK_KERNEL_TC_HALO = 1,
+  TK_KERNEL_TC_PIXN = 2,
+  TK_KERNEL_TC_PIXM = 3,
+  TK_KERNEL_TC_GATHER = 4,
+  TK_KERNEL_TC_POINTWISE = 5,
+  TK_KERNEL_TC_IM2COL = 6,
+  TK_KERNEL_WINOGRAD = 7      /* transforms + batched transform-domain GEMM */
+};
+
+/* The plan of one convolution call (tk_conv2d_plan_info): what
+ * tk_conv2d_dev / tk_conv2d_run_dev will launch for this shape, algorithm
+ * and options.  `precision` is the arithmetic the contraction actually runs
+ * in -- it differs from the request when a path has no kernel for it (the
+ * gather producers and the Winograd batched GEMM compute BF16 requests in
+ * TF32). */
+typedef struct tk_conv_plan_info {
+  int kernel;              /* enum tk_kernel_kind                            */
+  int precision;           /* effective enum tk_precision                    */
+  int requested_precision; /* tk_exec_options.precision of the call          */
+  int cta_group;           /* SMs per tensor-core tile (1 or 2); 1 for SIMT  */
+  int tile_m, tile_n;      /* MMA tile (TC) or CTA output tile (SIMT)        */
+  int splits;              /* split-K partial sums (1 = none)                */
+  int tail_pieces;         /* stream-K tail: max pieces per tile (0 = none)  */
+  int imgs, flat;          /* pixN: whole images per tile / flat-row tiles   */
+  int box_w, box_h;        /* pixel box of the box / halo modes              */
+  int halo_resident;       /* halo: filter slice resident in shared memory   */
+  int winograd_m;          /* 2 or 4 for TK_KERNEL_WINOGRAD, else 0          */
+  int reserved[4];
+} tk_conv_plan_info;
+
 /* ---- library --------------------------------------------------------- */
 TK_API const char* tk_last_error(void);
 TK_API int tk_abi_version(void);
@@ -234,6 +268,10 @@ TK_API int tk_conv2d_run_dev(const tk_conv_shape* shape, const tk_conv_params* p
                              const tk_exec_options* opts, const float* d_in, const float* d_filt,
                              float* d_out, void* d_workspace, size_t workspace_bytes,
                              void* stream);
+/* The plan tk_conv2d_dev would run (host-side only: no GPU work, usable
+ * without a GPU for the shape/option logic). */
+TK_API int tk_conv2d_plan_info(const tk_conv_shape* shape, const tk_conv_params* params,
+                               const tk_exec_options* opts, tk_conv_plan_info* out);
 TK_API int tk_im2col_dev(const tk_conv_shape* shape, const float* d_in,
                   float* d_patches, void* stream);
 

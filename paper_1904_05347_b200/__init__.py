@@ -110,6 +110,18 @@ class ExecOptionsC(C.Structure):
                 ("reserved", C.c_int * 2)]
 
 
+class ConvPlanInfoC(C.Structure):
+    _fields_ = [(n, C.c_int) for n in (
+        "kernel", "precision", "requested_precision", "cta_group", "tile_m", "tile_n", "splits",
+        "tail_pieces", "imgs", "flat", "box_w", "box_h", "halo_resident", "winograd_m")] + \
+        [("reserved", C.c_int * 4)]
+
+
+KERNELS = {0: "exact_simt", 1: "tc_halo", 2: "tc_pixn", 3: "tc_pixm", 4: "tc_gather",
+           5: "tc_pointwise", 6: "tc_im2col", 7: "winograd"}
+PRECISION_NAMES = {v: k for k, v in PRECISIONS.items()}
+
+
 # Every symbol the header declares (checked by the CPU tests).
 EXPORTS = [
     "tk_last_error", "tk_abi_version", "tk_device_count", "tk_b200_device_spec",
@@ -119,7 +131,7 @@ EXPORTS = [
     "tk_conv2d_im2col", "tk_conv2d_winograd", "tk_im2col", "tk_filter_matrix",
     "tk_conv2d_dev", "tk_conv2d_workspace_size", "tk_conv2d_ex", "tk_im2col_dev",
     "tk_bench_gemm", "tk_bench_conv2d", "tk_gemm_ex", "tk_conv2d_prepare_dev",
-    "tk_conv2d_run_dev",
+    "tk_conv2d_run_dev", "tk_conv2d_plan_info",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -176,6 +188,8 @@ def lib() -> C.CDLL:
                                   C.POINTER(ExecOptionsC), _vp, _vp, C.c_size_t, _vp],
         "tk_conv2d_run_dev": [C.POINTER(ConvShapeC), C.POINTER(ConvParamsC),
                               C.POINTER(ExecOptionsC), _vp, _vp, _vp, _vp, C.c_size_t, _vp],
+        "tk_conv2d_plan_info": [C.POINTER(ConvShapeC), C.POINTER(ConvParamsC),
+                                C.POINTER(ExecOptionsC), C.POINTER(ConvPlanInfoC)],
         "tk_gemm_ex": [C.POINTER(GemmShapeC), C.POINTER(ExecOptionsC), _vp, _vp, _vp, _vp],
         "tk_bench_gemm": [C.POINTER(GemmShapeC), C.POINTER(GemmConfigC), C.POINTER(ExecOptionsC),
                           _vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(C.c_int64)],
@@ -625,6 +639,22 @@ def conv2d_workspace_size(shape: ConvShape, params: ConvAlgoParams, precision="f
     _check(lib().tk_conv2d_workspace_size(C.byref(shape.c()), C.byref(params.c()),
                                           C.byref(opts), C.byref(n)))
     return int(n.value)
+
+
+def conv2d_plan_info(shape: ConvShape, params: ConvAlgoParams, precision="fp32",
+                     options=None) -> dict:
+    """The plan conv2d_dev runs for this call (tk_conv2d_plan_info): kernel
+    family, EFFECTIVE precision (a BF16 request on a path without BF16
+    operands reports tf32), tile and work split.  Host-side only."""
+    info = ConvPlanInfoC()
+    opts = options if options is not None else exec_options(precision)
+    _check(lib().tk_conv2d_plan_info(C.byref(shape.c()), C.byref(params.c()), C.byref(opts),
+                                     C.byref(info)))
+    d = {f: getattr(info, f) for f, _ in ConvPlanInfoC._fields_ if f != "reserved"}
+    d["kernel"] = KERNELS[d["kernel"]]
+    d["precision"] = PRECISION_NAMES[d["precision"]]
+    d["requested_precision"] = PRECISION_NAMES[d["requested_precision"]]
+    return d
 
 
 def gemm_dev(a, b, c, out, shape: GemmShape, cfg: Optional[GemmConfig] = None,

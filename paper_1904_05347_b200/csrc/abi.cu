@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "exact_gemm.cuh"
+#include "experiments.cuh"
 #include "layout.cuh"
 #include "tc_gemm.cuh"
 #include "tilekit/gemm.hpp"
@@ -261,9 +262,14 @@ ExactLaunch exact_auto(long long M, long long N) {
     L.r = 8;  // 64 x 128
     if (tiles(64, 128) < 2 * 148) L.w = 4;  // 64 x 64
   }
-  if (const char* e = std::getenv("TK_EXACT_STAGES")) L.stages = std::atoi(e);
-  if (const char* e = std::getenv("TK_EXACT_TILE"))
-    std::sscanf(e, "%d,%d,%d,%d", &L.h, &L.w, &L.r, &L.c);
+  const Experiments& xp = experiments();
+  if (xp.exact_stages > 0) L.stages = xp.exact_stages;
+  if (xp.exact_tile[0] > 0) {
+    L.h = xp.exact_tile[0];
+    L.w = xp.exact_tile[1];
+    L.r = xp.exact_tile[2];
+    L.c = xp.exact_tile[3];
+  }
   return L;
 }
 
@@ -1058,6 +1064,77 @@ int tk_conv2d_run_dev(const tk_conv_shape* shape, const tk_conv_params* params,
                       float* d_out, void* d_ws, size_t ws_bytes, void* stream) {
   return conv_phase_dev(shape, params, opts, d_in, d_filt, d_out, d_ws, ws_bytes, stream,
                         kConvRun);
+}
+
+int tk_conv2d_plan_info(const tk_conv_shape* shape, const tk_conv_params* params,
+                        const tk_exec_options* opts, tk_conv_plan_info* out) {
+  return guarded([&] {
+    KnobScope knobs(opts);
+    if (!params || !out) fail(TK_ERR_CONTRACT, "conv2d_plan_info: NULL argument");
+    const tilekit::ConvShape s = conv_shape(shape);
+    const ConvGeom g = conv_geom(s);
+    const int prec = precision_of(opts);
+    tk_conv_plan_info r{};
+    r.requested_precision = prec;
+    r.cta_group = 1;
+    r.splits = 1;
+    r.imgs = 1;
+    auto exact = [&](const ExactLaunch& L) {
+      r.kernel = TK_KERNEL_EXACT;
+      r.precision = TK_PREC_FP32_EXACT;
+      r.tile_m = L.h * L.r;
+      r.tile_n = L.w * L.c;
+    };
+    switch (params->algo) {
+      case 0:
+      case 2:
+        if (prec == TK_PREC_FP32_EXACT) {
+          exact(exact_conv_default(g));
+          break;
+        }
+        if (params->algo == 0)
+          fail(TK_ERR_CAPABILITY, "conv2d: algorithm \"naive\" is FP32-exact only; use im2col or "
+                                  "winograd for tensor cores");
+        {
+          const TcConvInfo t = tc_conv_info(g, prec);
+          r.kernel = t.mode;
+          r.precision = t.precision;
+          r.cta_group = t.cta_group;
+          r.tile_m = t.tile_m;
+          r.tile_n = t.tile_n;
+          r.splits = t.splits;
+          r.tail_pieces = t.tail_pieces;
+          r.imgs = t.imgs;
+          r.flat = t.flat;
+          r.box_w = t.box_w;
+          r.box_h = t.box_h;
+          r.halo_resident = t.halo_resident;
+        }
+        break;
+      case 1:
+        check_tiled_params(s, params);
+        if (prec != TK_PREC_FP32_EXACT)
+          fail(TK_ERR_CAPABILITY, "conv2d: algorithm \"tiled\" is FP32-exact only; use im2col or "
+                                  "winograd for tensor cores");
+        exact(tiled_launch(params));
+        break;
+      case 3: {
+        const int m = check_winograd(s, params);
+        if (prec == TK_PREC_3XTF32)
+          fail(TK_ERR_CAPABILITY, "conv2d_winograd: 3xTF32 is provided on the im2col path only");
+        r.kernel = TK_KERNEL_WINOGRAD;
+        r.winograd_m = m;
+        const bool tc = prec != TK_PREC_FP32_EXACT && g.C % 4 == 0;
+        // The transform-domain operands are fp32 scratch: kind::tf32 for
+        // every tensor-core request.
+        r.precision = tc ? TK_PREC_TF32 : TK_PREC_FP32_EXACT;
+        break;
+      }
+      default:
+        fail(TK_ERR_CONTRACT, "conv2d: unknown algorithm");
+    }
+    *out = r;
+  });
 }
 
 int tk_bench_gemm(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const tk_exec_options* opts,

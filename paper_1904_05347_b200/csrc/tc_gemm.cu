@@ -39,6 +39,7 @@
 #include <cstdio>
 
 #include "common.cuh"
+#include "experiments.cuh"
 #include "tc_gemm.cuh"
 #include "tc_ptx.cuh"
 
@@ -1049,13 +1050,7 @@ int sm_count() {
   return n;
 }
 
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("TK_PDL");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+bool pdl_enabled() { return experiments().pdl; }
 
 // Launch of a helper kernel (reductions, conversions) as a programmatic
 // dependent of the previous kernel in the stream: its CTAs may be scheduled
@@ -1183,10 +1178,7 @@ inline double waves_cost_us(long long tiles, int num_kb, int cg, int bn) {
 // at ~4 TB/s + launch) says it pays.
 TailPlan plan_tail(long long tiles, int num_kb, int cg, int bn) {
   TailPlan t;
-  static const bool off = [] {
-    const char* e = getenv("TK_TAIL");
-    return e && e[0] == '0';
-  }();
+  const bool off = !experiments().tail;
   const long long pairs = sm_count() / cg;
   const long long rem = tiles % pairs, full = tiles / pairs;
   const double base = waves_cost_us(tiles, num_kb, cg, bn);
@@ -1236,16 +1228,11 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   // Tuning experiments: TK_TC_STAGES caps the ring, TK_TC_EPI=1 forces one
   // staging buffer.
   if (tc_knobs().stages > 0) stages_req = tc_knobs().stages;
-  if (const char* e = getenv("TK_TC_STAGES")) stages_req = atoi(e);
-  if (const char* e = getenv("TK_TC_EPI")) p.epi_bufs = std::min(p.epi_bufs, atoi(e));
-  {
-    // Chunk-ring staging (32 KiB) for tiles wider than one chunk.
-    static const bool ring_on = [] {
-      const char* e = getenv("TK_EPI_RING");
-      return !(e && e[0] == '0');
-    }();
-    p.epi_ring = (p.store_tma && ring_on && p.BN > 32) ? 1 : 0;
-  }
+  const Experiments& xp = experiments();
+  if (xp.tc_stages > 0) stages_req = xp.tc_stages;
+  if (xp.tc_epi > 0) p.epi_bufs = std::min(p.epi_bufs, xp.tc_epi);
+  // Chunk-ring staging (32 KiB) for tiles wider than one chunk.
+  p.epi_ring = (p.store_tma && xp.epi_ring && p.BN > 32) ? 1 : 0;
   // Double-buffered TMA-store staging when it leaves room for >= 3 stages.
   if (p.store_tma && p.epi_bufs > 1 &&
       232448 - 2048 - ktab_bytes0 - 2 * ((p.BN + 31) / 32) * kRows * kSlabBytes < 3 * stage_bytes)
@@ -1262,7 +1249,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     const int want = std::min(kMaxStages, std::max(3, kb_unit + 1));
     int bs = (room - want * stage_bytes) / (2 * kChunkBytes);
     bs = std::max(1, std::min(nchunks, bs));
-    if (const char* e = getenv("TK_EPI_RING_N")) bs = std::max(1, std::min(nchunks, atoi(e)));
+    if (xp.epi_ring_n > 0) bs = std::max(1, std::min(nchunks, xp.epi_ring_n));
     p.epi_ring = bs;
   }
   const int epi_bytes = !p.store_tma ? 0
@@ -1281,10 +1268,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   TKB_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   {
-    static const int forced = [] {
-      const char* e = getenv("TK_TC_ACC");
-      return e ? atoi(e) : 0;
-    }();
+    const int forced = xp.tc_acc;
     p.acc_slots = p.BN <= 64 ? 8 : (p.BN <= 128 ? 4 : 2);
     if (forced == 2 || forced == 4 || forced == 8) p.acc_slots = std::min(p.acc_slots, forced);
     p.acc_cols = 2 * kAccCols / p.acc_slots;
@@ -1294,10 +1278,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     p.kb_per = p.num_kb;
   }
   {
-    static const int raster = [] {
-      const char* e = getenv("TK_RASTER");
-      return e ? atoi(e) : 8;
-    }();
+    const int raster = xp.raster;
     const long long units_all = (long long)p.num_m * p.num_n * p.batch * p.splits;
     // Grouping only pays once tiles queue up behind the resident wave.
     p.raster = ((plain_like<MODE>() || MODE == kConvPixN) && units_all > 2LL * (sm_count() / CG))
@@ -1326,14 +1307,9 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  static const bool pdl = [] {
-    const char* e = getenv("TK_PDL");
-    return !(e && e[0] == '0');
-  }();
-  cfg.numAttrs = pdl ? 2 : 1;
-  const char* tr = getenv("TK_TC_TRACE");
+  cfg.numAttrs = xp.pdl ? 2 : 1;
   unsigned long long* trace = nullptr;
-  if (tr && tr[0] == '1') {
+  if (xp.trace) {
     TKB_CUDA(cudaMalloc(&trace, (size_t)grid * kTraceEvents * 8));
     TKB_CUDA(cudaMemset(trace, 0, (size_t)grid * kTraceEvents * 8));
     p.trace = trace;
@@ -1987,10 +1963,7 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
   const bool b_ok = tf32 && !tb && kp == (long long)k && aligned(b);
   // Column-major, untransposed A is MN-major: the tensor core reads it in
   // place (no transpose pass) when M is a multiple of 32.
-  static const bool mn_on = [] {
-    const char* e = getenv("TK_A_MN");
-    return !(e && e[0] == '0');
-  }();
+  const bool mn_on = experiments().a_mn;
   const bool a_mn = mn_on && tf32 && !ta && m % 32 == 0 && aligned(a) && m <= (1ull << 31);
   const size_t esz = tf32 ? 4 : 2;
   void* pa = nullptr;
@@ -2153,7 +2126,7 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
   const bool tf32 = precision == TK_PREC_TF32;
   const int esize = tf32 ? 4 : 2, ek = kSlabBytes / esize;
   const long long pix = (long long)g.N * g.OH * g.OW;
-  const char* force = getenv("TK_CONV_MODE");
+  const char* force = experiments().conv_mode.empty() ? nullptr : experiments().conv_mode.c_str();
   const int mode = tc_knobs().mode;
   // Strided 1x1 in TF32 reads the strided pixels straight through a
   // traversal-stride pixel box (no compacting pass); BF16 needs a conversion
@@ -2187,7 +2160,7 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
     // two TMA-store staging buffers, so a tile's store overlaps the next
     // drain.
     if (c.bn > 128 && c.kp / ek <= 4) c.bn = 128;
-    if (const char* e = getenv("TK_PW_BN")) c.bn = atoi(e);
+    if (experiments().pw_bn > 0) c.bn = experiments().pw_bn;
     c.num_m = (int)((pix + kRows * c.cg - 1) / (kRows * c.cg));
     c.num_n = (g.K + c.bn - 1) / c.bn;
     const int num_kb = (int)(c.kp / ek);
@@ -2305,9 +2278,8 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
       const size_t out_bytes = (size_t)g.N * g.OH * g.OW * g.K * 4;
       const bool aligned = g.K % 4 == 0;
       const long long pairs = sm_count() / c.cg;
-      const char* nosplit = getenv("TK_NO_SPLIT");
       const int pbn = c.bx.wb * c.bx.tileH * c.imgs;
-      const int sp = (aligned && !(nosplit && nosplit[0] == '1'))
+      const int sp = (aligned && !experiments().no_split)
                          ? choose_splits((long long)c.num_m * c.num_n, c.num_kb, pairs,
                                          kRows * c.cg, pbn, out_bytes, 64ull << 20)
                          : 1;
@@ -2347,10 +2319,7 @@ ConvPlan plan_conv(const ConvGeom& g, int precision) {
   return c;
 }
 
-bool tf32_filter_rounding() {
-  const char* rnd = getenv("TK_TF32_ROUND");
-  return !(rnd && rnd[0] == '0');
-}
+bool tf32_filter_rounding() { return experiments().tf32_round; }
 
 // 1x1 convolution as a plain tensor-core GEMM (see plan_conv).
 void launch_pointwise(const ConvGeom& g, const ConvPlan& c, const float* in, const float* filt,
@@ -2483,6 +2452,30 @@ size_t split3_bytes_in(const ConvGeom& g) { return align256((size_t)g.N * g.H * 
 size_t split3_bytes_filt(const ConvGeom& g) { return align256((size_t)g.R * g.S * g.C * g.K * 12); }
 }  // namespace
 
+// Feature tile of the halo mode: 128 wide when the features come in 128s
+// (N = 128 MMAs and half the units of N = 64: VGG conv2_1 105 -> 91 us,
+// ResNet res3a/res4a_branch2b 27 -> 25 us, same-box A/B); two operand stages
+// (halo 22.5 KiB + 9 filter taps x 8 KiB each) still fit.
+static int halo_bn(const ConvGeom& g) {
+  int bn = g.K <= 32 ? 32 : (g.K % 128 == 0 ? 128 : 64);
+  const int b = experiments().halo_bn;
+  if ((b == 64 || b == 128) && g.K % b == 0) bn = b;
+  return bn;
+}
+
+// Halo mode keeps the CTA's filter slice resident in shared memory when it
+// fits next to three halo stages and the feature blocks divide the SM pairs.
+static bool halo_resident(const ConvGeom& g, int bn, int cchunks, int halo_bytes, int num_n) {
+  const int cg = 2;
+  const int b_bytes_h = (bn / cg) * kSlabBytes;
+  const int fres = g.R * g.S * cchunks * b_bytes_h;
+  const int epi = ((bn + 31) / 32) * kRows * kSlabBytes;
+  const int left = 232448 - 2048 - epi - fres;
+  const int units = sm_count() / cg;
+  if (experiments().conv_mode == "halo_stream") return false;
+  return left >= 3 * halo_bytes && units % num_n == 0;
+}
+
 size_t tc_conv_workspace(const ConvGeom& g, int precision) {
   if (precision == TK_PREC_3XTF32)
     return split3_bytes_in(g) + split3_bytes_filt(g) + tc_conv_workspace(tripled(g), TK_PREC_TF32);
@@ -2550,8 +2543,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     const int pixels = g.N * g.OH * g.OW;
     // One SM per tile (cta_group::1): the gather producers then signal their
     // own CTA's barrier -- no cross-CTA release on every K-slab.
-    int cg = 1;
-    if (const char* e = getenv("TK_GATHER_CG")) cg = atoi(e) == 2 ? 2 : 1;
+    const int cg = experiments().gather_cg;
     TcArgs p{};
     p.M = pixels;
     p.N = g.K;
@@ -2611,7 +2603,6 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
 
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + plan.filt_bytes + plan.in_bytes);
   if (!run) return;
-  const char* force = getenv("TK_CONV_MODE");
   const bool use_halo = plan.halo;
   if (use_halo) {
     const int cg = 2;
@@ -2629,11 +2620,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     // and half the units of N = 64: VGG conv2_1 105 -> 91 us, ResNet
     // res3a/res4a_branch2b 27 -> 25 us, same-box A/B); two operand stages
     // (halo 22.5 KiB + 9 filter taps x 8 KiB each) still fit.
-    p.BN = g.K <= 32 ? 32 : (g.K % 128 == 0 ? 128 : 64);
-    if (const char* e = getenv("TK_HALO_BN")) {  // experiment knob
-      const int b = atoi(e);
-      if ((b == 64 || b == 128) && g.K % b == 0) p.BN = b;
-    }
+    p.BN = halo_bn(g);
     p.Wb = p.TW;
     p.tileH = cg * p.TH;
     p.tiles_w = (g.OW + p.TW - 1) / p.TW;
@@ -2660,15 +2647,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     const CUtensorMap md = make_map(out, 4, 4, dims, strides, box);
     p.store_tma = 1;
     p.epi_bufs = 1;
-    {
-      const int b_bytes_h = (p.BN / cg) * kSlabBytes;
-      const int fres = p.taps * p.cchunks * b_bytes_h;
-      const int epi = ((p.BN + 31) / 32) * kRows * kSlabBytes;
-      const int left = 232448 - 2048 - epi - fres;
-      const int units = sm_count() / cg;
-      p.resident = (left >= 3 * p.halo_bytes && units % p.num_n == 0) ? 1 : 0;
-      if (force && std::string(force) == "halo_stream") p.resident = 0;
-    }
+    p.resident = halo_resident(g, p.BN, p.cchunks, p.halo_bytes, p.num_n) ? 1 : 0;
     dispatch<kConvHalo>(ma, mb, md, p, cg, tf32, st);
     return;
   }
@@ -2738,6 +2717,72 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     p.epi_bufs = 2;
     dispatch<kConvPixM>(ma, mb, md, p, cg, tf32, st);
   }
+}
+
+TcConvInfo tc_conv_info(const ConvGeom& g, int precision) {
+  require_tc(precision);
+  TcConvInfo r;
+  if (precision == TK_PREC_3XTF32) {
+    // One TF32 convolution over 3C channels ([x | x | x_lo] . [f_hi | f_lo | f_hi]).
+    r = tc_conv_info(tripled(g), TK_PREC_TF32);
+    r.precision = TK_PREC_3XTF32;
+    return r;
+  }
+  const ConvPlan c = plan_conv(g, precision);
+  r.precision = c.tf32 ? TK_PREC_TF32 : TK_PREC_BF16;
+  r.cta_group = c.cg;
+  r.splits = c.splits;
+  r.tail_pieces = c.tail.q > 1 ? c.tail.q : 0;
+  switch (c.kind) {
+    case kPointwisePlan:
+    case kIm2colPlan:
+      r.mode = c.kind == kPointwisePlan ? TK_TC_POINTWISE : TK_TC_IM2COL;
+      r.tile_m = kRows * c.cg;
+      r.tile_n = c.bn;
+      break;
+    case kGatherPlan:
+      // fp32 operands built by the producer warps: kind::tf32 whatever the request.
+      r.mode = TK_TC_GATHER;
+      r.precision = TK_PREC_TF32;
+      r.cta_group = experiments().gather_cg;
+      r.tile_m = kRows * r.cta_group;
+      r.tile_n = std::min(128, (g.K + 16 * r.cta_group - 1) / (16 * r.cta_group) * (16 * r.cta_group));
+      r.splits = 1;
+      r.tail_pieces = 0;
+      break;
+    default:
+      if (c.halo) {
+        const int ek = kSlabBytes / (c.tf32 ? 4 : 2);
+        const int TH = kRows / 16, TW = 16 - (g.S - 1);
+        const int bn = halo_bn(g);
+        const int num_n = (g.K + bn - 1) / bn;
+        r.mode = TK_TC_HALO;
+        r.cta_group = 2;
+        r.tile_m = kRows * 2;  // 2 x 8 rows of a pitch-16 halo (TW useful columns)
+        r.tile_n = bn;
+        r.box_w = TW;
+        r.box_h = 2 * TH;
+        r.halo_resident =
+            halo_resident(g, bn, g.C / ek, (TH + g.R) * 16 * kSlabBytes, num_n) ? 1 : 0;
+        r.splits = 1;
+        r.tail_pieces = 0;
+      } else if (c.pix_on_n) {
+        r.mode = TK_TC_PIXN;
+        r.tile_m = kRows * c.cg;
+        r.tile_n = c.bx.wb * c.bx.tileH * c.imgs;
+        r.imgs = c.imgs;
+        r.flat = c.flat ? 1 : 0;
+        r.box_w = c.bx.wb;
+        r.box_h = c.bx.tileH;
+      } else {
+        r.mode = TK_TC_PIXM;
+        r.tile_m = kRows * c.cg;
+        r.tile_n = (g.K + 16 * c.cg - 1) / (16 * c.cg) * (16 * c.cg);
+        r.box_w = c.bx.wb;
+        r.box_h = c.bx.tileH;
+      }
+  }
+  return r;
 }
 
 }  // namespace tkb

@@ -57,6 +57,16 @@ size_t tc_conv_workspace(const ConvGeom& g, int precision);
 // phase: kConvPrepare packs the filter into the workspace (depends only on
 // the filter), kConvRun runs the convolution from a prepared workspace.
 constexpr int kConvPrepare = 1, kConvRun = 2, kConvAll = 3;
+// What launch_tc_conv will run for this geometry and precision request
+// (tk_conv2d_plan_info): operand path, the precision the tensor cores
+// actually compute in, tile and work split.
+struct TcConvInfo {
+  int mode = 0;        // enum tk_tc_mode of the operand path
+  int precision = 0;   // effective enum tk_precision
+  int cta_group = 1, tile_m = 0, tile_n = 0, splits = 1, tail_pieces = 0;
+  int imgs = 1, flat = 0, box_w = 0, box_h = 0, halo_resident = 0;
+};
+TcConvInfo tc_conv_info(const ConvGeom& g, int precision);
 void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float* out,
                     int precision, void* ws, cudaStream_t st, int phase = kConvAll);
 

@@ -1,0 +1,137 @@
+"""GPU parity at exactly the configurations bench.py times.
+
+Every distinct VGG-16 (9) and ResNet-50 (21) conv shape at batch 32 -- the
+per-GPU shard of BASELINE configs[4], the plans the headline and the
+secondary stacks run (tail plan, split-K count, flat rows, multi-image
+tiles, halo width, resident filter all depend on N) -- through the bench's
+own call sequence: tk_conv2d_workspace_size, tk_conv2d_prepare_dev,
+tk_conv2d_run_dev.  Images {0, 15, 31} are checked against single-image runs
+of the oracle (conv2d_naive, reference conv.hpp:74-113; batch independence,
+test_conv.cpp:268-293), in every precision:
+
+  fp32    bit-identical (max_rel_error == 0)
+  tf32    max_scaled_error <= 1e-3
+  bf16    max_scaled_error <= 5e-3 (the EFFECTIVE precision from
+          tk_conv2d_plan_info decides the bar: a BF16 request that runs in
+          TF32 is reported and held to the TF32 bar)
+  3xtf32  max_scaled_error <= 5e-5
+
+The oracle result of a (layer, image) is computed once and shared by the
+four precisions.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import RESNET50, VGG16  # noqa: E402
+
+N = 32
+IMAGES = (0, 15, 31)
+TOL = {"tf32": 1e-3, "bf16": 5e-3, "3xtf32": 5e-5}
+
+LAYERS = [(name, 3, 1, h, c, k) for name, h, c, k, _ in VGG16] + \
+         [(name, r, s, h, c, k) for name, r, s, h, c, k, _ in RESNET50]
+
+_inputs = {}
+_want = {}
+
+
+def _host_inputs(tk, idx):
+    """Selected images of the layer's seeded batch-32 input + its filter."""
+    import torch
+    name, r, s, h, c, k = LAYERS[idx]
+    if idx not in _inputs:
+        gen = torch.Generator(device="cuda").manual_seed(1000 + idx)
+        x = torch.rand((N, h, h, c), device="cuda", generator=gen) * 2 - 1
+        f = torch.rand((r, r, c, k), device="cuda", generator=gen) * 2 - 1
+        _inputs[idx] = ({i: x[i:i + 1].cpu().numpy() for i in IMAGES}, f.cpu().numpy())
+        del x, f
+    return _inputs[idx]
+
+
+def _device_inputs(idx):
+    import torch
+    name, r, s, h, c, k = LAYERS[idx]
+    gen = torch.Generator(device="cuda").manual_seed(1000 + idx)
+    x = torch.rand((N, h, h, c), device="cuda", generator=gen) * 2 - 1
+    f = torch.rand((r, r, c, k), device="cuda", generator=gen) * 2 - 1
+    return x, f
+
+
+def _oracle(oracle, tk, idx, img):
+    key = (idx, img)
+    if key not in _want:
+        name, r, s, h, c, k = LAYERS[idx]
+        xs, f = _host_inputs(tk, idx)
+        conv = oracle.Conv(1, h, h, c, k, r, r, s, True)
+        _want[key] = oracle.conv2d_naive(conv, xs[img], f)
+    return _want[key]
+
+
+def _run(tk, idx, prec, x, f):
+    import torch
+    name, r, s, h, c, k = LAYERS[idx]
+    shape = tk.ConvShape(N, h, h, c, k, r, r, s, True)
+    algo = tk.parse_conv_params("im2col")
+    ws = torch.empty(max(tk.conv2d_workspace_size(shape, algo, prec), 4) // 4 + 1, device="cuda")
+    y = torch.full(shape.out_shape, float("nan"), device="cuda")
+    side = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    side.wait_stream(main)
+    # the bench forks the filter prepare to a side stream and joins before run
+    tk.conv2d_prepare_dev(f, shape, algo, ws, precision=prec, stream=side)
+    main.wait_stream(side)
+    tk.conv2d_run_dev(x, f, y, shape, algo, ws, precision=prec, stream=main)
+    torch.cuda.synchronize()
+    return y
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("prec", ["tf32", "bf16", "3xtf32", "fp32"])
+@pytest.mark.parametrize("idx", range(len(LAYERS)), ids=[lay[0] for lay in LAYERS])
+def test_bench_layer_batch32(tk, oracle, idx, prec):
+    name, r, s, h, c, k = LAYERS[idx]
+    shape = tk.ConvShape(N, h, h, c, k, r, r, s, True)
+    plan = tk.conv2d_plan_info(shape, tk.parse_conv_params("im2col"), prec)
+    assert plan["requested_precision"] == prec
+    x, f = _device_inputs(idx)
+    y = _run(tk, idx, prec, x, f)
+    assert not bool(torch_isnan_any(y)), (name, prec, plan)
+    for img in IMAGES:
+        want = _oracle(oracle, tk, idx, img)
+        got = y[img:img + 1].cpu().numpy()
+        if prec == "fp32":
+            assert plan["precision"] == "fp32"
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (name, img)
+        else:
+            bar = TOL[plan["precision"]] if plan["precision"] in TOL else TOL[prec]
+            err = oracle.max_scaled_error(got, want)
+            assert err <= bar, (name, prec, img, err, plan)
+    if prec == "tf32":
+        # deterministic run to run (ordered split-K / tail reductions)
+        y2 = _run(tk, idx, prec, x, f)
+        import torch
+        assert torch.equal(y.view(torch.int32), y2.view(torch.int32)), (name, plan)
+
+
+def torch_isnan_any(y):
+    import torch
+    return torch.isnan(y).any().item()
+
+
+@pytest.mark.parametrize("idx", range(len(LAYERS)), ids=[lay[0] for lay in LAYERS])
+def test_plan_reports_effective_precision(tk, idx):  # host-only: runs on CPU too
+    """BF16 requests report the arithmetic that actually runs: bf16 on the
+    box / halo / pointwise / im2col paths, tf32 on the gather producers
+    (fp32 operands) -- never silently."""
+    name, r, s, h, c, k = LAYERS[idx]
+    shape = tk.ConvShape(N, h, h, c, k, r, r, s, True)
+    plan = tk.conv2d_plan_info(shape, tk.parse_conv_params("im2col"), "bf16")
+    if plan["kernel"] == "tc_gather":
+        assert plan["precision"] == "tf32"
+    else:
+        assert plan["precision"] == "bf16"

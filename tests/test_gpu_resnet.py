@@ -69,20 +69,21 @@ def test_resnet_layer_exact(tk, oracle, row):
 
 
 @pytest.mark.timeout(120)
-def test_gather_mode_many_tiles_many_slabs(tk, oracle, monkeypatch):
+def test_gather_mode_many_tiles_many_slabs(tk, oracle):
     """Regression: res3a_branch2a (1x1/s2, C=256) at batch 32 runs the gather
     producer with several tiles per CTA and more K-slabs per tile than
     pipeline stages (the configuration that once deadlocked).  Images 0 and
     31 are checked against single-image oracle runs."""
     import torch
-    monkeypatch.setenv("TK_CONV_MODE", "gather")  # 1x1 layers default to the pointwise GEMM
     N, H, C, K = 32, 56, 256, 128
     s = tk.ConvShape(N, H, H, C, K, 1, 1, 2, True)
     gen = torch.Generator(device="cuda").manual_seed(3)
     dx = torch.rand((N, H, H, C), device="cuda", generator=gen) * 2 - 1
     df = torch.rand((1, 1, C, K), device="cuda", generator=gen) * 2 - 1
     dy = torch.empty(s.out_shape, device="cuda")
-    tk.conv2d_dev(dx, df, dy, s, tk.parse_conv_params("im2col"), precision="tf32")
+    # 1x1 layers default to the pointwise GEMM: force the gather producers
+    tk.conv2d_dev(dx, df, dy, s, tk.parse_conv_params("im2col"),
+                  options=tk.exec_options("tf32", mode="gather"))
     torch.cuda.synchronize()
     f = df.cpu().numpy()
     for img in (0, N - 1):

@@ -40,6 +40,7 @@ else:
 for _ in range(3):
     run()
 torch.cuda.synchronize()
+os.environ["TK_EXPERIMENTS"] = "1"
 os.environ["TK_TC_TRACE"] = "1"
 run()
 torch.cuda.synchronize()
