@@ -4,6 +4,17 @@ configs[1]; configs[4] when run on 8 GPUs = batch 256 sharded by batch).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--precision tf32|fp32]
     python bench.py --impl reference ...     # the reference CPU implementation
 
+--gpus N > 1 outside torchrun re-executes itself under torch.distributed.run
+(one process per GPU, NCCL, 127.0.0.1); under torchrun WORLD_SIZE must equal N.
+Multi-GPU: rank r owns images [32 r, 32 r + 32) of one
+logical batch-(32 N) tensor per layer (each image seeded by its global
+index, so the shard is built with no communication), filters are broadcast
+once from rank 0 over NCCL; no collective runs inside the timed region.
+After timing, one layer's output shards are gathered to rank 0 over NCCL and
+compared bitwise with rank 0 recomputing every shard; a GEMM leg (8192^3
+TF32, column panels of C = the row-major "M-panels", A broadcast) runs the
+same way.
+
 One step = every conv layer of VGG-16 (13 layers, 9 distinct shapes from
 proj/data/vgg_layers.csv with the canonical multiplicities) on its own
 resident synthetic input, through the C ABI (tk_conv2d_dev).  Metric: total
@@ -231,7 +242,7 @@ class CpuReference:
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
-        return
+        return 0
     ref = CpuReference()
     # A step = one full VGG16 stack (all 13 layer instances) at batch 1: the
     # same per-layer mix as the GPU step, 1/32 of its images (~0.7 s on 16
@@ -262,6 +273,26 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def relaunch(args) -> int:
+    """--gpus N outside torchrun: re-execute this script under
+    torch.distributed.run with N local ranks (rank 0 prints the line)."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) visible"}),
+              flush=True)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------------------
@@ -270,8 +301,9 @@ def run_reference(args):
 def main():
     args = parse()
     if args.impl == "reference":
-        run_reference(args)
-        return
+        return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
 
     import torch
     import torch.distributed as dist
@@ -281,6 +313,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -288,22 +322,26 @@ def main():
     stream = torch.cuda.current_stream()
     N = args.batch
     prec = args.precision
+    lo_img, hi_img = rank * N, (rank + 1) * N  # this rank's images of the global batch
 
     # Resident inputs: one independent seeded input + filter per layer
     # instance (the reference `layers` harness, tilekit_cli.cpp:374-403).
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    # Inputs: this rank's slice of the logical batch-(N * world) tensor;
+    # filters: seeded on rank 0, replicated by one NCCL broadcast.
+    gen = torch.Generator(device=dev).manual_seed(1234)
     layers = []
     for name, h, c, k, mult in VGG16:
         for rep in range(mult):
             shape = tk.ConvShape(N, h, h, c, k, 3, 3, 1, True)
             algo = tk.parse_conv_params("im2col")
-            x = torch.rand((N, h, h, c), device=dev, generator=gen) * 2 - 1
+            x = shard.seeded_images((h, h, c), lo_img, hi_img, 1234, len(layers), dev)
             f = torch.rand((3, 3, c, k), device=dev, generator=gen) * 2 - 1
+            shard.broadcast_(f)
             y = torch.empty((N, h, h, k), device=dev)
             ws_n = tk.conv2d_workspace_size(shape, algo, prec)
             ws = torch.empty(max(ws_n, 4) // 4 + 1, device=dev)
             layers.append(dict(name=name, shape=shape, algo=algo, x=x, f=f, y=y, ws=ws,
-                               flops=conv_flops(N, h, c, k)))
+                               flops=conv_flops(N, h, c, k), hwc=(h, h, c)))
     flush = torch.empty(64 * 1024 * 1024, device=dev)  # 256 MiB > 126 MB L2
     step_flops = sum(L["flops"] for L in layers)
 
@@ -400,9 +438,86 @@ def main():
     if launches_per_step is not None:
         launches = launches_per_step * args.steps
     torch.cuda.synchronize()
+    rank_ms = shard.all_gather_scalar(float(sum(times)) / args.steps, device=dev)
     total_ms = shard.max_over_ranks(float(sum(times)), device=dev)
     ms_per_step = total_ms / args.steps
     value = step_flops * world / (ms_per_step * 1e-3) / 1e9
+
+    # Multi-GPU verification (outside every timed region): the last layer's
+    # output shards (vgg_conv5, 12.8 MB per rank) gathered to rank 0 over
+    # NCCL, compared bitwise with rank 0 recomputing each shard from its
+    # seeded images (same shape, same plan => same bits), and image 0 of each
+    # shard against the library's bit-exact FP32 path.
+    multi = {"ranks": world, "rank_ms_per_step": [round(v, 4) for v in rank_ms],
+             "images_per_rank": N, "global_batch": N * world}
+    vi = len(layers) - 1
+    Lv = layers[vi]
+    torch.cuda.synchronize()
+    parts = shard.gather_to(Lv["y"], 0)
+    if rank == 0:
+        same, worst = True, 0.0
+        for r, part in enumerate(parts):
+            xr = shard.seeded_images(Lv["hwc"], r * N, (r + 1) * N, 1234, vi, dev)
+            yr = torch.empty_like(Lv["y"])
+            tk.conv2d_dev(xr, Lv["f"], yr, Lv["shape"], Lv["algo"], precision=prec, stream=stream)
+            s1 = tk.ConvShape(1, *Lv["hwc"][:2], Lv["hwc"][2], Lv["shape"].features, 3, 3, 1, True)
+            ye = torch.empty((1,) + tuple(Lv["y"].shape[1:]), device=dev)
+            tk.conv2d_dev(xr[:1].contiguous(), Lv["f"], ye, s1, Lv["algo"], precision="fp32",
+                          stream=stream)
+            torch.cuda.synchronize()
+            same &= bool(torch.equal(yr.view(torch.int32), part.view(torch.int32)))
+            worst = max(worst, float((part[:1] - ye).abs().max() / ye.abs().max().clamp_min(1e-6)))
+        multi["verify"] = {"layer": Lv["name"], "gathered_bytes": int(Lv["y"].numel() * 4 * world),
+                           "shards_bitwise_equal_to_recompute": same,
+                           "max_scaled_error_vs_fp32_exact_img0": worst}
+    del parts
+
+    # GEMM leg (BASELINE configs[3] at 8192^3, TF32): column panels of the
+    # column-major C (the row-major formulation's M-panels), panel edges on
+    # the 256-wide tensor-core tile, A replicated by broadcast, each rank's
+    # B panel seeded per 256-column block.  Strong scaling: fixed total work.
+    gn = 8192
+    glo, ghi = shard.panel_range(gn, world, rank, 256)
+    ga = torch.rand(gn * gn, device=dev, generator=torch.Generator(device=dev).manual_seed(99)) * 2 - 1
+    shard.broadcast_(ga)
+    gb = shard.seeded_columns(gn, glo, ghi, 4242, 256, dev)
+    gc = torch.empty(gn * (ghi - glo), device=dev)
+    gshape = tk.GemmShape(gn, ghi - glo, gn)
+    for _ in range(2):
+        tk.gemm_dev(ga, gb, None, gc, gshape, None, precision="tf32", stream=stream)
+    gts = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(5):
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        tk.gemm_dev(ga, gb, None, gc, gshape, None, precision="tf32", stream=stream)
+        b_.record(stream)
+        b_.synchronize()
+        gts.append(a_.elapsed_time(b_))
+    g_ms = float(np.median(gts))
+    g_rank = shard.all_gather_scalar(g_ms, device=dev)
+    g_max = max(g_rank)
+    panels = {"value": round(2 * gn ** 3 / (g_max * 1e-3) / 1e9, 1), "unit": "GFLOP/s",
+              "scaling": "strong", "ms_max_over_ranks": round(g_max, 4),
+              "rank_ms": [round(v, 4) for v in g_rank], "panel_cols": ghi - glo,
+              "config": f"C = A B, {gn}^3 TF32, column panels of C (A broadcast)"}
+    gparts = shard.gather_to(gc[: gn * 256].clone(), 0)  # first 256 columns of every panel
+    if rank == 0:
+        same = True
+        for r, part in enumerate(gparts):
+            rlo, rhi = shard.panel_range(gn, world, r, 256)
+            br = shard.seeded_columns(gn, rlo, rhi, 4242, 256, dev)
+            cr = torch.empty(gn * (rhi - rlo), device=dev)
+            tk.gemm_dev(ga, br, None, cr, tk.GemmShape(gn, rhi - rlo, gn), None, precision="tf32",
+                        stream=stream)
+            torch.cuda.synchronize()
+            same &= bool(torch.equal(cr[: gn * 256].view(torch.int32), part.view(torch.int32)))
+            del br, cr
+        panels["verify_first_256_cols_bitwise"] = same
+    multi["gemm8192_tf32_panels"] = panels
+    del ga, gb, gc, gparts
 
     # Per-layer device times of the conv kernels (after the timed steps; same
     # stream, CUDA events),
@@ -576,7 +691,7 @@ def main():
     # of the stack and BASELINE configs[0], SGEMM 1024^3 (row-major C = A B as
     # the column-major nn call with operands swapped).
     secondary = {}
-    if not args.no_secondary:
+    if not args.no_secondary and world == 1:
         def stack_ms(p_, reps):
             ts = []
             for _ in range(reps):
@@ -838,12 +953,15 @@ def main():
                         "median": round(float(np.median(times)), 4),
                         "max": round(float(np.max(times)), 4)},
             "layers": layer_rows,
+            "multi_gpu": multi,
             "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

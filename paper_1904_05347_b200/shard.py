@@ -74,3 +74,78 @@ def gather_batch_shards(local, total_batch: int, dst: int = 0):
     if local.shape[0] > 0:
         dist.send(local.contiguous(), dst=dst)
     return None
+
+
+# ---------------------------------------------------------------------------
+# Logical full-batch tensors, sharded without communication
+# ---------------------------------------------------------------------------
+def image_seed(base: int, layer: int, image: int) -> int:
+    """Seed of image `image` (global index) of layer `layer`'s input: the
+    logical batch-256 tensor is defined image by image, so a rank
+    materialises exactly its slice [lo, hi) and any other rank can rebuild
+    it bit for bit for verification."""
+    return base + layer * 1_000_003 + image
+
+
+def seeded_images(hwc, lo: int, hi: int, base: int, layer: int, device):
+    """Images [lo, hi) of the logical NHWC tensor (uniform [-1, 1))."""
+    import torch
+    out = torch.empty((hi - lo,) + tuple(hwc), device=device)
+    gen = torch.Generator(device=device)
+    for i in range(lo, hi):
+        gen.manual_seed(image_seed(base, layer, i))
+        out[i - lo].uniform_(-1.0, 1.0, generator=gen)
+    return out
+
+
+def seeded_columns(rows: int, lo: int, hi: int, base: int, block: int, device):
+    """Columns [lo, hi) of a logical column-major rows x n matrix, generated
+    in blocks of `block` columns (lo, hi multiples of `block` except the
+    end): a rank builds its own column panel of B without communication."""
+    import torch
+    out = torch.empty((hi - lo) * rows, device=device)
+    gen = torch.Generator(device=device)
+    for b0 in range(lo, hi, block):
+        b1 = min(hi, b0 + block)
+        gen.manual_seed(base + b0 // block)
+        out[(b0 - lo) * rows:(b1 - lo) * rows].uniform_(-1.0, 1.0, generator=gen)
+    return out
+
+
+def broadcast_(t, src: int = 0):
+    """One-time replication of a shared operand (filters, GEMM A) over NCCL
+    (NVLink); identity without a process group.  Never on the timed path."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.broadcast(t, src=src)
+    return t
+
+
+def all_gather_scalar(value: float, device=None) -> List[float]:
+    """Per-rank scalars (device times) on every rank, in rank order."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [float(value)]
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t)
+    return [float(p.item()) for p in parts]
+
+
+def gather_to(local, dst: int = 0):
+    """Verification-only gather of equally shaped per-rank tensors to `dst`
+    (a list in rank order there, None elsewhere)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [local]
+    world, rank = dist.get_world_size(), dist.get_rank()
+    if rank == dst:
+        parts = [local if r == rank else torch.empty_like(local) for r in range(world)]
+        for r in range(world):
+            if r != rank:
+                dist.recv(parts[r], src=r)
+        return parts
+    dist.send(local.contiguous(), dst=dst)
+    return None

@@ -82,3 +82,55 @@ def test_two_rank_gloo_decomposition():
     ok_conv, ok_gemm, t = q.get(timeout=10)
     assert ok_conv and ok_gemm
     assert t == 2.0  # MAX over ranks
+
+
+def _worker_helpers(rank, world, port, q):
+    """The helpers bench.py's multi-GPU leg uses, on gloo: per-rank seeded
+    slices of one logical tensor, broadcast of the shared operand, gather to
+    rank 0, per-rank scalars."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    from paper_1904_05347_b200 import shard
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        per = 3
+        lo, hi = rank * per, (rank + 1) * per
+        mine = shard.seeded_images((4, 5, 2), lo, hi, 1234, 7, "cpu")
+        cols = shard.seeded_columns(6, *shard.panel_range(8, world, rank, 4), 4242, 4, "cpu")
+        f = torch.full((3,), float(rank))
+        shard.broadcast_(f)  # rank 0's filter everywhere
+        parts = shard.gather_to(mine, 0)
+        cparts = shard.gather_to(cols, 0)
+        ts = shard.all_gather_scalar(10.0 + rank)
+        if rank == 0:
+            whole = shard.seeded_images((4, 5, 2), 0, per * world, 1234, 7, "cpu")
+            wcols = shard.seeded_columns(6, 0, 8, 4242, 4, "cpu")
+            q.put((bool(torch.equal(torch.cat(parts), whole)),
+                   bool(torch.equal(torch.cat(cparts), wcols)),
+                   float(f.sum()), ts))
+        else:
+            q.put(None)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gloo_bench_helpers():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30600 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_worker_helpers, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(240)
+        assert p.exitcode == 0
+    res = [q.get(timeout=10) for _ in range(2)]
+    res = [r for r in res if r is not None][0]
+    ok_imgs, ok_cols, fsum, ts = res
+    assert ok_imgs and ok_cols
+    assert fsum == 0.0  # broadcast from rank 0
+    assert ts == [10.0, 11.0]
