@@ -658,7 +658,9 @@ def conv2d_plan_info(shape: ConvShape, params: ConvAlgoParams, precision="fp32",
 
 
 def gemm_dev(a, b, c, out, shape: GemmShape, cfg: Optional[GemmConfig] = None,
-             precision="fp32", stream=None, tile_n=0) -> None:
+             precision="fp32", stream=None, tile_n=0, options=None) -> None:
+    """options: an exec_options(...) record (tensor-core knobs); overrides
+    precision / tile_n when given."""
     na, nb, nc = _gemm_sizes(shape)
     _need_dev(a, "gemm: operand A", na)
     _need_dev(b, "gemm: operand B", nb)
@@ -668,7 +670,8 @@ def gemm_dev(a, b, c, out, shape: GemmShape, cfg: Optional[GemmConfig] = None,
         _need_dev(c, "gemm: operand C", nc)
     _need_dev(out, "gemm: output", nc)
     cfg_c = C.byref(cfg.c()) if cfg is not None else None
-    _check(lib().tk_gemm_dev(C.byref(shape.c()), cfg_c, C.byref(exec_options(precision, tile_n)),
+    opts = options if options is not None else exec_options(precision, tile_n)
+    _check(lib().tk_gemm_dev(C.byref(shape.c()), cfg_c, C.byref(opts),
                              _dptr(a), _dptr(b), _dptr(c), _dptr(out), _stream(stream)))
 
 

@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "exact_gemm.cuh"
 #include "experiments.cuh"
+#include "launch_cache.cuh"
 #include "layout.cuh"
 #include "tc_gemm.cuh"
 #include "tilekit/gemm.hpp"
@@ -1022,8 +1023,8 @@ int tk_conv2d_dev(const tk_conv_shape* shape, const tk_conv_params* params,
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (need && (!d_ws || ws_bytes < need)) {
       keep_pool_memory();
-      DevBuf tmp(need, st);
-      conv_dev(s, params, prec, d_in, d_filt, d_out, tmp.p, st);
+      Scratch tmp(st, kScratchConvWs, need);
+      conv_dev(s, params, prec, d_in, d_filt, d_out, tmp.get(), st);
     } else {
       conv_dev(s, params, prec, d_in, d_filt, d_out, d_ws, st);
     }

@@ -2,6 +2,7 @@
 #include <string>
 
 #include "exact_gemm.cuh"
+#include "launch_cache.cuh"
 
 namespace tkb {
 
@@ -64,8 +65,7 @@ NolocFn pick_noloc(int h, int w, bool conv) {
 // Resource check: a configuration the SM cannot host is rejected loudly
 // (the paper's register/local-memory budget, measured on the real kernel).
 void check_fits(const void* fn, int threads, size_t smem, const ExactLaunch& L) {
-  cudaFuncAttributes attr{};
-  TKB_CUDA(cudaFuncGetAttributes(&attr, fn));
+  const cudaFuncAttributes& attr = func_attrs(fn);
   const std::string name = std::to_string(L.h) + "x" + std::to_string(L.w) + "_" +
                            std::to_string(L.r) + "x" + std::to_string(L.c);
   if (threads > attr.maxThreadsPerBlock) {
@@ -103,9 +103,7 @@ void launch_exact(const ExactArgs& p, const ExactLaunch& L, bool conv, int batch
                          (size_t)(bl == kMN ? kExactBK * (BN + 4) : BN * (kExactBK + 4));
     const size_t smem = words * 4 * stages + (conv ? BM * 16 : 0);  // + pixel table
     check_fits((const void*)fn, threads, smem, L);
-    if (smem > 48 * 1024)
-      TKB_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
+    if (smem > 48 * 1024) func_smem((const void*)fn, smem);
     fn<<<grid, threads, smem, stream>>>(p, L.r, L.c, stages);
   } else {
     NolocFn fn = pick_noloc(L.h, L.w, conv);

@@ -33,13 +33,16 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 #include <cstdio>
 
 #include "common.cuh"
 #include "experiments.cuh"
+#include "launch_cache.cuh"
 #include "tc_gemm.cuh"
 #include "tc_ptx.cuh"
 
@@ -934,11 +937,57 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// Tensor maps are memoised per calling thread on every argument of the
+// encode (base pointer included): a repeated call with the same buffers pays
+// a hash lookup instead of a driver encode (~1-2 us each, three per launch).
+struct MapKey {
+  const void* base;
+  int kind, esize, rank, swz;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], trav[5];
+  int lower[2], upper[2];
+  cuuint32_t chans, pixels;
+};
+
+struct MapMemo {
+  std::unordered_map<std::string, CUtensorMap> maps;
+  static std::string key(const MapKey& k) {
+    return std::string(reinterpret_cast<const char*>(&k), sizeof k);
+  }
+  const CUtensorMap* find(const MapKey& k) const {
+    auto it = maps.find(key(k));
+    return it == maps.end() ? nullptr : &it->second;
+  }
+  void put(const MapKey& k, const CUtensorMap& m) {
+    if (maps.size() >= 4096) maps.clear();
+    maps.emplace(key(k), m);
+  }
+};
+
+MapMemo& map_memo() {
+  thread_local MapMemo memo;
+  return memo;
+}
+
 // esize: 4 (fp32 / tf32) or 2 (bf16).  dims[0] is the contiguous K axis.
 CUtensorMap make_map(const void* base, int esize, int rank, const cuuint64_t* dims,
                      const cuuint64_t* strides, const cuuint32_t* box,
                      const cuuint32_t* traversal = nullptr,
                      CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  MapKey key;
+  std::memset(&key, 0, sizeof key);
+  key.base = base;
+  key.kind = 0;
+  key.esize = esize;
+  key.rank = rank;
+  key.swz = (int)swz;
+  for (int i = 0; i < rank; ++i) {
+    key.dims[i] = dims[i];
+    key.box[i] = box[i];
+    key.trav[i] = traversal ? traversal[i] : 1;
+    if (i + 1 < rank) key.strides[i] = strides[i];
+  }
+  if (const CUtensorMap* hit = map_memo().find(key)) return *hit;
   CUtensorMap m;
   cuuint32_t elem_strides[5] = {1, 1, 1, 1, 1};
   if (traversal)
@@ -950,6 +999,7 @@ CUtensorMap make_map(const void* base, int esize, int rank, const cuuint64_t* di
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     fail(TK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  map_memo().put(key, m);
   return m;
 }
 
@@ -1021,6 +1071,24 @@ CUtensorMap map_nhwc_im2col(const void* base, int esize, const ConvGeom& g, int 
   const int lower[2] = {-g.pad_l, -g.pad_t};
   const int upper[2] = {pad_r - (g.S - 1), pad_b - (g.R - 1)};
   const cuuint32_t trav[4] = {1, (cuuint32_t)g.stride, (cuuint32_t)g.stride, 1};
+  MapKey key;
+  std::memset(&key, 0, sizeof key);
+  key.base = base;
+  key.kind = 1;
+  key.esize = esize;
+  key.rank = 4;
+  for (int i = 0; i < 4; ++i) {
+    key.dims[i] = dims[i];
+    key.trav[i] = trav[i];
+    if (i < 3) key.strides[i] = strides[i];
+  }
+  key.lower[0] = lower[0];
+  key.lower[1] = lower[1];
+  key.upper[0] = upper[0];
+  key.upper[1] = upper[1];
+  key.chans = (cuuint32_t)(kSlabBytes / esize);
+  key.pixels = (cuuint32_t)pixels;
+  if (const CUtensorMap* hit = map_memo().find(key)) return *hit;
   CUtensorMap m;
   const CUresult r = encode_im2col_fn()(
       &m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
@@ -1031,10 +1099,13 @@ CUtensorMap map_nhwc_im2col(const void* base, int esize, const ConvGeom& g, int 
     fail(TK_ERR_CUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string(r) + ")");
   // Same driver workaround as CUTLASS's im2col descriptors (drivers <= 13.1,
   // tensors under 128 KiB): clear bit 21 of the second descriptor word.
-  int drv = 0;
-  if (cudaDriverGetVersion(&drv) == cudaSuccess && drv <= 13010 &&
-      (size_t)g.N * g.H * g.W * g.C * esize < 131072)
+  static const int drv = [] {
+    int v = 0;
+    return cudaDriverGetVersion(&v) == cudaSuccess ? v : 0;
+  }();
+  if (drv > 0 && drv <= 13010 && (size_t)g.N * g.H * g.W * g.C * esize < 131072)
     reinterpret_cast<uint64_t*>(&m)[1] &= ~(1ull << 21);
+  map_memo().put(key, m);
   return m;
 }
 
@@ -1157,10 +1228,13 @@ struct TailPlan {
 
 // Per-slab time of an SM pair (us): max(MMA, operand feed) -- the constants
 // of choose_splits.
+// A slab is 128 bytes of K (32 tf32 / 64 bf16: the same tensor-core time);
+// each SM of the group does 2 * (bm / cg) * bn * 32 tf32-equivalent flops
+// and stages (bm + bn) / cg operand rows of 128 bytes at ~70 B/clk.
 inline double slab_time_us(int cg, int bn) {
   const int bm = kRows * cg;
-  const double mma_clk = 4.0 * (double)bm * bn * 8 / kTcFlopPerClk;
-  const double feed_clk = (double)(bm / 2 + bn / 2) * 128 / 70.0;
+  const double mma_clk = 64.0 * (double)bm * bn / (cg * kTcFlopPerClk);
+  const double feed_clk = (double)(bm + bn) / cg * 128 / 70.0;
   return std::max(mma_clk, feed_clk) / 1900.0;
 }
 
@@ -1265,8 +1339,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   const size_t smem =
       1024 + (size_t)stages * stage_bytes + fres_bytes + 1024 + epi_bytes + ktab_bytes;
   auto fn = tc_gemm_kernel<MODE, CG, TF32>;
-  TKB_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  func_smem((const void*)fn, smem);
   {
     const int forced = xp.tc_acc;
     p.acc_slots = p.BN <= 64 ? 8 : (p.BN <= 128 ? 4 : 2);
@@ -1855,6 +1928,32 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
   int cg = g.M > kRows ? 2 : 1;
   if (tc_knobs().cluster == 1 || tc_knobs().cluster == 2) cg = tc_knobs().cluster;
   int bn = g.tile_n > 0 ? g.tile_n : (g.N >= 256 ? 256 : ((g.N + 15) / 16) * 16);
+  if (g.tile_n <= 0 && g.N >= 64) {
+    // Library tile for a GEMM too small to fill the SMs with 256 x 256
+    // tiles: the (cluster, N tile) whose modelled time (waves of
+    // max(MMA, operand feed) per slab + the stream-K tail) is least.
+    const int num_kb = (g.K + ek - 1) / ek;
+    double best = 1e30;
+    for (int c : {2, 1}) {
+      if (tc_knobs().cluster != 0 && c != tc_knobs().cluster) continue;
+      if (c == 2 && g.M <= kRows) continue;
+      for (int b : {256, 128, 64}) {
+        if (b > 64 && b >= 2 * g.N) continue;
+        const long long tiles = (long long)((g.M + kRows * c - 1) / (kRows * c)) *
+                                ((g.N + b - 1) / b) * g.batch;
+        // Candidates in order of preference (SM pairs, wide tiles: the
+        // measured winners whenever the SMs fill); a later one must beat
+        // the model by 15% (4096^3: the model ties cg1/cg2, hardware
+        // prefers the pair, 199 vs 225 us).
+        const double t = plan_tail(tiles, num_kb, c, b).cost_us;
+        if (t < best * 0.85) {
+          best = t;
+          cg = c;
+          bn = b;
+        }
+      }
+    }
+  }
   if (bn > 256) bn = 256;
   const int step = 16 * cg;
   bn = (bn + step - 1) / step * step;
@@ -1905,16 +2004,11 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
     p.store_tma = 1;
     p.epi_bufs = 2;
   }
-  void* tail_buf = nullptr;
-  if (!p.read_c) {
-    const TailPlan tp = plan_tail((long long)p.num_m * p.num_n * p.batch, p.num_kb, cg, bn);
-    if (tp.q > 1) {
-      TKB_CUDA(cudaMallocAsync(&tail_buf, tp.bytes, st));
-      apply_tail(p, tp, static_cast<float*>(tail_buf));
-    }
-  }
+  const TailPlan tp = p.read_c ? TailPlan{}
+                               : plan_tail((long long)p.num_m * p.num_n * p.batch, p.num_kb, cg, bn);
+  Scratch tail_buf(st, kScratchTail, tp.q > 1 ? tp.bytes : 0);
+  if (tp.q > 1) apply_tail(p, tp, tail_buf.as<float>());
   dispatch<kPlain>(ma, mb, md, p, cg, tf32, st);
-  if (tail_buf) cudaFreeAsync(tail_buf, st);
 }
 
 void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float beta, bool ta,
@@ -1925,11 +2019,9 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
     // Pack both operands K-major (fp32, unrounded), expand to the split
     // triple along K, run one TF32 GEMM of depth 3 kp.
     const long long kp = (long long)((k + 3) / 4 * 4);
-    float *pa = nullptr, *pb = nullptr, *a3 = nullptr, *b3 = nullptr;
-    TKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pa), (size_t)m * kp * 4, st));
-    TKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pb), (size_t)n * kp * 4, st));
-    TKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a3), (size_t)m * kp * 12, st));
-    TKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b3), (size_t)n * kp * 12, st));
+    Scratch spa(st, kScratchPackA, (size_t)m * kp * 4), spb(st, kScratchPackB, (size_t)n * kp * 4);
+    Scratch sa3(st, kScratchSplitA, (size_t)m * kp * 12), sb3(st, kScratchSplitB, (size_t)n * kp * 12);
+    float *pa = spa.as<float>(), *pb = spb.as<float>(), *a3 = sa3.as<float>(), *b3 = sb3.as<float>();
     if (ta) pack_kmajor<float>(a, (long long)k, 1, (long long)m, (long long)k, kp, pa, false, st);
     else pack_kmajor<float>(a, 1, (long long)m, (long long)m, (long long)k, kp, pa, false, st);
     if (tb) pack_kmajor<float>(b, 1, (long long)n, (long long)n, (long long)k, kp, pb, false, st);
@@ -1951,7 +2043,6 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
     g.precision = TK_PREC_TF32;
     g.tile_n = tile_n;
     launch_tc_gemm(g, st);
-    for (float* q : {pa, pb, a3, b3}) cudaFreeAsync(q, st);
     return;
   }
   const bool tf32 = precision == TK_PREC_TF32;
@@ -1966,10 +2057,10 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
   const bool mn_on = experiments().a_mn;
   const bool a_mn = mn_on && tf32 && !ta && m % 32 == 0 && aligned(a) && m <= (1ull << 31);
   const size_t esz = tf32 ? 4 : 2;
-  void* pa = nullptr;
-  void* pb = nullptr;
-  if (!a_ok && !a_mn) TKB_CUDA(cudaMallocAsync(&pa, (size_t)m * kp * esz, st));
-  if (!b_ok) TKB_CUDA(cudaMallocAsync(&pb, (size_t)n * kp * esz, st));
+  Scratch spa(st, kScratchPackA, (!a_ok && !a_mn) ? (size_t)m * kp * esz : 0);
+  Scratch spb(st, kScratchPackB, !b_ok ? (size_t)n * kp * esz : 0);
+  void* pa = spa.get();
+  void* pb = spb.get();
   auto pack = [&](const float* src, long long rs, long long ks, long long rows, void* dst) {
     if (tf32) pack_kmajor<float>(src, rs, ks, rows, (long long)k, kp, (float*)dst, false, st);
     else pack_kmajor<__nv_bfloat16>(src, rs, ks, rows, (long long)k, kp, (__nv_bfloat16*)dst, false, st);
@@ -2000,8 +2091,6 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
   g.precision = precision;
   g.tile_n = tile_n;
   launch_tc_gemm(g, st);
-  if (pa) cudaFreeAsync(pa, st);
-  if (pb) cudaFreeAsync(pb, st);
 }
 
 namespace {
@@ -2061,9 +2150,7 @@ int choose_splits(long long units, int num_kb, long long pairs, int bm, int bn,
     while (sp > 1 && (size_t)sp * out_bytes > cap) --sp;
     return sp;
   }
-  const double mma_clk = 4.0 * (double)bm * bn * 8 / kTcFlopPerClk;      // per slab, per pair
-  const double feed_clk = (double)(bm / 2 + bn / 2) * 128 / 70.0;  // bytes per SM / (B/clk)
-  const double slab_us = std::max(mma_clk, feed_clk) / 1900.0;
+  const double slab_us = slab_time_us(bm / kRows, bn);
   auto cost = [&](int s) {
     const long long waves = (units * s + pairs - 1) / pairs;
     const int kb = (num_kb + s - 1) / s;
