@@ -96,6 +96,20 @@ def plan_str(tk, shape, algo, prec):
     return s
 
 
+def bound_frac(flops, nbytes, ms, peak_tf, hbm_gbs):
+    """Roofline verdict of one layer: HBM-bound when its operational
+    intensity (conv_flops / compulsory fp32 bytes) is under the ridge
+    peak / HBM; the fraction is then achieved GB/s over HBM, else achieved
+    TF/s over the tensor (or FP32) peak."""
+    oi = flops / nbytes
+    ridge = peak_tf * 1e12 / (hbm_gbs * 1e9)
+    if oi < ridge:
+        return {"bound": "hbm", "oi": round(oi, 1),
+                "frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm_gbs, 3)}
+    return {"bound": "tensor", "oi": round(oi, 1),
+            "frac": round(flops / (ms * 1e-3) / 1e12 / peak_tf, 3)}
+
+
 def conv_flops(n, h, c, k):
     return 2 * n * h * h * k * 9 * c
 
@@ -682,9 +696,11 @@ def main():
 
     layer_rows = []
     for L, ms, kms in zip(layers, step_layer, per_layer):
-        layer_rows.append({"layer": L["name"], "ms": round(ms, 4), "kernel_ms": round(kms, 4),
-                           "tflops": round(L["flops"] / (ms * 1e-3) / 1e12, 2),
-                           "plan": plan_str(tk, L["shape"], L["algo"], prec)})
+        nbytes = 4 * (L["x"].numel() + L["f"].numel() + L["y"].numel())
+        layer_rows.append(dict({"layer": L["name"], "ms": round(ms, 4), "kernel_ms": round(kms, 4),
+                                "tflops": round(L["flops"] / (ms * 1e-3) / 1e12, 2),
+                                "plan": plan_str(tk, L["shape"], L["algo"], prec)},
+                               **bound_frac(L["flops"], nbytes, ms, peak_tf, peaks["hbm_gbs"])))
 
     peaks, peaks_kind = load_peaks()
     # Secondary lines (same run, same resident inputs): the other precisions
@@ -828,11 +844,33 @@ def main():
                     k0 += mult
                     kms = kernel_ms(lambda st, shp=shp, x=x, f=f, y=y, ws0=ws0: tk.conv2d_run_dev(
                         x, f, y, shp, im2col, ws0, precision=p_, stream=st))
-                    rows.append({"layer": name, "ms": round(kms, 4),
-                                 "tflops": round(fl / (kms * 1e-3) / 1e12, 1),
-                                 "frac_of_peak": round(fl / (kms * 1e-3) / 1e12 / pk, 3),
-                                 "plan": plan_str(tk, shp, im2col, p_)})
+                    nbytes = 4 * (x.numel() + f.numel() + y.numel())
+                    rows.append(dict({"layer": name, "ms": round(kms, 4),
+                                      "tflops": round(fl / (kms * 1e-3) / 1e12, 1),
+                                      "frac_of_peak": round(fl / (kms * 1e-3) / 1e12 / pk, 3),
+                                      "plan": plan_str(tk, shp, im2col, p_)},
+                                     **bound_frac(fl, nbytes, kms, pk, peaks["hbm_gbs"])))
                 secondary[f"resnet50_{p_}"]["layers"] = rows
+        # configs[2]'s "tiled path": the whole 53-layer stack through the
+        # exact FP32 tiled algorithm (bit-identical to the reference).
+        tiled = tk.parse_conv_params("tiled_t4x5_v4x2")
+
+        def rn_tiled(st_):
+            for shp, x, f, y, ws, mult, _fl in rn:
+                for _ in range(mult):
+                    tk.conv2d_dev(x, f, y, shp, tiled, precision="fp32", stream=st_)
+        rn_tiled(stream)
+        torch.cuda.synchronize()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        a_.record(stream)
+        rn_tiled(stream)
+        b_.record(stream)
+        b_.synchronize()
+        ms = a_.elapsed_time(b_)
+        secondary["resnet50_tiled_fp32"] = {"value": round(rn_flops / (ms * 1e-3) / 1e9, 1),
+                                            "unit": "GFLOP/s", "ms_per_step": round(ms, 3),
+                                            "algorithm": "tiled_t4x5_v4x2", "bit_exact": True}
         del rn
         # BASELINE configs[1]'s algorithm comparison: every distinct VGG16
         # layer at batch 32 through each conv algorithm of the selector
@@ -843,15 +881,18 @@ def main():
         # included, as the reference's conv2d does) from a graph, L2-cold,
         # launch latency removed as for the layers.  GFLOP/s count the
         # direct-equivalent conv_flops for every algorithm (tuner.hpp:442).
-        if not args.no_graph:
-            algos = [("tiled_fp32", "tiled_t4x5_v4x2", "fp32"), ("im2col_tf32", "im2col", "tf32"),
+        # Batch 1 too (configs[1] names "batch 1 and 32"): there the layers
+        # are latency-bound small grids.
+        for nb in ((N, 1) if not args.no_graph else ()):
+            algos = [("naive_fp32", "naive", "fp32"), ("tiled_fp32", "tiled_t4x5_v4x2", "fp32"),
+                     ("im2col_tf32", "im2col", "tf32"), ("im2col_bf16", "im2col", "bf16"),
                      ("winograd_t2x2_tf32", "winograd_t2x2", "tf32"),
                      ("winograd_t4x4_tf32", "winograd_t4x4", "tf32"),
                      ("winograd_t2x2_fp32", "winograd_t2x2", "fp32")]
             table = {}
             for name, h, c, k, _mult in VGG16:
-                shp = tk.ConvShape(N, h, h, c, k, 3, 3, 1, True)
-                x = torch.rand((N, h, h, c), device=dev, generator=gen) * 2 - 1
+                shp = tk.ConvShape(nb, h, h, c, k, 3, 3, 1, True)
+                x = torch.rand((nb, h, h, c), device=dev, generator=gen) * 2 - 1
                 f = torch.rand((3, 3, c, k), device=dev, generator=gen) * 2 - 1
                 y = torch.empty(shp.out_shape, device=dev)
                 row = {}
@@ -872,7 +913,7 @@ def main():
                     del ws
                 table[name] = row
                 del x, f, y
-            secondary["vgg16_algorithms_b32"] = table
+            secondary[f"vgg16_algorithms_b{nb}"] = table
         # BASELINE configs[3]: large square GEMMs on the tensor cores
         # (column-major nn through tk_gemm_dev; operands in HBM, > L2 from 4096).
         for n in (2048, 4096, 8192):
@@ -917,9 +958,32 @@ def main():
                 b_.synchronize()
                 ts.append(a_.elapsed_time(b_))
             ms = float(np.median(ts))
-            secondary[f"sgemm1024_{p_}"] = {"value": round(2 * n ** 3 / (ms * 1e-3) / 1e9, 1),
-                                             "unit": "GFLOP/s", "ms": round(ms, 4),
-                                             "note": "L2-resident operands (12.6 MB)"}
+            # Device time without host work: 20 calls captured in a graph.
+            cap = torch.cuda.Stream(device=dev)
+            cap.wait_stream(stream)
+            gg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gg, stream=cap):
+                for _ in range(20):
+                    tk.gemm_dev(gb, ga, None, gc, gshape, cfg, precision=p_, stream=cap)
+            gg.replay()
+            torch.cuda.synchronize()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            gg.replay()
+            b_.record(stream)
+            b_.synchronize()
+            dms = a_.elapsed_time(b_) / 20
+            del gg
+            pk = {"fp32": 148 * 128 * 1.965e9 / 1e12, "tf32": peaks["bf16_tflops"] / 2.0,
+                  "bf16": peaks["bf16_tflops"]}[p_]
+            secondary[f"sgemm1024_{p_}"] = {
+                "value": round(2 * n ** 3 / (dms * 1e-3) / 1e9, 1), "unit": "GFLOP/s",
+                "ms": round(dms, 4), "frac_of_peak": round(2 * n ** 3 / (dms * 1e-3) / 1e12 / pk, 4),
+                "api_ms": round(ms, 4),
+                "api_gflops": round(2 * n ** 3 / (ms * 1e-3) / 1e9, 1),
+                "note": "value/ms: device time (graph of 20 calls); api_*: one tk_gemm_dev call "
+                        "between events (host work included); L2-resident operands (12.6 MB); "
+                        "fp32 peak = FMUL+FADD issue cap 37.2 TF/s"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -956,6 +1020,21 @@ def main():
             "multi_gpu": multi,
             "secondary": secondary,
         }
+        # Compact digest LAST in the line (a log tail shows it whole).
+        summ = {"vgg16_" + prec + "_gflops": round(value, 1), "e2e_gflops": e2e and e2e["value"],
+                "roofline_frac": roofline["frac"]}
+        for key in ("vgg16_tf32", "vgg16_bf16", "vgg16_3xtf32", "vgg16_fp32", "resnet50_tf32",
+                    "resnet50_bf16", "resnet50_tiled_fp32", "sgemm1024_fp32", "sgemm1024_tf32",
+                    "sgemm1024_bf16", "gemm4096_tf32", "gemm4096_bf16", "gemm8192_tf32",
+                    "gemm8192_bf16"):
+            if key in secondary:
+                v = secondary[key]
+                summ[key] = {"gflops": v["value"], "ms": v.get("ms_per_step", v.get("ms"))}
+        if "gemm8192_tf32_panels" in multi:
+            summ["gemm8192_tf32_panels_gflops"] = multi["gemm8192_tf32_panels"]["value"]
+        if "verify" in multi:
+            summ["shards_verified"] = multi["verify"]["shards_bitwise_equal_to_recompute"]
+        line["summary"] = summ
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
