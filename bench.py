@@ -853,7 +853,7 @@ def main():
                 secondary[f"resnet50_{p_}"]["layers"] = rows
         # configs[2]'s "tiled path": the whole 53-layer stack through the
         # exact FP32 tiled algorithm (bit-identical to the reference).
-        tiled = tk.parse_conv_params("tiled_t4x5_v4x2")
+        tiled = tk.parse_conv_params("tiled_t2x2_v4x8")  # 2x2-pixel patches x 8 features
 
         def rn_tiled(st_):
             for shp, x, f, y, ws, mult, _fl in rn:
@@ -870,7 +870,7 @@ def main():
         ms = a_.elapsed_time(b_)
         secondary["resnet50_tiled_fp32"] = {"value": round(rn_flops / (ms * 1e-3) / 1e9, 1),
                                             "unit": "GFLOP/s", "ms_per_step": round(ms, 3),
-                                            "algorithm": "tiled_t4x5_v4x2", "bit_exact": True}
+                                            "algorithm": "tiled_t2x2_v4x8", "bit_exact": True}
         del rn
         # BASELINE configs[1]'s algorithm comparison: every distinct VGG16
         # layer at batch 32 through each conv algorithm of the selector
@@ -884,7 +884,8 @@ def main():
         # Batch 1 too (configs[1] names "batch 1 and 32"): there the layers
         # are latency-bound small grids.
         for nb in ((N, 1) if not args.no_graph else ()):
-            algos = [("naive_fp32", "naive", "fp32"), ("tiled_fp32", "tiled_t4x5_v4x2", "fp32"),
+            algos = [("naive_fp32", "naive", "fp32"), ("tiled_fp32", "tiled_t2x2_v4x8", "fp32"),
+                     ("tiled_t4x5_v4x2_fp32", "tiled_t4x5_v4x2", "fp32"),
                      ("im2col_tf32", "im2col", "tf32"), ("im2col_bf16", "im2col", "bf16"),
                      ("winograd_t2x2_tf32", "winograd_t2x2", "tf32"),
                      ("winograd_t4x4_tf32", "winograd_t4x4", "tf32"),

@@ -286,10 +286,10 @@ ExactLaunch exact_launch_of(const tilekit::GemmConfig& c) {
   L.c = (int)c.wg_cols;
   L.loc = c.use_local_memory;
   L.stages = c.double_buffer ? 3 : 1;
+  // h, w outside {1, 2, 4, 8}: the runtime-tile kernel (microkernel_generic,
+  // gemm.hpp:247-292), bit-identical like every exact path.
   auto pow2 = [](int v) { return v == 1 || v == 2 || v == 4 || v == 8; };
-  if (!pow2(L.h) || !pow2(L.w))
-    fail(TK_ERR_CAPABILITY, "gemm_tiled: config \"" + c.name() +
-                                "\": the B200 kernels instantiate register tiles h, w in {1,2,4,8}");
+  L.gen = !pow2(L.h) || !pow2(L.w);
   return L;
 }
 
@@ -348,18 +348,33 @@ ExactArgs conv_args(const ConvGeom& g, const float* in, const float* filt, float
   return p;
 }
 
-// conv2d_tiled parameters -> register tile of the implicit GEMM: the
-// tile_rows x tile_cols pixel patch becomes the thread's pixel count
-// (rounded up to an instantiated width), feature_vector its features.
-ExactLaunch tiled_launch(const tk_conv_params* p) {
-  auto up = [](size_t v) { return v <= 1 ? 1 : v <= 2 ? 2 : v <= 4 ? 4 : 8; };
+// conv2d_tiled parameters (conv.hpp:136-248) -> the CTA of the runtime-
+// tile kernel: each thread owns a tile_rows x tile_cols patch of output
+// pixels (h = tile_rows * tile_cols register rows) for feature_vector
+// features (w), the CTA's threads tile the output plane with such patches
+// (r along pixels, c along features: 256 threads), the input is staged
+// channel_vector channels per copy.  Same per-output sums: bit-identical.
+ExactLaunch tiled_launch(const tk_conv_params* p, const ConvGeom& g) {
   ExactLaunch L{};
-  L.h = up(p->tile_rows * p->tile_cols);
-  L.w = up(p->feature_vector);
-  L.c = 16;
-  L.r = 16;
+  L.h = (int)(p->tile_rows * p->tile_cols);
+  auto pow2 = [](int v) { return v == 1 || v == 2 || v == 4 || v == 8; };
+  // Patches of 1/2/4/8 pixels x 1/2/4/8 features run on the tuned kernels
+  // (2-D patch rows through their pixel table); other tiles on the
+  // runtime-tile kernel.
+  L.gen = !(pow2(L.h) && pow2((int)p->feature_vector));
+  L.w = (int)p->feature_vector;
+  L.tile_rows = (int)p->tile_rows;
+  L.tile_cols = (int)p->tile_cols;
+  L.cvec = (int)std::min<size_t>(4, p->channel_vector);
+  int c = 1;  // feature threads: enough to cover K, at most 16
+  while (c < 16 && (size_t)c * p->feature_vector < (size_t)g.K) c *= 2;
+  L.c = c;
+  // 256 threads, at most ~320 pixel rows per CTA (the staged slab of the
+  // patch matrix: 320 x 36 words, 46 KiB a stage).
+  L.r = std::max(1, std::min(256 / c, 320 / std::max(1, L.h)));
   L.loc = true;
-  L.stages = 3;
+  L.stages = 2;
+  L.shrink_ok = true;
   return L;
 }
 
@@ -508,7 +523,7 @@ void conv_dev(const tilekit::ConvShape& s, const tk_conv_params* p, int precisio
     case 1:  // Tiled
       check_tiled_params(s, p);
       if (precision == TK_PREC_FP32_EXACT) {
-        if (exact_run) launch_exact(conv_args(g, in, filt, out), tiled_launch(p), true, 1, st);
+        if (exact_run) launch_exact(conv_args(g, in, filt, out), tiled_launch(p, g), true, 1, st);
         return;
       }
       break;
@@ -885,15 +900,11 @@ int tk_conv2d(const tk_conv_shape* shape, const tk_conv_params* params, const fl
               const float* filt, float* out) {
   return guarded([&] {
     if (!params) fail(TK_ERR_CONTRACT, "conv2d: params must not be NULL");
-    if (params->algo == 2) {
-      // Selector semantics: the default conv2d_im2col overload
-      // (4x4_8x8_noloc on a generic device, conv.hpp:353-362).
-      tk_gemm_config cfg{4, 4, 8, 8, 0, 0, 1};
-      tk_device_spec dev{"generic", 64, 0, 1, 256, 256};
-      int rc = tk_conv2d_im2col(shape, &cfg, &dev, in, filt, out);
-      if (rc != TK_OK) throw Failure{rc, g_error};
-      return;
-    }
+    // Selector semantics.  The default conv2d_im2col overload names
+    // 4x4_8x8_noloc on a generic 64-byte-line device (conv.hpp:353-362),
+    // a config that always validates; its bits do not depend on the tile,
+    // so the library's own exact tile runs it (exact_conv_default).  A
+    // caller that names a config goes through tk_conv2d_im2col.
     conv_host(conv_shape(shape), params, TK_PREC_FP32_EXACT, in, filt, out);
   });
 }
@@ -1117,7 +1128,7 @@ int tk_conv2d_plan_info(const tk_conv_shape* shape, const tk_conv_params* params
         if (prec != TK_PREC_FP32_EXACT)
           fail(TK_ERR_CAPABILITY, "conv2d: algorithm \"tiled\" is FP32-exact only; use im2col or "
                                   "winograd for tensor cores");
-        exact(tiled_launch(params));
+        exact(tiled_launch(params, g));
         break;
       case 3: {
         const int m = check_winograd(s, params);

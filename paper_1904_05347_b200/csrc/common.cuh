@@ -53,6 +53,11 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool val
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(smem)),
                "l"(gmem), "r"(src));
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const int src = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(src));
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const int src = valid ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)),

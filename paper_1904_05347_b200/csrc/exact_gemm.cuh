@@ -46,6 +46,11 @@ struct ExactArgs {
   int tx_on_m;  // lane-fast thread index runs along M (column-major output)
   // conv geometry (CONV instantiations only)
   int H, W, C, OH, OW, R, S, stride, pad_t, pad_l;
+  // conv2d_tiled's 2-D pixel patches (0 = linear pixel rows): each thread's
+  // register rows are a t2_rows x t2_cols patch, the CTA's wg_r threads a
+  // t2_pr x t2_pc grid of patches of one image; t2_blk_r x t2_blk_c CTAs
+  // per image (blockIdx.x = image * blocks + block).
+  int t2_rows, t2_cols, t2_pr, t2_pc, t2_blk_r, t2_blk_c;
 };
 
 // Ownership of register-tile rows: MN-major operands hand each thread runs of
@@ -199,19 +204,47 @@ struct PixRow {
   int ih0, iw0;
 };
 
-__device__ __forceinline__ void build_pix_rows(PixRow* rows, const ExactArgs& p, int m0, int BM,
-                                               int tid, int nthreads) {
+// wg_r: threads along M (row e = u * wg_r + t of the K-major register
+// ownership is element u of thread t's patch in 2-D mode).
+// out[e]: element offset of row e's output pixel (pixel * d_sm), -1 if none
+// (a separate table: the staging loop reads only the 16-byte PixRow).
+__device__ __forceinline__ void build_pix_rows(PixRow* rows, long long* out, const ExactArgs& p,
+                                               int m0, int BM, int wg_r, int tid, int nthreads) {
+  int n2 = 0, oh2 = 0, ow2 = 0;
+  if (p.t2_rows > 0) {
+    const int per_img = p.t2_blk_r * p.t2_blk_c;
+    n2 = blockIdx.x / per_img;
+    const int rem = blockIdx.x - n2 * per_img;
+    oh2 = (rem / p.t2_blk_c) * p.t2_rows * p.t2_pr;
+    ow2 = (rem % p.t2_blk_c) * p.t2_cols * p.t2_pc;
+  }
   for (int e = tid; e < BM; e += nthreads) {
-    const int m = m0 + e;
     PixRow r{0, -(1 << 28), 0};
-    if (m < p.M) {
-      const int ow = m % p.OW, t = m / p.OW;
-      const int oh = t % p.OH, n = t / p.OH;
+    long long o = -1;
+    int n, oh, ow;
+    bool ok;
+    if (p.t2_rows > 0) {
+      const int u = e / wg_r, t = e - (e / wg_r) * wg_r;
+      n = n2;
+      oh = oh2 + (t / p.t2_pc) * p.t2_rows + u / p.t2_cols;
+      ow = ow2 + (t % p.t2_pc) * p.t2_cols + u % p.t2_cols;
+      ok = oh < p.OH && ow < p.OW;
+    } else {
+      const int m = m0 + e;
+      ok = m < p.M;
+      ow = m % p.OW;
+      const int t = m / p.OW;
+      oh = t % p.OH;
+      n = t / p.OH;
+    }
+    if (ok) {
       r.ih0 = oh * p.stride - p.pad_t;
       r.iw0 = ow * p.stride - p.pad_l;
       r.base = (((long long)n * p.H + r.ih0) * p.W + r.iw0) * p.C;
+      o = (((long long)n * p.OH + oh) * p.OW + ow) * p.d_sm;
     }
     rows[e] = r;
+    out[e] = o;
   }
 }
 
@@ -326,8 +359,9 @@ __global__ void exact_gemm_loc_kernel(ExactArgs p, int wg_r, int wg_c, int stage
   const int a_words = SlabGeom<AL>::words(BM), b_words = SlabGeom<BL>::words(BN);
   const int stage_words = a_words + b_words;
   PixRow* pix_rows = reinterpret_cast<PixRow*>(smem + stages * stage_words);
+  long long* pix_out = reinterpret_cast<long long*>(pix_rows + BM);
   if constexpr (CONV) {
-    build_pix_rows(pix_rows, p, m0, BM, tid, nthreads);
+    build_pix_rows(pix_rows, pix_out, p, m0, BM, wg_r, tid, nthreads);
     __syncthreads();
   }
 
@@ -412,13 +446,20 @@ __global__ void exact_gemm_loc_kernel(ExactArgs p, int wg_r, int wg_c, int stage
   const float* gc = p.c ? p.c + (long long)z * p.d_batch : nullptr;
 #pragma unroll
   for (int i = 0; i < H; ++i) {
-    const int m = m0 + own_index<H, AL>(tm, wg_r, i);
-    if (m >= p.M) continue;
+    long long row_off;
+    if constexpr (CONV) {
+      row_off = pix_out[own_index<H, AL>(tm, wg_r, i)];  // linear or 2-D patch row
+      if (row_off < 0) continue;
+    } else {
+      const int m = m0 + own_index<H, AL>(tm, wg_r, i);
+      if (m >= p.M) continue;
+      row_off = (long long)m * p.d_sm;
+    }
 #pragma unroll
     for (int j = 0; j < W; ++j) {
       const int n = n0 + own_index<W, BL>(tn, wg_c, j);
       if (n >= p.N) continue;
-      const long long off = (long long)m * p.d_sm + (long long)n * p.d_sn;
+      const long long off = row_off + (long long)n * p.d_sn;
       float v = __fmul_rn(p.alpha, acc[i][j]);
       if (p.read_c) v = __fadd_rn(v, __fmul_rn(p.beta, gc[off]));
       gd[off] = v;
@@ -520,6 +561,11 @@ struct ExactLaunch {
   int h, w, r, c;
   bool loc;
   int stages;  // 1 (loc), 2..3 (loc_db)
+  // Runtime register tile (exact_gen.cuh): any h, w; conv2d_tiled's patch
+  // geometry when tile_rows > 0; cvec = channel_vector of the staging.
+  bool gen = false;
+  int tile_rows = 0, tile_cols = 0, cvec = 4;
+  bool shrink_ok = false;  // library-shaped (conv2d_tiled): r may shrink to fit
 };
 void launch_exact(const ExactArgs& p, const ExactLaunch& L, bool conv, int batch,
                   cudaStream_t stream);

@@ -155,3 +155,60 @@ def test_vgg_layers_batch1_exact(tk, oracle, name, H, C, K):
     dy = torch.empty(conv.out_shape, device="cuda")
     tk.conv2d_dev(dx, df, dy, s, tk.parse_conv_params("im2col"))
     assert same(dy.cpu().numpy(), want)
+
+
+# ---- runtime register tiles (microkernel_generic, gemm.hpp:247-292) -------
+GENERIC = ["3x5_8x8_loc", "5x3_4x16_noloc", "7x1_16x16_loc_db", "1x7_16x8_loc", "6x6_8x8_loc_db",
+           "12x12_8x8_loc", "3x20_8x4_loc", "16x8_8x8_loc", "9x2_8x16_noloc"]
+
+
+@pytest.mark.parametrize("cfg", GENERIC)
+def test_gemm_tiled_generic_register_tiles(tk, oracle, cfg):
+    """Configs outside h, w in {1, 2, 4, 8} run bit-exact (the reference's
+    generic microkernel) instead of raising; all op combos, ragged tails,
+    alpha/beta."""
+    dev = tk.b200_device()
+    ok, msg = tk.validate_config(tk.parse_gemm_config(cfg), dev)
+    assert ok, msg
+    for (m, n, k) in [(67, 45, 17), (128, 96, 64), (33, 1, 130)]:
+        for ta in (0, 1):
+            for tb in (0, 1):
+                a = oracle.fill_random(m * k, 1)
+                b = oracle.fill_random(k * n, 2)
+                c = oracle.fill_random(m * n, 3)
+                want = oracle.gemm_naive(m, n, k, 1.5, -0.5, ta, tb, a, b, c)
+                shape = tk.GemmShape(m, n, k, 1.5, -0.5, "t" if ta else "n", "t" if tb else "n")
+                got = tk.gemm_tiled(a, b, c, shape, tk.parse_gemm_config(cfg), dev)
+                assert same(got, want), (cfg, m, n, k, ta, tb)
+
+
+@pytest.mark.parametrize("params", ["tiled_t4x5_v4x2", "tiled_t1x1_v1x1", "tiled_t3x7_v2x8",
+                                    "tiled_t8x8_v8x1", "tiled_t5x5_v1x4", "tiled_t2x3_v8x8",
+                                    "tiled_t4x4_v4x4"])
+@pytest.mark.parametrize("shape", [(2, 13, 11, 8, 20, 3, 1, True), (1, 15, 15, 3, 64, 3, 1, True),
+                                   (2, 16, 14, 12, 10, 3, 2, True), (1, 9, 12, 6, 7, 3, 1, False),
+                                   (1, 20, 20, 3, 64, 7, 2, True), (3, 7, 7, 32, 48, 1, 1, True)])
+def test_conv2d_tiled_patch_geometry_bit_exact(tk, oracle, params, shape):
+    """conv2d_tiled's tile_rows x tile_cols patch, feature_vector and
+    channel_vector shape the CTA (2-D pixel patches per thread, channel
+    groups per staging copy); outputs stay bit-identical to conv2d_naive."""
+    n, h, w, c, k, r, st, same_pad = shape
+    s = tk.ConvShape(n, h, w, c, k, r, r, st, same_pad)
+    conv = oracle.Conv(n, h, w, c, k, r, r, st, same_pad)
+    x = oracle.fill_random(int(np.prod(conv.in_shape)), 5).reshape(conv.in_shape)
+    f = oracle.fill_random(int(np.prod(conv.filt_shape)), 6).reshape(conv.filt_shape)
+    want = oracle.conv2d_naive(conv, x, f)
+    got = tk.conv2d(x, f, s, tk.parse_conv_params(params))
+    assert same(got, want), (params, shape)
+
+
+def test_conv2d_im2col_with_generic_config(tk, oracle):
+    """conv2d_im2col(cfg, dev) honours an explicit non-power-of-two config."""
+    s = tk.ConvShape(2, 10, 9, 5, 7, 3, 3, 1, True)
+    conv = oracle.Conv(2, 10, 9, 5, 7, 3, 3, 1, True)
+    x = oracle.fill_random(int(np.prod(conv.in_shape)), 8).reshape(conv.in_shape)
+    f = oracle.fill_random(int(np.prod(conv.filt_shape)), 9).reshape(conv.filt_shape)
+    want = oracle.conv2d_naive(conv, x, f)
+    for cfg in ("3x5_8x8_loc", "5x3_4x16_noloc"):
+        got = tk.conv2d_im2col(x, f, s, tk.parse_gemm_config(cfg), tk.b200_device())
+        assert same(got, want), cfg
