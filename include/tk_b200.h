@@ -164,7 +164,8 @@ typedef struct tk_conv_plan_info {
   int box_w, box_h;        /* pixel box of the box / halo modes              */
   int halo_resident;       /* halo: filter slice resident in shared memory   */
   int winograd_m;          /* 2 or 4 for TK_KERNEL_WINOGRAD, else 0          */
-  int reserved[4];
+  int tuned;               /* 1: knobs from the loaded tuning DB             */
+  int reserved[3];
 } tk_conv_plan_info;
 
 /* ---- library --------------------------------------------------------- */
@@ -274,6 +275,17 @@ TK_API int tk_conv2d_plan_info(const tk_conv_shape* shape, const tk_conv_params*
                                const tk_exec_options* opts, tk_conv_plan_info* out);
 TK_API int tk_im2col_dev(const tk_conv_shape* shape, const float* d_in,
                   float* d_patches, void* stream);
+
+/* ---- tuning DB (lookup_best on the launch path, tuner.hpp:684-694) ------ */
+/* Load (merge) the tuner's NDJSON DB: for each (problem key, algorithm,
+ * precision) the fastest valid record's tensor-core knobs are kept.  A
+ * conv (im2col algorithm) or GEMM call on tensor cores whose
+ * tk_exec_options leave every knob automatic then runs with those knobs
+ * instead of the built-in rules.  device: keep only records of this device
+ * name (NULL = any).  *records = records kept. */
+TK_API int tk_tuning_db_load(const char* path, const char* device, size_t* records);
+TK_API int tk_tuning_db_clear(void);
+TK_API int tk_tuning_db_size(size_t* entries);
 
 /* ---- benchmarking (the tuner's device clock) --------------------------- */
 /* Upload the given HOST inputs once, run `warmup` untimed and `samples`

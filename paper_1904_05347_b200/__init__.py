@@ -113,8 +113,8 @@ class ExecOptionsC(C.Structure):
 class ConvPlanInfoC(C.Structure):
     _fields_ = [(n, C.c_int) for n in (
         "kernel", "precision", "requested_precision", "cta_group", "tile_m", "tile_n", "splits",
-        "tail_pieces", "imgs", "flat", "box_w", "box_h", "halo_resident", "winograd_m")] + \
-        [("reserved", C.c_int * 4)]
+        "tail_pieces", "imgs", "flat", "box_w", "box_h", "halo_resident", "winograd_m", "tuned")] + \
+        [("reserved", C.c_int * 3)]
 
 
 KERNELS = {0: "exact_simt", 1: "tc_halo", 2: "tc_pixn", 3: "tc_pixm", 4: "tc_gather",
@@ -131,7 +131,8 @@ EXPORTS = [
     "tk_conv2d_im2col", "tk_conv2d_winograd", "tk_im2col", "tk_filter_matrix",
     "tk_conv2d_dev", "tk_conv2d_workspace_size", "tk_conv2d_ex", "tk_im2col_dev",
     "tk_bench_gemm", "tk_bench_conv2d", "tk_gemm_ex", "tk_conv2d_prepare_dev",
-    "tk_conv2d_run_dev", "tk_conv2d_plan_info",
+    "tk_conv2d_run_dev", "tk_conv2d_plan_info", "tk_tuning_db_load", "tk_tuning_db_clear",
+    "tk_tuning_db_size",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -190,6 +191,9 @@ def lib() -> C.CDLL:
                               C.POINTER(ExecOptionsC), _vp, _vp, _vp, _vp, C.c_size_t, _vp],
         "tk_conv2d_plan_info": [C.POINTER(ConvShapeC), C.POINTER(ConvParamsC),
                                 C.POINTER(ExecOptionsC), C.POINTER(ConvPlanInfoC)],
+        "tk_tuning_db_load": [C.c_char_p, C.c_char_p, C.POINTER(C.c_size_t)],
+        "tk_tuning_db_clear": [],
+        "tk_tuning_db_size": [C.POINTER(C.c_size_t)],
         "tk_gemm_ex": [C.POINTER(GemmShapeC), C.POINTER(ExecOptionsC), _vp, _vp, _vp, _vp],
         "tk_bench_gemm": [C.POINTER(GemmShapeC), C.POINTER(GemmConfigC), C.POINTER(ExecOptionsC),
                           _vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(C.c_int64)],
@@ -655,6 +659,25 @@ def conv2d_plan_info(shape: ConvShape, params: ConvAlgoParams, precision="fp32",
     d["precision"] = PRECISION_NAMES[d["precision"]]
     d["requested_precision"] = PRECISION_NAMES[d["requested_precision"]]
     return d
+
+
+def tuning_db_load(path: str, device: Optional[str] = None) -> int:
+    """Load the tuner's NDJSON DB into the library (lookup_best on the launch
+    path): calls with automatic tensor-core knobs then run the fastest
+    recorded knobs for their problem.  Returns the records kept."""
+    n = C.c_size_t(0)
+    _check(lib().tk_tuning_db_load(path.encode(), device.encode() if device else None, C.byref(n)))
+    return int(n.value)
+
+
+def tuning_db_clear() -> None:
+    _check(lib().tk_tuning_db_clear())
+
+
+def tuning_db_size() -> int:
+    n = C.c_size_t(0)
+    _check(lib().tk_tuning_db_size(C.byref(n)))
+    return int(n.value)
 
 
 def gemm_dev(a, b, c, out, shape: GemmShape, cfg: Optional[GemmConfig] = None,

@@ -19,6 +19,7 @@
 #include "exact_gemm.cuh"
 #include "experiments.cuh"
 #include "launch_cache.cuh"
+#include "tuning_db.cuh"
 #include "layout.cuh"
 #include "tc_gemm.cuh"
 #include "tilekit/gemm.hpp"
@@ -238,6 +239,41 @@ struct KnobScope {
   KnobScope(const KnobScope&) = delete;
   KnobScope& operator=(const KnobScope&) = delete;
 };
+
+// Tuning DB on the launch path: a call whose tensor-core knobs are all
+// automatic takes the DB's fastest valid record for its problem (tuning_db.cuh).
+bool all_auto(const tk_exec_options* o) {
+  return !o || (o->tc_tile_n == 0 && o->tc_stages == 0 && o->tc_cluster == 0 && o->tc_mode == 0 &&
+                o->tc_split == 0);
+}
+
+bool apply_tuned_conv(const tilekit::ConvShape& s, const tk_conv_params* p,
+                      const tk_exec_options* o) {
+  const int prec = o ? o->precision : TK_PREC_FP32_EXACT;
+  if (!p || p->algo != 2 || prec == TK_PREC_FP32_EXACT || !all_auto(o)) return false;
+  TunedKnobs k;
+  if (!tuning_db_lookup(s.key(), "im2col", prec, &k)) return false;
+  TcKnobs& t = tc_knobs();
+  t.stages = k.stages;
+  t.cluster = k.cluster;
+  t.mode = k.mode;
+  t.split = k.split;
+  return true;
+}
+
+// GEMM: the N tile travels as an argument, the rest through tc_knobs.
+int tuned_gemm_tile(const tilekit::GemmShape& g, const tk_exec_options* o) {
+  const int prec = o ? o->precision : TK_PREC_FP32_EXACT;
+  if (prec == TK_PREC_FP32_EXACT) return 0;
+  if (!all_auto(o)) return o->tc_tile_n;
+  TunedKnobs k;
+  if (!tuning_db_lookup(g.key(), "gemm", prec, &k)) return 0;
+  TcKnobs& t = tc_knobs();
+  t.stages = k.stages;
+  t.cluster = k.cluster;
+  t.split = k.split;
+  return k.tile_n;
+}
 
 // ---- exact GEMM plumbing ---------------------------------------------------
 
@@ -786,9 +822,10 @@ int tk_gemm_dev(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const tk_
       const ExactLaunch L = cfg ? exact_launch_of(gemm_config(cfg)) : exact_auto((long long)g.m, (long long)g.n);
       launch_exact(gemm_args(g, d_a, d_b, d_c, d_out), L, false, 1, st);
     } else {
+      const int tile = tuned_gemm_tile(g, opts);
       launch_tc_colmajor_gemm(g.m, g.n, g.k, g.alpha, g.beta, g.op_a == tilekit::Op::Transpose,
-                              g.op_b == tilekit::Op::Transpose, d_a, d_b, d_c, d_out, prec,
-                              opts ? opts->tc_tile_n : 0, st);
+                              g.op_b == tilekit::Op::Transpose, d_a, d_b, d_c, d_out, prec, tile,
+                              st);
     }
   });
 }
@@ -812,7 +849,7 @@ int tk_gemm_ex(const tk_gemm_shape* shape, const tk_exec_options* opts, const fl
     else
       launch_tc_colmajor_gemm(g.m, g.n, g.k, g.alpha, g.beta, g.op_a == tilekit::Op::Transpose,
                               g.op_b == tilekit::Op::Transpose, da.f(), db.f(), dc.f(), dd.f(),
-                              prec, opts ? opts->tc_tile_n : 0, st);
+                              prec, tuned_gemm_tile(g, opts), st);
     d2h(out, dd.p, 4 * nc, st);
     finish(st);
   });
@@ -914,6 +951,7 @@ int tk_conv2d_ex(const tk_conv_shape* shape, const tk_conv_params* params,
   return guarded([&] {
     KnobScope knobs(opts);
     if (!params) fail(TK_ERR_CONTRACT, "conv2d: params must not be NULL");
+    apply_tuned_conv(conv_shape(shape), params, opts);
     conv_host(conv_shape(shape), params, precision_of(opts), in, filt, out);
   });
 }
@@ -1016,6 +1054,7 @@ int tk_conv2d_workspace_size(const tk_conv_shape* shape, const tk_conv_params* p
     if (!params || !bytes) fail(TK_ERR_CONTRACT, "conv2d_workspace_size: NULL argument");
     const tilekit::ConvShape s = conv_shape(shape);
     if (params->algo == 3) check_winograd(s, params);
+    apply_tuned_conv(s, params, opts);
     *bytes = conv_workspace(conv_geom(s), params, precision_of(opts));
   });
 }
@@ -1030,6 +1069,7 @@ int tk_conv2d_dev(const tk_conv_shape* shape, const tk_conv_params* params,
     const tilekit::ConvShape s = conv_shape(shape);
     const int prec = precision_of(opts);
     if (params->algo == 3) check_winograd(s, params);
+    apply_tuned_conv(s, params, opts);
     const size_t need = conv_workspace(conv_geom(s), params, prec);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (need && (!d_ws || ws_bytes < need)) {
@@ -1056,6 +1096,7 @@ static int conv_phase_dev(const tk_conv_shape* shape, const tk_conv_params* para
     const int prec = precision_of(opts);
     if (params->algo == 3) check_winograd(s, params);
     if (params->algo == 1) check_tiled_params(s, params);
+    apply_tuned_conv(s, params, opts);
     const size_t need = conv_workspace(conv_geom(s), params, prec);
     if (need && (!d_ws || ws_bytes < need))
       fail(TK_ERR_CONTRACT, "conv2d prepare/run: a workspace of " + std::to_string(need) +
@@ -1088,6 +1129,7 @@ int tk_conv2d_plan_info(const tk_conv_shape* shape, const tk_conv_params* params
     const int prec = precision_of(opts);
     tk_conv_plan_info r{};
     r.requested_precision = prec;
+    r.tuned = apply_tuned_conv(s, params, opts) ? 1 : 0;
     r.cta_group = 1;
     r.splits = 1;
     r.imgs = 1;
@@ -1149,6 +1191,25 @@ int tk_conv2d_plan_info(const tk_conv_shape* shape, const tk_conv_params* params
   });
 }
 
+int tk_tuning_db_load(const char* path, const char* device, size_t* records) {
+  return guarded([&] {
+    if (!path) fail(TK_ERR_CONTRACT, "tuning_db_load: path must not be NULL");
+    const size_t kept = tuning_db_load(path, device ? device : "");
+    if (records) *records = kept;
+  });
+}
+
+int tk_tuning_db_clear(void) {
+  return guarded([&] { tuning_db_clear(); });
+}
+
+int tk_tuning_db_size(size_t* entries) {
+  return guarded([&] {
+    if (!entries) fail(TK_ERR_CONTRACT, "tuning_db_size: NULL argument");
+    *entries = tuning_db_size();
+  });
+}
+
 int tk_bench_gemm(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const tk_exec_options* opts,
                   const float* a, const float* b, const float* c, int warmup, int samples,
                   int64_t* ns) {
@@ -1164,13 +1225,14 @@ int tk_bench_gemm(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const t
     if (read_c) h2d(dc.p, c, 4 * nc, st);
     const int prec = precision_of(opts);
     const ExactLaunch L = cfg ? exact_launch_of(gemm_config(cfg)) : exact_auto((long long)g.m, (long long)g.n);
+    const int tile = tuned_gemm_tile(g, opts);
     auto run = [&] {
       if (prec == TK_PREC_FP32_EXACT) {
         launch_exact(gemm_args(g, da.f(), db.f(), dc.f(), dd.f()), L, false, 1, st);
       } else {
         launch_tc_colmajor_gemm(g.m, g.n, g.k, g.alpha, g.beta, g.op_a == tilekit::Op::Transpose,
                                 g.op_b == tilekit::Op::Transpose, da.f(), db.f(), dc.f(), dd.f(),
-                                prec, opts ? opts->tc_tile_n : 0, st);
+                                prec, tile, st);
       }
     };
     time_samples(run, warmup, samples, ns, st);
@@ -1187,6 +1249,7 @@ int tk_bench_conv2d(const tk_conv_shape* shape, const tk_conv_params* params,
     const ConvGeom g = conv_geom(s);
     if (params->algo == 1) check_tiled_params(s, params);
     if (params->algo == 3) check_winograd(s, params);
+    apply_tuned_conv(s, params, opts);
     const int prec = precision_of(opts);
     cudaStream_t st = host_stream();
     DevBuf din(4 * in_elems(g), st), dfl(4 * filt_elems(g), st), dout(4 * out_elems(g), st);

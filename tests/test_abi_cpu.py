@@ -131,3 +131,43 @@ def test_undersized_operands_raise_shape_error(tk):
                       torch.zeros(s.out_shape), s, tk.parse_conv_params("im2col"))
     with pytest.raises(tk.ContractError, match="CUDA tensor"):
         tk.gemm_dev(torch.zeros(64), torch.zeros(64), None, torch.zeros(64), g)
+
+
+def test_tuning_db_drives_the_plan(tk, tmp_path):
+    """lookup_best on the launch path: with a DB loaded, a call whose
+    tensor-core knobs are automatic takes the fastest valid record's knobs
+    for its (problem, algorithm, precision); explicit knobs still win, and
+    clearing the DB restores the built-in rules.  Host-side (plan only)."""
+    s = tk.ConvShape(32, 56, 56, 256, 256, 3, 3, 1, True)
+    im = tk.parse_conv_params("im2col")
+    base = tk.conv2d_plan_info(s, im, "tf32")
+    assert base["kernel"] == "tc_im2col" and base["tuned"] == 0
+    key = s.key()
+    db = tmp_path / "db.ndjson"
+    recs = [
+        {"problem": key, "config": "im2col@tf32", "median_ns": 170000, "valid": True},
+        {"problem": key, "config": "im2col@tf32_c2_pixn", "median_ns": 150000, "valid": True},
+        {"problem": key, "config": "im2col@tf32_halo", "median_ns": 100000, "valid": False},
+        {"problem": key, "config": "im2col@bf16_halo", "median_ns": 90000, "valid": True},
+        {"problem": key, "config": "tiled_t2x2_v4x8", "median_ns": 5000000, "valid": True},
+    ]
+    import json
+    db.write_text("\n".join(json.dumps(dict(r, device="NVIDIA B200", samples=5, min_ns=1,
+                                             mean_ns=1, gflops=1.0)) for r in recs) + "\n")
+    try:
+        assert tk.tuning_db_load(str(db)) >= 2
+        d = tk.conv2d_plan_info(s, im, "tf32")
+        assert d["tuned"] == 1 and d["kernel"] == "tc_pixn" and d["cta_group"] == 2
+        assert tk.conv2d_plan_info(s, im, "bf16")["kernel"] == "tc_halo"
+        # explicit knobs are the caller's
+        d = tk.conv2d_plan_info(s, im, options=tk.exec_options("tf32", mode="im2col"))
+        assert d["tuned"] == 0 and d["kernel"] == "tc_im2col"
+        # other shapes keep the rules
+        s2 = tk.ConvShape(32, 28, 28, 512, 512, 3, 3, 1, True)
+        assert tk.conv2d_plan_info(s2, im, "tf32")["tuned"] == 0
+    finally:
+        tk.tuning_db_clear()
+    assert tk.tuning_db_size() == 0
+    assert tk.conv2d_plan_info(s, im, "tf32")["kernel"] == "tc_im2col"
+    with pytest.raises(tk.IoError):
+        tk.tuning_db_load(str(tmp_path / "missing.ndjson"))
