@@ -93,6 +93,8 @@ def plan_str(tk, shape, algo, prec):
         s += " flat"
     if d["precision"] != d["requested_precision"]:
         s += f" (requested {d['requested_precision']})"
+    if d.get("tuned"):
+        s += " [db]"
     return s
 
 
@@ -126,6 +128,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch layer by layer")
+    ap.add_argument("--tuning-db", default=os.path.join(ROOT, "profiles", "r02_tune_ncu.ndjson"),
+                    help="NDJSON tuning DB loaded into the library (tools/tune_ncu.py); "
+                         "'none' = the built-in rules only")
     ap.add_argument("--no-layers", action="store_true",
                     help="skip the per-layer kernel timing (profiling runs: the step's launches "
                          "are then the last ones after the L2 flush)")
@@ -337,6 +342,11 @@ def main():
     N = args.batch
     prec = args.precision
     lo_img, hi_img = rank * N, (rank + 1) * N  # this rank's images of the global batch
+    # The tuner's DB (lookup_best on the launch path): calls with automatic
+    # knobs take the fastest recorded knobs of their shape.
+    db_records = 0
+    if args.tuning_db != "none" and os.path.exists(args.tuning_db):
+        db_records = tk.tuning_db_load(args.tuning_db)
 
     # Resident inputs: one independent seeded input + filter per layer
     # instance (the reference `layers` harness, tilekit_cli.cpp:374-403).
@@ -1009,7 +1019,9 @@ def main():
                        "batch_per_gpu": N, "global_batch": N * world,
                        "algorithm": "im2col implicit GEMM",
                        "precision": prec, "step_gflop": round(step_flops / 1e9, 2),
-                       "l2": "flushed between steps (256 MiB write, outside events)"},
+                       "l2": "flushed between steps (256 MiB write, outside events)",
+                       "tuning_db": (os.path.relpath(args.tuning_db, ROOT) if db_records else None),
+                       "tuning_db_entries": db_records},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": dict(clocks.summary(), samples_in_timed=timed_samples,

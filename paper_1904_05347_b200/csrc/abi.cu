@@ -460,11 +460,14 @@ int check_winograd(const tilekit::ConvShape& s, const tk_conv_params* p) {
 
 struct WinoSizes {
   size_t v, u, p;
-  size_t bytes() const { return 4 * (v + u + p) + 3 * 256; }
+  bool split3 = false;  // 3xTF32: + the tripled V and U operands
+  size_t bytes() const { return 4 * (v + u + p) + 3 * 256 + (split3 ? 12 * (v + u) + 2 * 256 : 0); }
 };
-WinoSizes wino_sizes(const WinoGeom& w) {
+WinoSizes wino_sizes(const WinoGeom& w, int precision = TK_PREC_FP32_EXACT) {
   const size_t spots = (size_t)w.t * w.t;
-  return WinoSizes{spots * w.tiles * w.C, spots * (size_t)w.C * w.K, spots * w.tiles * w.K};
+  WinoSizes z{spots * w.tiles * w.C, spots * (size_t)w.C * w.K, spots * w.tiles * w.K};
+  z.split3 = precision == TK_PREC_3XTF32 && w.C % 4 == 0;
+  return z;
 }
 
 float* carve(char*& cursor, size_t elems) {
@@ -477,18 +480,25 @@ float* carve(char*& cursor, size_t elems) {
 void winograd_dev(const ConvGeom& g, int m, int precision, const float* in, const float* filt,
                   float* out, void* ws, cudaStream_t st, int phase = kConvAll) {
   const WinoGeom w = wino_geom(g, m);
-  const WinoSizes sz = wino_sizes(w);
+  const WinoSizes sz = wino_sizes(w, precision);
   char* cur = static_cast<char*>(ws);
   float* v = carve(cur, sz.v);
   float* u = carve(cur, sz.u);
   float* prod = carve(cur, sz.p);
+  float* v3 = sz.split3 ? carve(cur, 3 * sz.v) : nullptr;
+  float* u3 = sz.split3 ? carve(cur, 3 * sz.u) : nullptr;
   // TMA needs 16-byte row strides; odd channel counts keep the exact GEMM.
   const bool tc = precision != TK_PREC_FP32_EXACT && w.C % 4 == 0;
-  // The filter transform depends only on the filter: the prepare phase.
-  if (phase & kConvPrepare) wino_filter_transform(w, filt, u, /*k_major=*/tc, st);
+  const int spots = w.t * w.t;
+  // The filter transform depends only on the filter: the prepare phase
+  // (3xTF32: also its (hi, lo, hi) expansion along C).
+  if (phase & kConvPrepare) {
+    wino_filter_transform(w, filt, u, /*k_major=*/tc, st);
+    if (sz.split3) launch_split3_rows(u, (long long)spots * w.K, w.C, u3, 1, st);
+  }
   if (!(phase & kConvRun)) return;
   wino_input_transform(w, in, v, st);
-  const int spots = w.t * w.t;
+  if (sz.split3) launch_split3_rows(v, (long long)spots * w.tiles, w.C, v3, 0, st);
   if (!tc) {
     ExactArgs p{};
     p.M = w.tiles;
@@ -515,15 +525,18 @@ void winograd_dev(const ConvGeom& g, int m, int precision, const float* in, cons
     // features on N, so P's rows (k contiguous) leave through the TMA-store
     // epilogue (features on M stored column by column from registers: the
     // F(4x4) batched GEMM of VGG conv4_2 ran 109 us that way).
+    // 3xTF32: the same GEMM over 3C ([v | v | v_lo] . [u_hi | u_lo | u_hi]),
+    // ~fp32-accurate products, so F(4x4) meets the reference's 1e-3.
+    const int kx = sz.split3 ? 3 : 1;
     TcGemm t{};
     t.M = w.tiles;
     t.N = w.K;
-    t.K = w.C;
+    t.K = kx * w.C;
     t.batch = spots;
-    t.a = v;
-    t.a_batch = (long long)w.tiles * w.C;
-    t.b = u;
-    t.b_batch = (long long)w.C * w.K;
+    t.a = sz.split3 ? v3 : v;
+    t.a_batch = (long long)w.tiles * w.C * kx;
+    t.b = sz.split3 ? u3 : u;
+    t.b_batch = (long long)w.C * w.K * kx;
     t.d = prod;
     t.d_sm = w.K;
     t.d_sn = 1;
@@ -537,7 +550,7 @@ void winograd_dev(const ConvGeom& g, int m, int precision, const float* in, cons
 }
 
 size_t conv_workspace(const ConvGeom& g, const tk_conv_params* p, int precision) {
-  if (p->algo == 3) return wino_sizes(wino_geom(g, (int)p->tile_rows)).bytes();
+  if (p->algo == 3) return wino_sizes(wino_geom(g, (int)p->tile_rows), precision).bytes();
   if (precision != TK_PREC_FP32_EXACT) return tc_conv_workspace(g, precision);
   return 0;
 }
@@ -572,8 +585,6 @@ void conv_dev(const tilekit::ConvShape& s, const tk_conv_params* p, int precisio
       return;
     case 3: {
       const int m = check_winograd(s, p);
-      if (precision == TK_PREC_3XTF32)
-        fail(TK_ERR_CAPABILITY, "conv2d_winograd: 3xTF32 is provided on the im2col path only");
       winograd_dev(g, m, precision, in, filt, out, ws, st, phase);
       return;
     }
@@ -1174,14 +1185,12 @@ int tk_conv2d_plan_info(const tk_conv_shape* shape, const tk_conv_params* params
         break;
       case 3: {
         const int m = check_winograd(s, params);
-        if (prec == TK_PREC_3XTF32)
-          fail(TK_ERR_CAPABILITY, "conv2d_winograd: 3xTF32 is provided on the im2col path only");
         r.kernel = TK_KERNEL_WINOGRAD;
         r.winograd_m = m;
         const bool tc = prec != TK_PREC_FP32_EXACT && g.C % 4 == 0;
         // The transform-domain operands are fp32 scratch: kind::tf32 for
-        // every tensor-core request.
-        r.precision = tc ? TK_PREC_TF32 : TK_PREC_FP32_EXACT;
+        // every tensor-core request (3xTF32 splits them).
+        r.precision = !tc ? TK_PREC_FP32_EXACT : prec == TK_PREC_3XTF32 ? TK_PREC_3XTF32 : TK_PREC_TF32;
         break;
       }
       default:

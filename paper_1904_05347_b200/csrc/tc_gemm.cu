@@ -2011,6 +2011,11 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
   dispatch<kPlain>(ma, mb, md, p, cg, tf32, st);
 }
 
+void launch_split3_rows(const float* src, long long rows, long long kp, float* dst, int pattern,
+                        cudaStream_t st) {
+  split3_rows(src, rows, kp, dst, pattern, st);
+}
+
 void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float beta, bool ta,
                              bool tb, const float* a, const float* b, const float* c, float* d,
                              int precision, int tile_n, cudaStream_t st) {

@@ -36,6 +36,12 @@ struct TcGemm {
 
 void launch_tc_gemm(const TcGemm& g, cudaStream_t st);
 
+// 3xTF32 operand expansion: rows x [kp] K-major fp32 -> rows x [3 kp];
+// pattern 0 = (x, x, x_lo) (the A side), 1 = (x_hi, x_lo, x_hi) (the B side):
+// one TF32 contraction of depth 3 kp then sums a_hi b_hi + a_hi b_lo + a_lo b_hi.
+void launch_split3_rows(const float* src, long long rows, long long kp, float* dst, int pattern,
+                        cudaStream_t st);
+
 // Per-call tensor-core knobs (tk_exec_options.tc_stages / tc_cluster /
 // tc_mode / tc_split), set by the C ABI for the duration of one call on the
 // calling thread; zero = automatic.

@@ -180,13 +180,135 @@ __global__ void __launch_bounds__(256) wino_output_kernel(WinoGeom g, const floa
   }
 }
 
+// Vectorised stage 1 / stage 4: V channels (V = 4 for F(2x2), 2 for
+// F(4x4): 16 x float4 / 36 x float2 patches stay in registers) per thread,
+// 16- / 8-byte loads and stores along C (input) or K (output).  Same
+// per-element arithmetic as the scalar kernels (transform_tile's two
+// passes, lane by lane), so the bits are the same.
+template <int V>
+struct VecT;
+template <>
+struct VecT<4> {
+  using type = float4;
+  static __device__ __forceinline__ float get(const float4& v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+  }
+  static __device__ __forceinline__ void set(float4& v, int i, float x) {
+    if (i == 0) v.x = x;
+    else if (i == 1) v.y = x;
+    else if (i == 2) v.z = x;
+    else v.w = x;
+  }
+};
+template <>
+struct VecT<2> {
+  using type = float2;
+  static __device__ __forceinline__ float get(const float2& v, int i) { return i == 0 ? v.x : v.y; }
+  static __device__ __forceinline__ void set(float2& v, int i, float x) {
+    if (i == 0) v.x = x;
+    else v.y = x;
+  }
+};
+
+template <class Plan, int V>
+__global__ void __launch_bounds__(256) wino_input_vec_kernel(WinoGeom g, const float* __restrict__ in,
+                                                             float* __restrict__ v) {
+  using VT = typename VecT<V>::type;
+  constexpr int T = Plan::T, M = Plan::M;
+  const int cv = g.C / V;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)g.tiles * cv) return;
+  const int c = (int)(idx % cv) * V;
+  const int tile = (int)(idx / cv);
+  const int tj = tile % g.tiles_c;
+  const int ti = (tile / g.tiles_c) % g.tiles_r;
+  const int b = tile / (g.tiles_c * g.tiles_r);
+  const int r0 = ti * M - g.pad_t, c0 = tj * M - g.pad_l;
+  VT patch[T * T];
+#pragma unroll
+  for (int i = 0; i < T; ++i) {
+    const int ih = r0 + i;
+#pragma unroll
+    for (int j = 0; j < T; ++j) {
+      const int iw = c0 + j;
+      const bool inside = ih >= 0 && iw >= 0 && ih < g.H && iw < g.W;
+      VT z{};
+      patch[i * T + j] =
+          inside ? __ldg(reinterpret_cast<const VT*>(in + (((long long)b * g.H + ih) * g.W + iw) * g.C + c))
+                 : z;
+    }
+  }
+  const long long plane = (long long)g.tiles * g.C;
+  VT res[T * T];
+#pragma unroll
+  for (int lane = 0; lane < V; ++lane) {
+    float src[T * T], out[T * T];
+#pragma unroll
+    for (int q = 0; q < T * T; ++q) src[q] = VecT<V>::get(patch[q], lane);
+    transform<T, T>([](int i, int k) { return Plan::bt(i * T + k); }, src, out);
+#pragma unroll
+    for (int q = 0; q < T * T; ++q) VecT<V>::set(res[q], lane, out[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < T * T; ++q)
+    __stcs(reinterpret_cast<VT*>(v + q * plane + (long long)tile * g.C + c), res[q]);
+}
+
+template <class Plan, int V>
+__global__ void __launch_bounds__(256) wino_output_vec_kernel(WinoGeom g, const float* __restrict__ prod,
+                                                              float* __restrict__ out) {
+  using VT = typename VecT<V>::type;
+  constexpr int T = Plan::T, M = Plan::M;
+  const int kv = g.K / V;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)g.tiles * kv) return;
+  const int k = (int)(idx % kv) * V;
+  const int tile = (int)(idx / kv);
+  const int tj = tile % g.tiles_c;
+  const int ti = (tile / g.tiles_c) % g.tiles_r;
+  const int b = tile / (g.tiles_c * g.tiles_r);
+  const long long plane = (long long)g.tiles * g.K;
+  VT gathered[T * T];
+#pragma unroll
+  for (int q = 0; q < T * T; ++q)
+    gathered[q] = __ldcs(reinterpret_cast<const VT*>(prod + q * plane + (long long)tile * g.K + k));
+  VT res[M * M];
+#pragma unroll
+  for (int lane = 0; lane < V; ++lane) {
+    float src[T * T], o[M * M];
+#pragma unroll
+    for (int q = 0; q < T * T; ++q) src[q] = VecT<V>::get(gathered[q], lane);
+    transform<M, T>([](int i, int kk) { return Plan::at(i * T + kk); }, src, o);
+#pragma unroll
+    for (int q = 0; q < M * M; ++q) VecT<V>::set(res[q], lane, o[q]);
+  }
+  const int rh = min(M, g.OH - ti * M), cw = min(M, g.OW - tj * M);
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    if (i >= rh) break;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      if (j >= cw) break;
+      *reinterpret_cast<VT*>(out + (((long long)b * g.OH + ti * M + i) * g.OW + tj * M + j) * g.K + k) =
+          res[i * M + j];
+    }
+  }
+}
+
 inline unsigned blocks_for(long long n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
 
 void wino_input_transform(const WinoGeom& g, const float* d_in, float* d_v, cudaStream_t st) {
   const long long n = (long long)g.tiles * g.C;
-  if (g.m == 2) wino_input_kernel<F2><<<blocks_for(n, 256), 256, 0, st>>>(g, d_in, d_v);
+  const bool vec = aligned16(d_in) && aligned16(d_v);
+  if (g.m == 2 && vec && g.C % 4 == 0)
+    wino_input_vec_kernel<F2, 4><<<blocks_for(n / 4, 256), 256, 0, st>>>(g, d_in, d_v);
+  else if (g.m == 4 && vec && g.C % 2 == 0)
+    wino_input_vec_kernel<F4, 2><<<blocks_for(n / 2, 256), 256, 0, st>>>(g, d_in, d_v);
+  else if (g.m == 2) wino_input_kernel<F2><<<blocks_for(n, 256), 256, 0, st>>>(g, d_in, d_v);
   else wino_input_kernel<F4><<<blocks_for(n, 256), 256, 0, st>>>(g, d_in, d_v);
   note_launch();
   TKB_CUDA(cudaGetLastError());
@@ -203,7 +325,12 @@ void wino_filter_transform(const WinoGeom& g, const float* d_filt, float* d_u, b
 
 void wino_output_transform(const WinoGeom& g, const float* d_prod, float* d_out, cudaStream_t st) {
   const long long n = (long long)g.tiles * g.K;
-  if (g.m == 2) wino_output_kernel<F2><<<blocks_for(n, 256), 256, 0, st>>>(g, d_prod, d_out);
+  const bool vec = aligned16(d_prod) && aligned16(d_out);
+  if (g.m == 2 && vec && g.K % 4 == 0)
+    wino_output_vec_kernel<F2, 4><<<blocks_for(n / 4, 256), 256, 0, st>>>(g, d_prod, d_out);
+  else if (g.m == 4 && vec && g.K % 2 == 0)
+    wino_output_vec_kernel<F4, 2><<<blocks_for(n / 2, 256), 256, 0, st>>>(g, d_prod, d_out);
+  else if (g.m == 2) wino_output_kernel<F2><<<blocks_for(n, 256), 256, 0, st>>>(g, d_prod, d_out);
   else wino_output_kernel<F4><<<blocks_for(n, 256), 256, 0, st>>>(g, d_prod, d_out);
   note_launch();
   TKB_CUDA(cudaGetLastError());
