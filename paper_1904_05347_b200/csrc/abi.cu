@@ -253,6 +253,7 @@ bool apply_tuned_conv(const tilekit::ConvShape& s, const tk_conv_params* p,
   if (!p || p->algo != 2 || prec == TK_PREC_FP32_EXACT || !all_auto(o)) return false;
   TunedKnobs k;
   if (!tuning_db_lookup(s.key(), "im2col", prec, &k)) return false;
+  if (!k.stages && !k.cluster && !k.mode && !k.split) return false;  // the DB keeps the rules
   TcKnobs& t = tc_knobs();
   t.stages = k.stages;
   t.cluster = k.cluster;

@@ -33,6 +33,9 @@ const Experiments& experiments() {
     x.tc_epi = env_int("TK_TC_EPI", 0);
     x.epi_ring = env_flag("TK_EPI_RING", true);
     x.epi_ring_n = env_int("TK_EPI_RING_N", 0);
+    x.epi_slots = env_int("TK_EPI_SLOTS", 0);
+    x.direct_store = env_int("TK_DIRECT_STORE", 0);
+    x.epi_groups = env_int("TK_EPI_GROUPS", 0);
     x.tc_acc = env_int("TK_TC_ACC", 0);
     x.raster = env_int("TK_RASTER", 8);
     x.trace = env_flag("TK_TC_TRACE", false);

@@ -18,7 +18,10 @@ struct Experiments {
   int tc_stages = 0;            // TK_TC_STAGES: operand ring depth cap
   int tc_epi = 0;               // TK_TC_EPI: staging buffers cap
   bool epi_ring = true;         // TK_EPI_RING=0: whole-tile epilogue staging
-  int epi_ring_n = 0;           // TK_EPI_RING_N: chunks per staging half
+  int epi_ring_n = 0;           // TK_EPI_RING_N: chunks per staging slot
+  int epi_slots = 0;            // TK_EPI_SLOTS: staging slots (2..8)
+  int direct_store = 0;         // TK_DIRECT_STORE=1: register -> global epilogue (narrow halo)
+  int epi_groups = 0;           // TK_EPI_GROUPS: 1 or 2 epilogue warpgroups
   int tc_acc = 0;               // TK_TC_ACC: TMEM accumulator slots (2/4/8)
   int raster = 8;               // TK_RASTER: M-blocks per raster group (0 = linear)
   bool trace = false;           // TK_TC_TRACE=1: in-kernel timeline probe

@@ -62,6 +62,7 @@ constexpr int kAccCols = 256;  // TMEM: 2 x 256 fp32 columns allocated
 constexpr int kMaxAcc = 8;     // accumulator slots when BN <= 64 (512 / 64)
 constexpr int kMaxStages = 8;
 constexpr int kMaxSplits = 16;  // split-K partials summed by splitk_reduce
+constexpr int kMaxNarrowMma = 32;  // narrow halo: MMAs per tile (two taps each, 7x7 -> 25)
 
 enum TcMode : int {
   kPlain = 0,
@@ -69,8 +70,14 @@ enum TcMode : int {
   kConvPixM = 2,
   kConvGather = 3,
   kConvHalo = 4,
-  kConvIm2col = 5  // plain GEMM whose A rows are output pixels loaded by im2col-mode TMA
+  kConvIm2col = 5,  // plain GEMM whose A rows are output pixels loaded by im2col-mode TMA
+  kConvHaloNarrow = 6  // halo mode on 16-byte pixels (the C = 3 first layers), see TcArgs::nphase
 };
+// Halo-family modes (halo box operand + shifted-view taps, halo epilogue).
+template <int MODE>
+constexpr bool halo_like() {
+  return MODE == kConvHalo || MODE == kConvHaloNarrow;
+}
 // Modes with the plain GEMM's unit decode, split-K partials and tail pieces.
 template <int MODE>
 constexpr bool plain_like() {
@@ -84,10 +91,27 @@ constexpr bool plain_like() {
 // pixel operand; groups take alternate K-slabs so their load latencies
 // overlap.
 constexpr int kGatherGroups = TKB_GATHER_GROUPS;
+// Epilogue warpgroups: two (warps 2..5 and 6..9, alternate tiles) except in
+// gather mode, whose warps 6.. are producers.  The second group runs only
+// when TcArgs::epi_groups == 2 (epilogue-bound tiles).
+#ifndef TKB_EPI_GROUPS
+#define TKB_EPI_GROUPS 2
+#endif
+#ifndef TKB_TMEM_PAIRS
+#define TKB_TMEM_PAIRS 1
+#endif
+template <int MODE>
+constexpr int epi_groups_of() {
+  // (only the narrow halo: a second group on the other modes measured no
+  // better for short-K tiles and costs every launch 128 threads)
+  return MODE == kConvHaloNarrow ? TKB_EPI_GROUPS : 1;
+}
 template <int MODE>
 constexpr int threads_of() {
-  return MODE == kConvGather ? kThreads + 128 * kGatherGroups : kThreads;
+  return MODE == kConvGather ? kThreads + 128 * kGatherGroups : kThreads + 128 * (epi_groups_of<MODE>() - 1);
 }
+// Epilogue group g's named barrier: ptx::epi_sync(g) (ids 1 / 2; gather mode,
+// whose producer groups use 2.., has one epilogue group).
 
 struct TcArgs {
   int M, N, K;
@@ -102,7 +126,10 @@ struct TcArgs {
   int store_tma;               // epilogue via swizzled smem tile + TMA store
   int epi_bytes;               // bytes of epilogue staging
   int epi_bufs;                // staging buffers for the TMA-store epilogue
-  int epi_ring;                // > 0: staging halves of epi_ring 32-column chunks (tma_store_epilogue)
+  int epi_ring;                // > 0: staging slots of epi_ring 32-column chunks (tma_store_epilogue)
+  int epi_slots;               // staging slots in the ring (2..8): bulk stores in flight per CTA
+  int direct_store;            // epilogue: st.global straight from the TMEM registers (no TMA store)
+  int epi_groups;              // epilogue warpgroups in use (1 or 2); staging split between them
   // TMEM accumulator ring: acc_slots slots of acc_cols columns (512 / slots);
   // more slots for narrow tiles let the MMA run further ahead of the
   // epilogue, decoupling their per-tile handshakes.
@@ -138,6 +165,15 @@ struct TcArgs {
   // 32 M x 32 K (box {32, 32, 4} of the view {32, K, M/32}), 4 KiB apart,
   // 128B_ATOM_32B-swizzled (ptx::desc_sw128_mn).
   int a_mn;
+  // Narrow halo (kConvHaloNarrow): window taps R*S of the 16-byte-pixel
+  // first layers (C <= 4 tf32 / 8 bf16 channels, input padded once).
+  int narrow_taps;
+  // Narrow halo (kConvHalo with 16-byte pixels): stride^2 phase boxes of
+  // phase_bytes each (stride 2: the even/odd rows x columns of the input,
+  // TMA traversal stride 2), taps ordered by (phase, row, column) so each
+  // MMA's two taps are increasing addresses (desc_none's LBO = their gap).
+  int nphase, phase_bytes;
+  int halo_tx;  // bytes the narrow halo's boxes deliver (halo_bytes: that, 1024-aligned)
   // Balanced tail (plain / pixN, splits == 1; stream-K over the last partial
   // wave): the tail_W = (tiles - tail_start) x num_kb slab-steps of the
   // tiles >= tail_start are dealt to the tail_P SM pairs as equal contiguous
@@ -365,6 +401,136 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
   }
 }
 
+// The narrow halo's epilogue (kConvHaloNarrow): the same staging / TMA
+// store, for one of two epilogue groups (own slots, barrier, bulk groups),
+// with epi_slots staging slots and two TMEM loads per wait.  (Kept apart:
+// these run-time generalities measured 10-20% slower on the other modes.)
+template <int CG>
+__device__ __forceinline__ void tma_store_epilogue_multi(const TcArgs& p, uint32_t taddr, uint8_t* stage,
+                                                         int local, uint32_t warp, uint32_t lane, int row,
+                                                   int srow,
+                                                   uint32_t empty_cluster_addr, uint64_t* empty_local,
+                                                   const CUtensorMap* map_d, int c0, int c1, int c2,
+                                                   int c3, int rank_dims, int& ring, uint32_t bar) {
+  const int nchunks = (p.BN + 31) / 32;
+  const bool issuer = (warp & 3) == 2 && lane == 0;  // group leader: warp 2 or 6
+  if (p.epi_ring) {
+    // Staging in two halves of epi_ring 32-column chunks each (as little as
+    // 2 x 16 KiB whatever the tile width): the chunks go out in batches of
+    // epi_ring, each batch one bulk group; a batch waits only for the batch
+    // before the previous one to have been read.  epi_ring >= nchunks is the
+    // whole-tile double buffer.
+    // epi_slots slots: up to epi_slots - 1 batches' stores stay in flight
+    // while the next is drained (the write-out of an HBM-bound layer needs
+    // several tiles of stores outstanding per SM).
+    const int bs = p.epi_ring;
+    for (int j0 = 0; j0 < nchunks; j0 += bs) {
+      const int nb = min(bs, nchunks - j0);
+      uint8_t* half = stage + (ring % p.epi_slots) * bs * kRows * kSlabBytes;
+      ++ring;
+      if (issuer) ptx::bulk_wait_read_dyn(p.epi_slots - 1);
+      ptx::epi_sync(bar);
+      // TKB_TMEM_PAIRS: two TMEM loads in flight per wait.
+#if TKB_TMEM_PAIRS
+      for (int jj = 0; jj < nb; jj += 2) {
+        uint32_t r[2][32];
+        ptx::tmem_ld32_async(taddr + (j0 + jj) * 32, r[0]);
+        if (jj + 1 < nb) ptx::tmem_ld32_async(taddr + (j0 + jj + 1) * 32, r[1]);
+        ptx::tmem_wait_ld();
+        if (srow < 0) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (jj + h >= nb) break;
+          const uint32_t rowp =
+              ptx::smem(half + (jj + h) * kRows * kSlabBytes + srow * kSlabBytes);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(rowp + ((c ^ (srow & 7)) << 4)),
+                         "f"(p.alpha * __uint_as_float(r[h][4 * c])),
+                         "f"(p.alpha * __uint_as_float(r[h][4 * c + 1])),
+                         "f"(p.alpha * __uint_as_float(r[h][4 * c + 2])),
+                         "f"(p.alpha * __uint_as_float(r[h][4 * c + 3]))
+                         : "memory");
+          }
+        }
+      }
+#else
+      for (int jj = 0; jj < nb; ++jj) {
+        float v[32];
+        ptx::tmem_ld32(taddr + (j0 + jj) * 32, v);
+        if (srow < 0) continue;
+        const uint32_t rowp = ptx::smem(half + jj * kRows * kSlabBytes + srow * kSlabBytes);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(rowp + ((c ^ (srow & 7)) << 4)),
+                       "f"(p.alpha * v[4 * c]), "f"(p.alpha * v[4 * c + 1]),
+                       "f"(p.alpha * v[4 * c + 2]), "f"(p.alpha * v[4 * c + 3])
+                       : "memory");
+        }
+      }
+#endif
+      const bool last = j0 + nb == nchunks;
+      if (last) ptx::tc_fence_before();
+      ptx::fence_proxy_async();
+      ptx::epi_sync(bar);
+      if (issuer) {
+        if (last) {
+          if constexpr (CG == 2) ptx::mbar_arrive_remote(empty_cluster_addr);
+          else ptx::mbar_arrive(empty_local);
+        }
+        for (int jj = 0; jj < nb; ++jj) {
+          const uint8_t* src = half + jj * kRows * kSlabBytes;
+          if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + 32 * (j0 + jj), c1, c2, c3);
+          else ptx::tma_store_3d(map_d, src, c0 + 32 * (j0 + jj), c1, c2);
+        }
+        ptx::bulk_commit();
+      }
+    }
+    return;
+  }
+  const int buf_bytes = nchunks * kRows * kSlabBytes;
+  uint8_t* sbuf = stage + (p.epi_bufs > 1 ? (local & 1) : 0) * buf_bytes;
+  if (issuer) {
+    if (p.epi_bufs > 1) ptx::bulk_wait_read<1>();
+    else ptx::bulk_wait_read<0>();
+  }
+  ptx::epi_sync(bar);
+  for (int j = 0; j < nchunks; ++j) {
+    float v[32];
+    ptx::tmem_ld32(taddr + j * 32, v);
+    if (srow < 0) continue;  // virtual row without an output pixel
+    const uint32_t rowp = ptx::smem(sbuf + j * kRows * kSlabBytes + srow * kSlabBytes);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(rowp + ((c ^ (srow & 7)) << 4)),
+                   "f"(p.alpha * v[4 * c]), "f"(p.alpha * v[4 * c + 1]),
+                   "f"(p.alpha * v[4 * c + 2]), "f"(p.alpha * v[4 * c + 3])
+                   : "memory");
+    }
+  }
+  if (local == 0 && issuer) trace_mark(p, 8);  // TMEM drained to smem (first unit)
+  if (local == kTraceUnit && issuer) trace_mark(p, 14);
+  ptx::tc_fence_before();
+  if (local == kTraceUnit && issuer) trace_mark(p, 18);
+  ptx::fence_proxy_async();
+  if (local == kTraceUnit && issuer) trace_mark(p, 19);
+  ptx::epi_sync(bar);
+  if (issuer) {
+    // Accumulator fully read by all 128 threads: hand TMEM back to the MMA.
+    if constexpr (CG == 2) ptx::mbar_arrive_remote(empty_cluster_addr);
+    else ptx::mbar_arrive(empty_local);
+    if (local == kTraceUnit) trace_mark(p, 20);  // (overrides: after the TMEM release)
+    for (int j = 0; j < nchunks; ++j) {
+      const uint8_t* src = sbuf + j * kRows * kSlabBytes;
+      if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + 32 * j, c1, c2, c3);
+      else ptx::tma_store_3d(map_d, src, c0 + 32 * j, c1, c2);
+    }
+    ptx::bulk_commit();
+    if (local == 0) trace_mark(p, 9);  // stores issued (first unit)
+    if (local == kTraceUnit) trace_mark(p, 15);
+  }
+}
+
 // Gather producer (conv fallback for channel counts / strides the TMA box
 // cannot express): 128 threads build the 128-pixel x 32-element fp32 K-slab
 // of the implicit patch matrix directly in the 128-byte-swizzled layout the
@@ -474,11 +640,11 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   constexpr int BM = kRows * CG;
-  const int a_bytes = MODE == kConvHalo ? p.halo_bytes : kRows * kSlabBytes;
+  const int a_bytes = halo_like<MODE>() ? p.halo_bytes : kRows * kSlabBytes;
   const int b_rows = p.BN / CG;
   const int b_bytes = b_rows * kSlabBytes;
   const int stage_bytes =
-      a_bytes + (MODE == kConvHalo ? (p.resident ? 0 : p.taps) : 1) * b_bytes;
+      a_bytes + (halo_like<MODE>() ? (p.resident ? 0 : p.taps) : 1) * b_bytes;
   // resident filter (halo mode): taps x cchunks slabs after the stages
   uint8_t* fres = base + p.stages * stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(
@@ -534,7 +700,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
                                   : p.num_m * p.num_n * p.batch * p.splits;
   const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
 
-  if (MODE == kConvHalo && warp == 0) {
+  if (halo_like<MODE>() && warp == 0) {
     // ---------------- TMA producer, halo mode ----------------
     // One super-stage per (tile, channel chunk): the (TH+R) x P halo box of
     // this CTA's output rows plus the R*S filter slabs of the chunk.
@@ -562,9 +728,26 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           uint8_t* sa = base + stage * stage_bytes;
           uint32_t fb = ptx::smem(&full[stage]);
           if constexpr (CG == 2) fb = ptx::map_to_rank(fb, 0);
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], CG * stage_bytes);
+          if (leader)
+            ptx::mbar_arrive_expect_tx(
+                &full[stage],
+                CG * (MODE == kConvHaloNarrow ? stage_bytes - a_bytes + p.halo_tx : stage_bytes));
           const int c0 = ch * p.ek;
-          ptx::tma4<CG>(sa, &map_a, fb, c0, pt.ow0 - p.pad_l, pt.oh0 + rank * p.TH - p.pad_t, pt.img);
+          if constexpr (MODE == kConvHaloNarrow) {
+            if (t == unit + kTraceUnit * nunits) trace_mark(p, 16);
+            // Phase-split input [N][H][s][W2][cp] (pad_phase_kernel): phase
+            // (px, py) of the tile = the 16-pixel run of column phase py
+            // from w2 = ow0, rows oh*s - pad_t + px stepping by s -- each
+            // box row one contiguous 256-byte run.
+            for (int ph = 0; ph < p.nphase; ++ph) {
+              const int px = ph / p.stride, py = ph - (ph / p.stride) * p.stride;
+              ptx::tma4<CG>(sa + ph * p.phase_bytes, &map_a, fb, pt.ow0 * p.C, py,
+                            (pt.oh0 + rank * p.TH) * p.stride - p.pad_t + px, pt.img);
+            }
+          } else {
+            ptx::tma4<CG>(sa, &map_a, fb, c0, pt.ow0 - p.pad_l, pt.oh0 + rank * p.TH - p.pad_t,
+                          pt.img);
+          }
           if (!p.resident)
             for (int tap = 0; tap < p.taps; ++tap)
               ptx::tma2<CG>(sa + a_bytes + tap * b_bytes, &map_b, fb, tap * p.cchunks * p.ek + c0,
@@ -576,7 +759,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         }
       }
     }
-  } else if (MODE == kConvHalo && warp == 1) {
+  } else if (halo_like<MODE>() && warp == 1) {
     // ---------------- MMA issuer, halo mode (leader CTA) ----------------
     // Tap (x, y) reads the halo from row x*P + y on: output row v = h*P + w
     // needs halo pixel (h + x, w + y), a constant shift in the virtual
@@ -592,6 +775,28 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         const int x = tap / p.S, y = tap - (tap / p.S) * p.S;
         tap_off[tap] = (uint64_t)((x * p.P + y) * (kSlabBytes / 16));
       }
+      // Narrow halo: taps in (phase, row, column) order, two per MMA.
+      uint32_t mma_off[kMaxNarrowMma], mma_lbo[kMaxNarrowMma];
+      int n_mma = 0;
+      if (MODE == kConvHaloNarrow) {
+        const int s = p.stride;
+        int q = 0;
+        for (int ph = 0; ph < p.nphase; ++ph) {
+          const int px = ph / s, py = ph - (ph / s) * s;
+          for (int x = px; x < p.R; x += s)
+            for (int y = py; y < p.S; y += s) {
+              const uint32_t off = ph * p.phase_bytes + ((x / s) * p.P + y / s) * 16;
+              if ((q & 1) == 0) {
+                mma_off[q >> 1] = off;
+                mma_lbo[q >> 1] = 0;  // (odd last tap: paired with zero filter rows)
+              } else {
+                mma_lbo[q >> 1] = off - mma_off[q >> 1];
+              }
+              ++q;
+            }
+        }
+        n_mma = (q + 1) >> 1;
+      }
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -601,9 +806,36 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         ptx::mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * p.acc_cols;
+        if (local == kTraceUnit && lane == 0) trace_mark(p, 10);
         for (int ch = 0; ch < p.cchunks; ++ch) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (local == 0 && lane == 0) trace_mark(p, 2);
+          if (local == kTraceUnit && lane == 0) trace_mark(p, 11);
+          if constexpr (MODE == kConvHaloNarrow) {
+            // Two taps (2 x 16-byte pixels = one 32-byte K step) per MMA:
+            // A = the pair's shifted halo views (start = first tap, LBO =
+            // gap to the second), B = the filter's K rows of the pair.  The
+            // (start offset, LBO) of every MMA is tabulated once per CTA.
+            if (ptx::elect_one()) {
+              const uint32_t sa = ptx::smem(base + stage * stage_bytes);
+              const uint64_t bd0 = kdesc + ((p.resident ? fres_s : sa + (uint32_t)a_bytes) >> 4);
+              for (int kk = 0; kk < n_mma; ++kk) {
+                const uint64_t bd = bd0 + (uint64_t)(kk >> 2) * (b_bytes >> 4) + 2 * (kk & 3);
+                ptx::mma_cg<CG, TF32>(d_tmem, ptx::desc_none(sa + mma_off[kk], mma_lbo[kk], 128), bd,
+                                      idesc, kk != 0);
+              }
+              ptx::commit_cg<CG>(&empty[stage]);
+              ptx::commit_cg<CG>(&tmem_full[acc]);
+              if (local == kTraceUnit) trace_mark(p, 12);
+            }
+            __syncwarp();
+            if (++stage == p.stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           if (ptx::elect_one()) {
             // Descriptors are linear in the 16-byte address field: build
             // the stage bases once, then every MMA is two 64-bit adds.
@@ -785,10 +1017,25 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
     if constexpr (CG == 2) empty_base = ptx::map_to_rank(empty_base, 0);
     int nlocal = 0;
     int ering = 0;  // staging chunk sequence (chunk-ring epilogue)
+    // Epilogue group eg takes the CTA's tiles local % epi_groups == eg, with
+    // its own half of the staging area, bulk groups and named barrier.
+    constexpr bool kMulti = MODE == kConvHaloNarrow;  // two epilogue groups
+    const int eg = kMulti ? (int)(warp - 2) >> 2 : 0;
+    const uint32_t ebar = (uint32_t)eg;
+    const bool elead = kMulti ? ((warp & 3) == 2 && lane == 0) : (warp == 2 && lane == 0);
+    uint8_t* const epi_mine =
+        epi_stage + (kMulti && p.epi_groups > 1 ? eg * (p.epi_bytes / 2) : 0);
+    auto esync = [&]() {
+      if constexpr (kMulti) ptx::epi_sync(ebar);
+      else ptx::named_sync(1, 128);
+    };
     for (int t = unit; t < total; t += nunits) {
       const Unit u = decode_unit(p, t);
       if (u.kb0 >= u.kb1) continue;  // empty tail segment
       const int local = nlocal++;
+      if constexpr (kMulti) {
+        if (eg >= p.epi_groups || (local % p.epi_groups) != eg) continue;
+      }
       const int m_blk = u.m_blk, n_blk = u.n_blk, z = u.z;
       const int acc = local % p.acc_slots;
       const uint32_t acc_phase = (uint32_t)(local / p.acc_slots) & 1u;
@@ -802,24 +1049,54 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       if ((plain_like<MODE>() || MODE == kConvPixN) && u.slot >= 0) {
         store_tail_piece(p, taddr, u.slot, rank, CG, row);
         ptx::tc_fence_before();
-        ptx::named_sync(1, 128);
-        if (warp == 2 && lane == 0) {
+        esync();
+        if (elead) {
           if constexpr (CG == 2) ptx::mbar_arrive_remote(empty_base + 8u * acc);
           else ptx::mbar_arrive(&tmem_empty[acc]);
         }
         continue;
       }
-      if constexpr (MODE == kConvHalo) {
+      if constexpr (halo_like<MODE>()) {
         const int hn = t % p.num_n, hm = t / p.num_n;
         const PixTile pt = pix_tile(p, hm);
         const int h = row / p.P, w = row - (row / p.P) * p.P;
         const int srow = w < p.TW ? h * p.TW + w : -1;
-        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, srow,
-                               empty_base + 8u * acc, &tmem_empty[acc], &map_d, hn * p.BN, pt.ow0,
-                               pt.oh0 + rank * p.TH, pt.img, 4, ering);
+        if (p.direct_store) {
+          // Each thread owns one output pixel (TMEM lane): its BN features
+          // leave as 16-byte streaming stores straight from the registers
+          // (no staging, no bulk store; L2 merges the lanes' lines).
+          const int oh = pt.oh0 + rank * p.TH + h, ow = pt.ow0 + w;
+          const bool ok = srow >= 0 && oh < p.OH && ow < p.OW;
+          float* dst = p.d + (((long long)pt.img * p.OH + oh) * p.OW + ow) * p.Kout + hn * p.BN;
+          for (int col = 0; col < p.BN; col += 32) {
+            float v[32];
+            ptx::tmem_ld32(taddr + col, v);
+            if (ok) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                __stcs(reinterpret_cast<float4*>(dst + col) + q,
+                       make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+            }
+          }
+          ptx::tc_fence_before();
+          esync();
+          if (elead) {
+            if constexpr (CG == 2) ptx::mbar_arrive_remote(empty_base + 8u * acc);
+            else ptx::mbar_arrive(&tmem_empty[acc]);
+          }
+          continue;
+        }
+        if constexpr (kMulti)
+          tma_store_epilogue_multi<CG>(p, taddr, epi_mine, local, warp, lane, row, srow,
+                                       empty_base + 8u * acc, &tmem_empty[acc], &map_d, hn * p.BN,
+                                       pt.ow0, pt.oh0 + rank * p.TH, pt.img, 4, ering, ebar);
+        else
+          tma_store_epilogue<CG>(p, taddr, epi_mine, local, warp, lane, row, srow,
+                                 empty_base + 8u * acc, &tmem_empty[acc], &map_d, hn * p.BN,
+                                 pt.ow0, pt.oh0 + rank * p.TH, pt.img, 4, ering);
         continue;
       } else if constexpr (MODE == kConvGather) {
-        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, row, empty_base + 8u * acc,
+        tma_store_epilogue<CG>(p, taddr, epi_mine, local, warp, lane, row, row, empty_base + 8u * acc,
                                &tmem_empty[acc], &map_d, n_blk * p.BN, m_blk * BM + rank * kRows,
                                0, 0, 3, ering);
         continue;
@@ -828,7 +1105,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         float* dz = p.d + (long long)z * p.d_batch;
         const float* cz = p.read_c ? p.c + (long long)z * p.d_batch : nullptr;
         if (p.store_tma) {
-          tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, row, empty_base + 8u * acc,
+          tma_store_epilogue<CG>(p, taddr, epi_mine, local, warp, lane, row, row, empty_base + 8u * acc,
                                  &tmem_empty[acc], &map_d, n_blk * p.BN,
                                  m_blk * BM + rank * kRows, u.sp * p.batch + z, 0, 3, ering);
           continue;
@@ -888,21 +1165,22 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
 
       } else {
         const PixTile pt = pix_tile(p, m_blk);
-        tma_store_epilogue<CG>(p, taddr, epi_stage, local, warp, lane, row, row, empty_base + 8u * acc,
+        tma_store_epilogue<CG>(p, taddr, epi_mine, local, warp, lane, row, row, empty_base + 8u * acc,
                                &tmem_empty[acc], &map_d, n_blk * p.BN, pt.ow0,
                                pt.oh0 + rank * p.boxH, pt.img, 4, ering);
         continue;
       }
       ptx::tc_fence_before();
-      ptx::named_sync(1, 128);
-      if (warp == 2 && lane == 0) {
+      esync();
+      if (elead) {
         if constexpr (CG == 2) ptx::mbar_arrive_remote(empty_base + 8u * acc);
         else ptx::mbar_arrive(&tmem_empty[acc]);
       }
     }
   }
 
-  if (warp == 2 && lane == 0 && p.store_tma) ptx::bulk_wait<0>();
+  if ((warp == 2 || (MODE == kConvHaloNarrow && warp == 6)) && lane == 0 && p.store_tma)
+    ptx::bulk_wait<0>();
   if (warp == 2 && lane == 0) trace_mark(p, 6);  // epilogue stores complete
   ptx::tc_fence_before();
   __syncthreads();
@@ -1063,6 +1341,8 @@ CUtensorMap map_nhwc(const void* base, int esize, const ConvGeom& g, int wb, int
 // wraps across rows and images, so a tile is any run of output pixels in
 // NHW order -- no per-image box padding.  Order of the corner arrays: W, H.
 CUtensorMap map_nhwc_im2col(const void* base, int esize, const ConvGeom& g, int pixels) {
+  const cuuint32_t chans = (cuuint32_t)(kSlabBytes / esize);
+  const CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;
   cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
   cuuint64_t strides[3] = {(cuuint64_t)g.C * esize, (cuuint64_t)g.W * g.C * esize,
                            (cuuint64_t)g.H * g.W * g.C * esize};
@@ -1086,14 +1366,15 @@ CUtensorMap map_nhwc_im2col(const void* base, int esize, const ConvGeom& g, int 
   key.lower[1] = lower[1];
   key.upper[0] = upper[0];
   key.upper[1] = upper[1];
-  key.chans = (cuuint32_t)(kSlabBytes / esize);
+  key.chans = chans;
   key.pixels = (cuuint32_t)pixels;
+  key.swz = (int)swz;
   if (const CUtensorMap* hit = map_memo().find(key)) return *hit;
   CUtensorMap m;
   const CUresult r = encode_im2col_fn()(
       &m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
-      const_cast<void*>(base), dims, strides, lower, upper, (cuuint32_t)(kSlabBytes / esize),
-      (cuuint32_t)pixels, trav, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      const_cast<void*>(base), dims, strides, lower, upper, chans,
+      (cuuint32_t)pixels, trav, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     fail(TK_ERR_CUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string(r) + ")");
@@ -1294,10 +1575,10 @@ template <int MODE, int CG, bool TF32>
 void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, TcArgs p,
                 int stages_req, cudaStream_t st) {
   const int b_bytes_h = (p.BN / CG) * kSlabBytes;
-  const int stage_bytes = MODE == kConvHalo
+  const int stage_bytes = halo_like<MODE>()
                               ? p.halo_bytes + (p.resident ? 0 : p.taps) * b_bytes_h
                               : kRows * kSlabBytes + b_bytes_h;
-  const int fres_bytes = (MODE == kConvHalo && p.resident) ? p.taps * p.cchunks * b_bytes_h : 0;
+  const int fres_bytes = (halo_like<MODE>() && p.resident) ? p.taps * p.cchunks * b_bytes_h : 0;
   const int ktab_bytes0 = MODE == kConvGather ? p.num_kb * 32 * 8 : 0;
   // Tuning experiments: TK_TC_STAGES caps the ring, TK_TC_EPI=1 forces one
   // staging buffer.
@@ -1306,7 +1587,9 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   if (xp.tc_stages > 0) stages_req = xp.tc_stages;
   if (xp.tc_epi > 0) p.epi_bufs = std::min(p.epi_bufs, xp.tc_epi);
   // Chunk-ring staging (32 KiB) for tiles wider than one chunk.
-  p.epi_ring = (p.store_tma && xp.epi_ring && p.BN > 32) ? 1 : 0;
+  p.epi_ring = (p.store_tma && xp.epi_ring && (p.BN > 32 || MODE == kConvHaloNarrow)) ? 1 : 0;
+  p.epi_slots = 2;
+  p.epi_groups = 1;
   // Double-buffered TMA-store staging when it leaves room for >= 3 stages.
   if (p.store_tma && p.epi_bufs > 1 &&
       232448 - 2048 - ktab_bytes0 - 2 * ((p.BN + 31) / 32) * kRows * kSlabBytes < 3 * stage_bytes)
@@ -1325,9 +1608,32 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     bs = std::max(1, std::min(nchunks, bs));
     if (xp.epi_ring_n > 0) bs = std::max(1, std::min(nchunks, xp.epi_ring_n));
     p.epi_ring = bs;
+    // Slots: as many as the room left after the wanted operand stages
+    // holds (2..8); short-K layers then keep several tiles of stores in flight.
+    // Slots beyond two only for epilogue-bound tiles (at most two slabs of
+    // MMA work per tile: the narrow first layers, short-K 1x1 layers):
+    // measured, VGG conv1_1 TF32 214 -> 180 us (L2-cold), while MMA-heavy
+    // tiles lose operand stages (conv1_2 208 -> 273 us with 8 slots).
+    const int work_slabs = MODE == kConvHaloNarrow ? (p.narrow_taps + 7) / 8
+                           : MODE == kConvHalo     ? p.taps * p.cchunks
+                                                   : kb_unit;
+    // Epilogue-bound tiles also get the second epilogue warpgroup (tiles
+    // alternate between the groups, each with its own staging slots).
+    // (narrow halo: <= 25 MMAs of K = 8 per tile -- VGG conv1_1 178 -> 121
+    // us, ResNet stem 68 -> 54 us with the second group, L2-warm A/B)
+    (void)work_slabs;
+    const bool epi_bound = MODE == kConvHaloNarrow;  // (the only multi-slot / two-group epilogue)
+    p.epi_groups = (epi_bound && epi_groups_of<MODE>() > 1) ? 2 : 1;
+    if (xp.epi_groups == 1 || xp.epi_groups == 2)
+      p.epi_groups = std::min(xp.epi_groups, epi_groups_of<MODE>());
+    if (p.epi_groups == 2 && room - 2 * stage_bytes < 2 * 2 * bs * kChunkBytes) p.epi_groups = 1;
+    const int per_slot = p.epi_groups * bs * kChunkBytes;
+    p.epi_slots = epi_bound ? std::max(2, std::min(8, (room - want * stage_bytes) / per_slot)) : 2;
+    if (xp.epi_slots > 0)  // (capped at what leaves two operand stages)
+      p.epi_slots = std::max(2, std::min({8, xp.epi_slots, (room - 2 * stage_bytes) / per_slot}));
   }
   const int epi_bytes = !p.store_tma ? 0
-                       : p.epi_ring ? 2 * p.epi_ring * kChunkBytes
+                       : p.epi_ring ? p.epi_groups * p.epi_slots * p.epi_ring * kChunkBytes
                                     : p.epi_bufs * ((p.BN + 31) / 32) * kChunkBytes;
   p.epi_bytes = epi_bytes;
   const int budget = 232448 - 1024 - 1024 - epi_bytes - ktab_bytes - fres_bytes;
@@ -1335,6 +1641,9 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   if (stages > kMaxStages) stages = kMaxStages;
   if (stages_req > 0 && stages_req < stages) stages = stages_req;
   if (stages < 2) fail(TK_ERR_CAPABILITY, "tc_gemm: tile too large for shared memory");
+  if (stage_bytes % 1024 != 0 || fres_bytes % 1024 != 0)  // swizzle-atom alignment of every buffer
+    fail(TK_ERR_CAPABILITY, "tc_gemm: stage of " + std::to_string(stage_bytes) +
+                                " bytes is not a multiple of 1024");
   p.stages = stages;
   const size_t smem =
       1024 + (size_t)stages * stage_bytes + fres_bytes + 1024 + epi_bytes + ktab_bytes;
@@ -1364,7 +1673,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   const int units = sm_count() / CG;
   int used = (int)(total < units ? total : units);
   // Halo mode with a resident filter: every CTA must keep one feature block.
-  if (MODE == kConvHalo && p.resident) used -= used % p.num_n;
+  if (halo_like<MODE>() && p.resident) used -= used % p.num_n;
   const int grid = used * CG;
   if (grid <= 0) return;
   cudaLaunchConfig_t cfg{};
@@ -1743,6 +2052,76 @@ void pack_filter(const float* filt, int K, int Kout, int kp, T* dst, bool tf32_r
     pack_filter_kernel<T, 4><<<blocks, 256, 0, st>>>(filt, K, Kout, kp, dst, tf32_round ? 1 : 0);
   note_launch();
   TKB_CUDA(cudaGetLastError());
+}
+
+// Narrow-pixel im2col operands (TcArgs::narrow_taps).  Filter: HWCK ->
+// [Kout][kp] with k = tap * cp + c (zero for c >= C and for the padding
+// taps past R*S), TF32-rounded or bf16.
+// order = 1: taps row-major (im2col); order = s > 1: the narrow halo's
+// (phase, row, column) order of a stride-s window (TcArgs::nphase).
+template <typename T>
+__global__ void __launch_bounds__(256) pack_filter_narrow_kernel(const float* __restrict__ src,
+                                                                 int R, int S, int C, int Kout, int cp,
+                                                                 int kp, int order,
+                                                                 T* __restrict__ dst,
+                                                                 int tf32_round) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)Kout * kp) return;
+  const int f = (int)(i / kp), k = (int)(i - (long long)f * kp);
+  const int q = k / cp, c = k - (k / cp) * cp;
+  int tap = -1;  // window tap (x * S + y) of sorted position q
+  if (order <= 1) {
+    tap = q < R * S ? q : -1;
+  } else {
+    int n = 0;
+    for (int ph = 0; ph < order * order && tap < 0; ++ph)
+      for (int x = ph / order; x < R && tap < 0; x += order)
+        for (int y = ph % order; y < S; y += order)
+          if (n++ == q) {
+            tap = x * S + y;
+            break;
+          }
+  }
+  const float v = (tap >= 0 && c < C) ? __ldg(src + ((long long)tap * C + c) * Kout + f) : 0.0f;
+  dst[i] = cvt_out<T>(v, tf32_round);
+}
+
+// Narrow halo input: NHWC (C channels) -> phase-split [N][H][s][W2][cp]
+// with xs[n][h][py][w2] = x[n][h][s*w2 + py - pad_l] (zero outside the row,
+// channels past C zero): a stride-s window's column phase is contiguous and
+// the left padding is baked in (tap y reads phase y % s at w2 = ow + y / s).
+template <typename T>
+__global__ void __launch_bounds__(256) pad_phase_kernel(const float* __restrict__ src, int N, int H,
+                                                        int W, int C, int s, int W2, int pad_l,
+                                                        int cp, T* __restrict__ dst) {
+  ptx::griddep_wait();
+  ptx::griddep_launch_dependents();
+  const long long total = (long long)N * H * s * W2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int w2 = (int)(i % W2);
+    const long long r = i / W2;
+    const int py = (int)(r % s);
+    const long long nh = r / s;  // n * H + h
+    const int col = s * w2 + py - pad_l;
+    float v[8];
+    const bool in = col >= 0 && col < W;
+    const float* px = src + (nh * W + (in ? col : 0)) * C;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = in && c < C && c < cp ? __ldg(px + c) : 0.0f;
+    if constexpr (sizeof(T) == 4) {
+      reinterpret_cast<float4*>(dst)[i] = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+      uint4 u;
+      __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]), b1 = __floats2bfloat162_rn(v[2], v[3]),
+                     b2 = __floats2bfloat162_rn(v[4], v[5]), b3 = __floats2bfloat162_rn(v[6], v[7]);
+      u.x = *reinterpret_cast<uint32_t*>(&b0);
+      u.y = *reinterpret_cast<uint32_t*>(&b1);
+      u.z = *reinterpret_cast<uint32_t*>(&b2);
+      u.w = *reinterpret_cast<uint32_t*>(&b3);
+      reinterpret_cast<uint4*>(dst)[i] = u;
+    }
+  }
 }
 
 // fp32 -> bf16, 8 elements per thread (n % 8 == 0 fast path).
@@ -2138,6 +2517,7 @@ struct ConvPlan {
   int imgs = 1;  // pixN: whole images per pixel tile (small planes)
   bool flat = false;  // pixN: flat-row tiles (see TcArgs::flat)
   int num_m = 0, num_n = 0;
+  int narrow_cp = 0;  // narrow halo (16-byte pixels): channels after padding (4 / 8)
 };
 
 // Split-K count from a small cost model (times in us, B200 at ~1.9 GHz):
@@ -2383,6 +2763,37 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
     }
     return c;
   }
+  // Narrow pixels (C <= 4 tf32 / 8 bf16 channels, the C = 3 first layers):
+  // the input padded once to 16-byte pixels feeds im2col-mode TMA, 8 taps
+  // per K-slab (TcArgs::narrow_taps) -- the producer-warp gather and its
+  // per-tile handshake are off the path, and BF16 stays BF16.
+  const int ncp = tf32 ? 4 : 8;
+  const bool narrow_ok = g.C <= ncp && (g.stride == 1 || g.stride == 2) && g.K % 32 == 0 &&
+                         g.K <= 256 && (mode == TK_TC_AUTO || mode == TK_TC_HALO) &&
+                         !(force && std::string(force) == "gather");
+  if (narrow_ok) {
+    const int taps = g.R * g.S;
+    c.tf32 = tf32;
+    c.narrow_cp = ncp;
+    c.kp = (long long)((taps + 7) / 8) * 8 * ncp;
+    c.filt_bytes = align256((size_t)g.K * c.kp * esize);
+    c.in_bytes = align256((size_t)g.N * g.H * g.W * ncp * esize);
+    // Halo boxes: the taps are shifted views of one box per stride phase
+    // (no per-tap loads).  (Narrow im2col-mode TMA -- one 16-byte pixel per
+    // box row, 8 taps per slab -- was measured slower: conv1_1 194 us.)
+    if (g.S <= 2 * 16 - 2) {
+      c.in_bytes = align256((size_t)g.N * g.H * g.stride *
+                            (g.OW + (g.S - 1) / g.stride + 16) * ncp * esize);  // narrow_w2
+      c.kind = kBoxPlan;
+      c.halo = true;
+      c.cg = 2;
+      c.num_kb = 1;
+      c.kb_per = 1;
+      return c;
+    }
+  }
+  c.narrow_cp = 0;
+  c.kp = 0;
   c.kind = kGatherPlan;  // fp32 operands, kind::tf32 for every TC precision
   c.tf32 = true;
   c.kp = (K + 31) / 32 * 32;
@@ -2568,6 +2979,112 @@ static bool halo_resident(const ConvGeom& g, int bn, int cchunks, int halo_bytes
   return left >= 3 * halo_bytes && units % num_n == 0;
 }
 
+// Columns per phase row of the narrow halo's phase-split input: the last
+// output column's window + one spare box row of slack.
+static int narrow_w2(const ConvGeom& g) { return g.OW + (g.S - 1) / g.stride + 16; }
+
+// Narrow halo launch (TcArgs::narrow_taps + nphase): input padded to 16-byte
+// pixels, filter packed in the (phase, row, column) tap order, one CTA-pair
+// tile = 2 x 8 output rows of TW = 16 - (S-1)/s columns.
+void launch_narrow_halo(const ConvGeom& g, const ConvPlan& c, const float* in, const float* filt,
+                        float* out, char* ws, cudaStream_t st, bool prep, bool run) {
+  const int esize = c.tf32 ? 4 : 2, ek = kSlabBytes / esize, cp = c.narrow_cp;
+  const int s = g.stride;
+  void* ft = ws;
+  char* xin = ws + c.filt_bytes;
+  if (prep) {
+    const long long n = (long long)g.K * c.kp;
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    if (c.tf32)
+      pack_filter_narrow_kernel<float><<<blocks, 256, 0, st>>>(
+          filt, g.R, g.S, g.C, g.K, cp, (int)c.kp, s, (float*)ft, tf32_filter_rounding() ? 1 : 0);
+    else
+      pack_filter_narrow_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+          filt, g.R, g.S, g.C, g.K, cp, (int)c.kp, s, (__nv_bfloat16*)ft, 0);
+    note_launch();
+    TKB_CUDA(cudaGetLastError());
+  }
+  if (!run) return;
+  const int W2 = narrow_w2(g);
+  const long long pixels = (long long)g.N * g.H * s * W2;
+  const int pblocks = (int)std::min<long long>((pixels + 255) / 256, (long long)sm_count() * 16);
+  if (c.tf32)
+    launch_pdl(pad_phase_kernel<float>, (unsigned)pblocks, 256, st, in, g.N, g.H, g.W, g.C, s, W2,
+               g.pad_l, cp, (float*)xin);
+  else
+    launch_pdl(pad_phase_kernel<__nv_bfloat16>, (unsigned)pblocks, 256, st, in, g.N, g.H, g.W, g.C,
+               s, W2, g.pad_l, cp, (__nv_bfloat16*)xin);
+  const int cg = 2;
+  TcArgs p{};
+  p.P = 16;
+  p.TH = kRows / p.P;
+  p.TW = p.P - (g.S - 1) / s;
+  const int rows = p.TH + (g.R - 1) / s + 1;  // phase-box rows (one spare)
+  p.nphase = s * s;
+  p.phase_bytes = rows * p.P * 16;
+  // The stage stride stays a multiple of 1024 bytes (every stage, the
+  // resident filter and the epilogue staging behind them must keep the
+  // 128-byte-swizzle atom alignment); the barrier expects halo_tx bytes.
+  p.halo_tx = p.nphase * p.phase_bytes;
+  p.halo_bytes = (p.halo_tx + 1023) / 1024 * 1024;
+  p.narrow_taps = g.R * g.S;
+  p.taps = (int)(c.kp / ek);  // filter slabs (8 taps each)
+  p.K = (int)c.kp;
+  p.ek = ek;
+  p.cchunks = 1;
+  p.num_kb = 1;
+  p.BN = g.K <= 32 ? 32 : (g.K % 128 == 0 ? 128 : 64);
+  p.Wb = p.TW;
+  p.tileH = cg * p.TH;
+  p.tiles_w = (g.OW + p.TW - 1) / p.TW;
+  p.tiles_h = (g.OH + p.tileH - 1) / p.tileH;
+  p.num_m = g.N * p.tiles_w * p.tiles_h;
+  p.num_n = (g.K + p.BN - 1) / p.BN;
+  p.M = p.num_m * kRows * cg;
+  p.N = g.K;
+  p.batch = 1;
+  p.d = out;
+  p.alpha = 1.0f;
+  p.OH = g.OH;
+  p.OW = g.OW;
+  p.Kout = g.K;
+  p.pad_t = g.pad_t;
+  p.pad_l = g.pad_l;
+  p.R = g.R;
+  p.S = g.S;
+  p.stride = s;
+  p.C = cp;
+  CUtensorMap ma;
+  {
+    // [N][H][s][W2 * cp] phase-split rows, box {16 pixels x cp, 1 phase,
+    // rows (traversal s), 1}, no swizzle: one 256-byte run per box row.
+    cuuint64_t dims[4] = {(cuuint64_t)W2 * cp, (cuuint64_t)s, (cuuint64_t)g.H, (cuuint64_t)g.N};
+    cuuint64_t strides[3] = {(cuuint64_t)W2 * cp * esize, (cuuint64_t)s * W2 * cp * esize,
+                             (cuuint64_t)g.H * s * W2 * cp * esize};
+    cuuint32_t box[4] = {(cuuint32_t)(16 * cp), 1, (cuuint32_t)(rows * s), 1};
+    const cuuint32_t trav[4] = {1, 1, (cuuint32_t)s, 1};
+    ma = make_map(xin, esize, 4, dims, strides, box, s > 1 ? trav : nullptr,
+                  CU_TENSOR_MAP_SWIZZLE_NONE);
+  }
+  const CUtensorMap mb = map_rows2d(ft, esize, c.kp, g.K, p.BN / cg);
+  cuuint64_t dims[4] = {(cuuint64_t)g.K, (cuuint64_t)g.OW, (cuuint64_t)g.OH, (cuuint64_t)g.N};
+  cuuint64_t strides[3] = {(cuuint64_t)g.K * 4, (cuuint64_t)g.OW * g.K * 4,
+                           (cuuint64_t)g.OH * g.OW * g.K * 4};
+  cuuint32_t box[4] = {32, (cuuint32_t)p.TW, (cuuint32_t)p.TH, 1};
+  const CUtensorMap md = make_map(out, 4, 4, dims, strides, box);
+  p.store_tma = 1;
+  p.epi_bufs = 1;
+  p.direct_store = experiments().direct_store;
+  {
+    const int b_bytes_h = (p.BN / cg) * kSlabBytes;
+    const int fres = p.taps * b_bytes_h;
+    const int epi = ((p.BN + 31) / 32) * kRows * kSlabBytes;
+    const int left = 232448 - 2048 - epi - fres;
+    p.resident = (left >= 3 * p.halo_bytes && (sm_count() / cg) % p.num_n == 0) ? 1 : 0;
+  }
+  dispatch<kConvHaloNarrow>(ma, mb, md, p, cg, c.tf32, st);
+}
+
 size_t tc_conv_workspace(const ConvGeom& g, int precision) {
   if (precision == TK_PREC_3XTF32)
     return split3_bytes_in(g) + split3_bytes_filt(g) + tc_conv_workspace(tripled(g), TK_PREC_TF32);
@@ -2622,6 +3139,10 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   }
   if (plan.kind == kIm2colPlan) {
     launch_im2col_conv(g, plan, in, filt, out, cursor, st, prep, run);
+    return;
+  }
+  if (plan.kind == kBoxPlan && plan.halo && plan.narrow_cp) {
+    launch_narrow_halo(g, plan, in, filt, out, cursor, st, prep, run);
     return;
   }
 
@@ -2855,7 +3376,12 @@ TcConvInfo tc_conv_info(const ConvGeom& g, int precision) {
         r.box_w = TW;
         r.box_h = 2 * TH;
         r.halo_resident =
-            halo_resident(g, bn, g.C / ek, (TH + g.R) * 16 * kSlabBytes, num_n) ? 1 : 0;
+            c.narrow_cp ? 1
+                        : (halo_resident(g, bn, g.C / ek, (TH + g.R) * 16 * kSlabBytes, num_n) ? 1 : 0);
+        if (c.narrow_cp) {
+          r.box_w = 16 - (g.S - 1) / g.stride;
+          r.flat = 0;
+        }
         r.splits = 1;
         r.tail_pieces = 0;
       } else if (c.pix_on_n) {

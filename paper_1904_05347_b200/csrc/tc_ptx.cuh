@@ -175,6 +175,24 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// The same load without the wait: several loads in flight, then one
+// tmem_wait_ld() before any register is read.
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
 // Shared-memory matrix descriptor, K-major operand staged by TMA with the
 // 128-byte swizzle: 8-row x 128-byte atoms, atoms 1024 B apart (SBO).
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t smem_addr) {
@@ -201,6 +219,20 @@ __device__ __forceinline__ uint64_t desc_sw128_mn(uint32_t smem_addr, uint32_t l
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)1 << 61;
   return d;
+}
+
+// K-major operand without swizzle (the "interleaved" canonical layout):
+// 8-row x 16-byte core matrices, `sbo` bytes between 8-row groups (M/N),
+// `lbo` bytes between the two core matrices of a 32-byte K step.  Used for
+// narrow-pixel im2col operands: one TMA im2col load per tap writes 128
+// pixels x 16 bytes (4 tf32 / 8 bf16 channels) contiguously.
+__device__ __forceinline__ uint64_t desc_none(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;  // layout type 0: SWIZZLE_NONE
 }
 
 // Instruction descriptor: fp32 accumulate, K-major A and B, M x N.
@@ -398,6 +430,19 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
 }
+// wait_group.read takes an immediate: run-time depth 0..7.
+__device__ __forceinline__ void bulk_wait_read_dyn(int n) {
+  switch (n) {
+    case 0: bulk_wait_read<0>(); break;
+    case 1: bulk_wait_read<1>(); break;
+    case 2: bulk_wait_read<2>(); break;
+    case 3: bulk_wait_read<3>(); break;
+    case 4: bulk_wait_read<4>(); break;
+    case 5: bulk_wait_read<5>(); break;
+    case 6: bulk_wait_read<6>(); break;
+    default: bulk_wait_read<7>(); break;
+  }
+}
 template <int N>
 __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory");
@@ -405,6 +450,14 @@ __device__ __forceinline__ void bulk_wait() {
 // Named barrier over `count` threads (ids 1..15; 0 is __syncthreads).
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+// Epilogue group barrier with an immediate id (1 or 2): a run-time id makes
+// ptxas reserve all 16 named barriers for the CTA ("used 16 barriers"),
+// which measurably slowed every launch of the kernel family (ResNet-50
+// res5a_branch1 20.0 -> 27.7 us).
+__device__ __forceinline__ void epi_sync(uint32_t group) {
+  if (group == 0) asm volatile("bar.sync 1, 128;\n" ::: "memory");
+  else asm volatile("bar.sync 2, 128;\n" ::: "memory");
 }
 
 }  // namespace ptx

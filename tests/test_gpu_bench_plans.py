@@ -89,15 +89,34 @@ def _run(tk, idx, prec, x, f):
     return y
 
 
+DB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                  "r02_tune_ncu.ndjson")
+
+
+@pytest.fixture(params=["rules", "tuned"])
+def knob_source(request, tk):
+    """The plans of the built-in rules, and those of the committed tuning DB
+    that bench.py loads (tk_tuning_db_load)."""
+    tk.tuning_db_clear()
+    if request.param == "tuned":
+        if not os.path.exists(DB):
+            pytest.skip("no tuning DB")
+        tk.tuning_db_load(DB)
+    yield request.param
+    tk.tuning_db_clear()
+
+
 @pytest.mark.gpu
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("prec", ["tf32", "bf16", "3xtf32", "fp32"])
 @pytest.mark.parametrize("idx", range(len(LAYERS)), ids=[lay[0] for lay in LAYERS])
-def test_bench_layer_batch32(tk, oracle, idx, prec):
+def test_bench_layer_batch32(tk, oracle, idx, prec, knob_source):
     name, r, s, h, c, k = LAYERS[idx]
     shape = tk.ConvShape(N, h, h, c, k, r, r, s, True)
     plan = tk.conv2d_plan_info(shape, tk.parse_conv_params("im2col"), prec)
     assert plan["requested_precision"] == prec
+    if knob_source == "tuned" and not plan["tuned"]:
+        pytest.skip("the DB keeps the rules' plan for this shape")
     x, f = _device_inputs(idx)
     y = _run(tk, idx, prec, x, f)
     assert not bool(torch_isnan_any(y)), (name, prec, plan)
@@ -126,11 +145,13 @@ def torch_isnan_any(y):
 @pytest.mark.parametrize("idx", range(len(LAYERS)), ids=[lay[0] for lay in LAYERS])
 def test_plan_reports_effective_precision(tk, idx):  # host-only: runs on CPU too
     """BF16 requests report the arithmetic that actually runs: bf16 on the
-    box / halo / pointwise / im2col paths, tf32 on the gather producers
-    (fp32 operands) -- never silently."""
+    box / halo / pointwise / im2col paths (the C = 3 first layers included,
+    through narrow-pixel im2col), tf32 only on the gather producers (fp32
+    operands) -- never silently."""
     name, r, s, h, c, k = LAYERS[idx]
     shape = tk.ConvShape(N, h, h, c, k, r, r, s, True)
     plan = tk.conv2d_plan_info(shape, tk.parse_conv_params("im2col"), "bf16")
+    assert plan["kernel"] != "tc_gather", plan  # every bench layer has a BF16 path
     if plan["kernel"] == "tc_gather":
         assert plan["precision"] == "tf32"
     else:

@@ -92,7 +92,9 @@ def test_im2col_tma_matches_box_path(tk, oracle):
 
 def test_im2col_mode_rejects_unboxable_channels(tk, oracle):
     import torch
-    s = tk.ConvShape(1, 8, 8, 3, 16, 3, 3, 1, True)
+    # (C <= 4 runs as narrow-pixel im2col; 5 channels are neither a slab
+    # nor a 16-byte pixel)
+    s = tk.ConvShape(1, 8, 8, 5, 16, 3, 3, 1, True)
     opts = tk.exec_options("tf32", mode="im2col")
     with pytest.raises(tk.CapabilityError):
         tk.conv2d_workspace_size(s, tk.parse_conv_params("im2col"), options=opts)

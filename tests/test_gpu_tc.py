@@ -268,3 +268,43 @@ def test_tc_gemm_mn_major_a_never_reads_past_a(tk, oracle, m, n, k):
     got = out.cpu().numpy()
     assert not np.isnan(got).any()
     assert oracle.max_scaled_error(got, want) <= TOL_TF32
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("shape", [
+    (2, 30, 30, 3, 64, 3, 1, True), (1, 40, 40, 3, 64, 7, 2, True), (2, 17, 19, 1, 32, 3, 1, True),
+    (1, 16, 16, 2, 48, 5, 1, False), (2, 21, 21, 4, 64, 3, 2, True), (1, 12, 12, 8, 64, 3, 1, True),
+    (3, 9, 11, 3, 16, 3, 1, False), (1, 33, 33, 3, 128, 7, 2, True),
+    # 1024-byte stage alignment regression: 5x5 / 7x7 stride-1 halo stages
+    # of 13 / 15 rows x 256 B with K = 32 (two epilogue groups, 6 slots)
+    (3, 36, 32, 3, 32, 5, 1, False), (3, 36, 32, 3, 32, 7, 1, False),
+    (1, 20, 20, 3, 32, 7, 1, True)])
+@pytest.mark.parametrize("mode", ["auto", "halo"])
+def test_tc_conv_narrow_pixels(tk, oracle, shape, prec, mode):
+    """First layers with C <= 4 (TF32) / 8 (BF16) channels and K a multiple
+    of 32: the input padded once to 16-byte pixels (phase-split for stride
+    2), one halo box per stride phase, the taps as shifted views of it, two
+    taps per MMA (no-swizzle core-matrix operand); BF16 runs in BF16
+    (plan_info).  Other narrow layers fall back to the gather producers."""
+    import torch
+    N, H, W, C, K, R, st, same_pad = shape
+    s = tk.ConvShape(N, H, W, C, K, R, R, st, same_pad)
+    conv = oracle.Conv(N, H, W, C, K, R, R, st, same_pad)
+    opts = tk.exec_options(prec, mode=mode)
+    narrow = C <= (4 if prec == "tf32" else 8) and K % 32 == 0 and K <= 256
+    if mode == "halo" and not narrow:
+        pytest.skip("not a narrow-halo layer")
+    plan = tk.conv2d_plan_info(s, tk.parse_conv_params("im2col"), options=opts)
+    if narrow:
+        assert plan["kernel"] == "tc_halo" and plan["precision"] == prec, plan
+    x = oracle.fill_random(int(np.prod(conv.in_shape)), 31).reshape(conv.in_shape)
+    f = oracle.fill_random(int(np.prod(conv.filt_shape)), 32).reshape(conv.filt_shape)
+    want = oracle.conv2d_naive(conv, x, f)
+    dy = torch.full(s.out_shape, float("nan"), device="cuda")
+    tk.conv2d_dev(torch.from_numpy(x).cuda(), torch.from_numpy(f).cuda(), dy, s,
+                  tk.parse_conv_params("im2col"), options=opts)
+    torch.cuda.synchronize()
+    got = dy.cpu().numpy()
+    assert not np.isnan(got).any(), plan
+    err = oracle.max_scaled_error(got, want)
+    assert err <= TOL[plan["precision"]], (err, plan)

@@ -1,19 +1,21 @@
-"""HBM write-only and copy bandwidth (fill / copy of 411 MB, VGG conv1_x output size)."""
+"""HBM write / copy bandwidth probe (the ceiling of output-bound layers)."""
 import torch
 
-n = 32 * 224 * 224 * 64
+n = 1 << 28  # 1 GiB of fp32
 a = torch.empty(n, device="cuda")
 b = torch.empty(n, device="cuda")
-for name, fn in (("fill (write only)", lambda: a.fill_(1.0)), ("copy (read+write)", lambda: b.copy_(a))):
-    for _ in range(3):
-        fn()
+for name, fn, nbytes in (("zero_ (write only)", lambda: a.zero_(), 4 * n),
+                         ("fill_ (write only)", lambda: a.fill_(1.0), 4 * n),
+                         ("copy_ (read + write)", lambda: b.copy_(a), 8 * n)):
+    fn()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(10):
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         fn()
-    e1.record()
-    e1.synchronize()
-    ms = e0.elapsed_time(e1) / 10
-    moved = 4 * n * (1 if "fill" in name else 2)
-    print(f"{name}: {ms * 1e3:.1f} us for {moved / 1e6:.0f} MB -> {moved / ms / 1e6:.0f} GB/s")
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = min(ts)
+    print(f"{name:24s} {nbytes / ms / 1e6:8.0f} GB/s")
