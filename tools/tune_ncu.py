@@ -23,7 +23,13 @@ Three passes, two GPU calls (ncu is one tool per call):
      CUDA-event timing of the shortlist (graph of [L2 eviction, run] x 4
      minus the eviction alone, as bench.py times layers); one NDJSON record
      per candidate in the reference's nine-key format plus precision,
-     tensor_pipe_pct, dram_pct, ncu_us.  tk_tuning_db_load picks the fastest
+     tensor_pipe_pct, dram_pct, ncu_us (all records: --db path with
+     "_all" before the extension).
+  4. CPU:          python tools/tune_ncu.py --curate profiles/r02_tune_ncu_all.ndjson \
+                       --db profiles/r02_tune_ncu.ndjson
+     the DB the library loads keeps a non-default record only where it beats
+     the built-in rule by >= 5% (isolated-layer wins below that measured no
+     better inside the stacks); tk_tuning_db_load then picks the fastest
      valid record per (problem, algorithm, precision).
 """
 from __future__ import annotations
@@ -246,9 +252,11 @@ def time_pass(short_path, db_path):
                "layer": c["layer"]}
         recs.append(rec)
         del ws
-    with open(db_path, "w") as fh:
+    all_path = db_path.replace(".ndjson", "_all.ndjson")
+    with open(all_path, "w") as fh:
         for r in recs:
             fh.write(json.dumps(r) + "\n")
+    curate(all_path, db_path)
     # summary: DB choice vs the built-in rule per (layer, precision)
     best = {}
     for r in recs:
@@ -263,11 +271,39 @@ def time_pass(short_path, db_path):
               f"(rules {a / 1e3:8.1f} us) tc {r['tensor_pipe_pct']:5.1f}% dram {r['dram_pct']:5.1f}%")
 
 
+MIN_GAIN = 0.05
+
+
+def curate(all_path, db_path):
+    """Keep, per (problem, precision), the built-in rule's record and the
+    fastest other record only if it beats the rule by MIN_GAIN."""
+    recs = [json.loads(ln) for ln in open(all_path) if ln.strip()]
+    groups = {}
+    for r in recs:
+        groups.setdefault((r["problem"], r["precision"]), []).append(r)
+    out = []
+    for (prob, prec), rs in sorted(groups.items()):
+        rule = [r for r in rs if r["config"] == f"im2col@{prec}"]
+        best = min(rs, key=lambda r: r["median_ns"])
+        if rule:
+            out.append(rule[0])
+            if best is not rule[0] and best["median_ns"] < (1 - MIN_GAIN) * rule[0]["median_ns"]:
+                out.append(best)
+        else:
+            out.append(best)
+    with open(db_path, "w") as fh:
+        for r in out:
+            fh.write(json.dumps(r) + "\n")
+    kept = sum(1 for r in out if not r["config"].endswith(("@tf32", "@bf16")))
+    print(f"curated DB: {len(out)} records, {kept} non-default choices (>= {MIN_GAIN:.0%} over the rule)")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--profile-pass", action="store_true")
     ap.add_argument("--shortlist", nargs=2, metavar=("NCU_CSV", "LAUNCHES_JSON"))
     ap.add_argument("--time", metavar="SHORTLIST_JSON")
+    ap.add_argument("--curate", metavar="ALL_NDJSON")
     ap.add_argument("--out", default="runs/tune_launches.json")
     ap.add_argument("--db", default="profiles/r02_tune_ncu.ndjson")
     args = ap.parse_args()
@@ -277,6 +313,8 @@ def main():
         shortlist(args.shortlist[0], args.shortlist[1], args.out)
     elif args.time:
         time_pass(args.time, args.db)
+    elif args.curate:
+        curate(args.curate, args.db)
     else:
         ap.print_help()
 
