@@ -131,6 +131,9 @@ def parse():
     ap.add_argument("--tuning-db", default=os.path.join(ROOT, "profiles", "r02_tune_ncu.ndjson"),
                     help="NDJSON tuning DB loaded into the library (tools/tune_ncu.py); "
                          "'none' = the built-in rules only")
+    ap.add_argument("--no-multi", action="store_true",
+                    help="skip the multi-GPU verification gather and the GEMM column-panel leg "
+                         "(profiling runs: the step's launches are then the last ones)")
     ap.add_argument("--no-layers", action="store_true",
                     help="skip the per-layer kernel timing (profiling runs: the step's launches "
                          "are then the last ones after the L2 flush)")
@@ -477,8 +480,8 @@ def main():
     vi = len(layers) - 1
     Lv = layers[vi]
     torch.cuda.synchronize()
-    parts = shard.gather_to(Lv["y"], 0)
-    if rank == 0:
+    parts = shard.gather_to(Lv["y"], 0) if not args.no_multi else []
+    if rank == 0 and not args.no_multi:
         same, worst = True, 0.0
         for r, part in enumerate(parts):
             xr = shard.seeded_images(Lv["hwc"], r * N, (r + 1) * N, 1234, vi, dev)
@@ -500,48 +503,49 @@ def main():
     # column-major C (the row-major formulation's M-panels), panel edges on
     # the 256-wide tensor-core tile, A replicated by broadcast, each rank's
     # B panel seeded per 256-column block.  Strong scaling: fixed total work.
-    gn = 8192
-    glo, ghi = shard.panel_range(gn, world, rank, 256)
-    ga = torch.rand(gn * gn, device=dev, generator=torch.Generator(device=dev).manual_seed(99)) * 2 - 1
-    shard.broadcast_(ga)
-    gb = shard.seeded_columns(gn, glo, ghi, 4242, 256, dev)
-    gc = torch.empty(gn * (ghi - glo), device=dev)
-    gshape = tk.GemmShape(gn, ghi - glo, gn)
-    for _ in range(2):
-        tk.gemm_dev(ga, gb, None, gc, gshape, None, precision="tf32", stream=stream)
-    gts = []
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for _ in range(5):
-        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a_.record(stream)
-        tk.gemm_dev(ga, gb, None, gc, gshape, None, precision="tf32", stream=stream)
-        b_.record(stream)
-        b_.synchronize()
-        gts.append(a_.elapsed_time(b_))
-    g_ms = float(np.median(gts))
-    g_rank = shard.all_gather_scalar(g_ms, device=dev)
-    g_max = max(g_rank)
-    panels = {"value": round(2 * gn ** 3 / (g_max * 1e-3) / 1e9, 1), "unit": "GFLOP/s",
-              "scaling": "strong", "ms_max_over_ranks": round(g_max, 4),
-              "rank_ms": [round(v, 4) for v in g_rank], "panel_cols": ghi - glo,
-              "config": f"C = A B, {gn}^3 TF32, column panels of C (A broadcast)"}
-    gparts = shard.gather_to(gc[: gn * 256].clone(), 0)  # first 256 columns of every panel
-    if rank == 0:
-        same = True
-        for r, part in enumerate(gparts):
-            rlo, rhi = shard.panel_range(gn, world, r, 256)
-            br = shard.seeded_columns(gn, rlo, rhi, 4242, 256, dev)
-            cr = torch.empty(gn * (rhi - rlo), device=dev)
-            tk.gemm_dev(ga, br, None, cr, tk.GemmShape(gn, rhi - rlo, gn), None, precision="tf32",
-                        stream=stream)
-            torch.cuda.synchronize()
-            same &= bool(torch.equal(cr[: gn * 256].view(torch.int32), part.view(torch.int32)))
-            del br, cr
-        panels["verify_first_256_cols_bitwise"] = same
-    multi["gemm8192_tf32_panels"] = panels
-    del ga, gb, gc, gparts
+    if not args.no_multi:
+        gn = 8192
+        glo, ghi = shard.panel_range(gn, world, rank, 256)
+        ga = torch.rand(gn * gn, device=dev, generator=torch.Generator(device=dev).manual_seed(99)) * 2 - 1
+        shard.broadcast_(ga)
+        gb = shard.seeded_columns(gn, glo, ghi, 4242, 256, dev)
+        gc = torch.empty(gn * (ghi - glo), device=dev)
+        gshape = tk.GemmShape(gn, ghi - glo, gn)
+        for _ in range(2):
+            tk.gemm_dev(ga, gb, None, gc, gshape, None, precision="tf32", stream=stream)
+        gts = []
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(5):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            tk.gemm_dev(ga, gb, None, gc, gshape, None, precision="tf32", stream=stream)
+            b_.record(stream)
+            b_.synchronize()
+            gts.append(a_.elapsed_time(b_))
+        g_ms = float(np.median(gts))
+        g_rank = shard.all_gather_scalar(g_ms, device=dev)
+        g_max = max(g_rank)
+        panels = {"value": round(2 * gn ** 3 / (g_max * 1e-3) / 1e9, 1), "unit": "GFLOP/s",
+                  "scaling": "strong", "ms_max_over_ranks": round(g_max, 4),
+                  "rank_ms": [round(v, 4) for v in g_rank], "panel_cols": ghi - glo,
+                  "config": f"C = A B, {gn}^3 TF32, column panels of C (A broadcast)"}
+        gparts = shard.gather_to(gc[: gn * 256].clone(), 0)  # first 256 columns of every panel
+        if rank == 0:
+            same = True
+            for r, part in enumerate(gparts):
+                rlo, rhi = shard.panel_range(gn, world, r, 256)
+                br = shard.seeded_columns(gn, rlo, rhi, 4242, 256, dev)
+                cr = torch.empty(gn * (rhi - rlo), device=dev)
+                tk.gemm_dev(ga, br, None, cr, tk.GemmShape(gn, rhi - rlo, gn), None, precision="tf32",
+                            stream=stream)
+                torch.cuda.synchronize()
+                same &= bool(torch.equal(cr[: gn * 256].view(torch.int32), part.view(torch.int32)))
+                del br, cr
+            panels["verify_first_256_cols_bitwise"] = same
+        multi["gemm8192_tf32_panels"] = panels
+        del ga, gb, gc, gparts
 
     # Per-layer device times of the conv kernels (after the timed steps; same
     # stream, CUDA events),
@@ -688,18 +692,18 @@ def main():
     # and output once, conv_oi's model).
     traffic, traffic_src = None, None
     import glob
-    profs = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_launches_{prec}.json")))
+    profs = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_launches_{prec}.json")))  # newest round
     prof = profs[-1] if profs else ""
     if prof:
         kern = json.load(open(prof))["kernels"]
         tb = sum(v["dram_bytes"] for k, v in kern.items()
                  if any(x in k for x in ("tc_gemm_kernel", "exact_gemm", "tail_reduce",
-                                         "splitk_reduce")))
+                                         "splitk_reduce", "pad_phase", "to_bf16")))
         traffic, traffic_src = int(tb), os.path.relpath(prof, ROOT)
     compulsory = sum(4 * (L["x"].numel() + L["f"].numel() + L["y"].numel()) for L in layers)
     roofline = {"bound": "tensor", "achieved": round(achieved_tf, 2), "peak": round(peak_tf, 1),
                 "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic,
-                "traffic_unit": "DRAM bytes per step, all conv launches (ncu dram__bytes_read+write)",
+                "traffic_unit": "DRAM bytes per step, all conv-path launches excl. the overlapped filter packs (ncu dram__bytes_read+write)",
                 "traffic_source": traffic_src, "compulsory_bytes": int(compulsory),
                 "kernel": "exact_gemm_loc_kernel" if prec == "fp32" else "tc_gemm_kernel (implicit-GEMM conv)",
                 "peak_source": peak_note}
