@@ -143,7 +143,9 @@ enum tk_kernel_kind {
   TK_KERNEL_TC_GATHER = 4,
   TK_KERNEL_TC_POINTWISE = 5,
   TK_KERNEL_TC_IM2COL = 6,
-  TK_KERNEL_WINOGRAD = 7      /* transforms + batched transform-domain GEMM */
+  TK_KERNEL_WINOGRAD = 7,     /* transforms + batched transform-domain GEMM */
+  TK_KERNEL_TC_HALO_NARROW = 8 /* C <= 16 bytes per pixel: padded 16-byte pixels, one
+                                  halo box per stride phase, two taps per MMA */
 };
 
 /* The plan of one convolution call (tk_conv2d_plan_info): what

@@ -118,7 +118,7 @@ class ConvPlanInfoC(C.Structure):
 
 
 KERNELS = {0: "exact_simt", 1: "tc_halo", 2: "tc_pixn", 3: "tc_pixm", 4: "tc_gather",
-           5: "tc_pointwise", 6: "tc_im2col", 7: "winograd"}
+           5: "tc_pointwise", 6: "tc_im2col", 7: "winograd", 8: "tc_halo_narrow"}
 PRECISION_NAMES = {v: k for k, v in PRECISIONS.items()}
 
 

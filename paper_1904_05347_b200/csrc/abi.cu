@@ -1163,7 +1163,7 @@ int tk_conv2d_plan_info(const tk_conv_shape* shape, const tk_conv_params* params
                                   "winograd for tensor cores");
         {
           const TcConvInfo t = tc_conv_info(g, prec);
-          r.kernel = t.mode;
+          r.kernel = t.narrow ? TK_KERNEL_TC_HALO_NARROW : t.mode;
           r.precision = t.precision;
           r.cta_group = t.cta_group;
           r.tile_m = t.tile_m;

@@ -113,6 +113,24 @@ constexpr int threads_of() {
 // Epilogue group g's named barrier: ptx::epi_sync(g) (ids 1 / 2; gather mode,
 // whose producer groups use 2.., has one epilogue group).
 
+// n / d for 0 <= n < 2^31 by multiply-shift (Granlund-Montgomery with a
+// 33-bit magic split as m + 2^32): l = ceil(log2 d), m = 2^32 (2^l - d) / d
+// + 1, n / d = (umulhi(n, m) + n) >> l.
+struct FDiv {
+  uint32_t m;
+  int l;
+};
+inline FDiv make_fdiv(int d) {
+  if (d < 1) d = 1;
+  int l = 0;
+  while ((1ll << l) < (long long)d) ++l;
+  const unsigned long long m = ((1ull << 32) * ((1ull << l) - (unsigned long long)d)) / (unsigned)d + 1;
+  return FDiv{(uint32_t)m, l};
+}
+__device__ __forceinline__ int fdiv(int n, FDiv f) {
+  return (int)((__umulhi((uint32_t)n, f.m) + (uint32_t)n) >> f.l);
+}
+
 struct TcArgs {
   int M, N, K;
   int BN;                      // UMMA N (columns of the tile)
@@ -189,6 +207,10 @@ struct TcArgs {
   // Timeline probe (TK_TC_TRACE=1, experiments only): per CTA, globaltimer
   // stamps of kTraceEvents milestones.
   unsigned long long* trace;
+  // Multiply-shift divisors of the unit decode (set by run_kernel): a chain
+  // of runtime integer divisions per tile sat on the epilogue's critical
+  // path of one-slab tiles (narrow halo).
+  FDiv fd_per, fd_span, fd_raster, fd_num_m, fd_batch, fd_per_img, fd_tiles_w;
 };
 
 constexpr int kTraceEvents = 21;
@@ -212,22 +234,24 @@ __device__ __forceinline__ Unit decode_tile(const TcArgs& p, int t) {
   Unit u;
   u.slot = -1;
   const int per = p.num_m * p.num_n;
-  int rest = t / per;
+  const int rest = fdiv(t, p.fd_per);
   const int t2 = t - rest * per;
   if (p.raster > 1) {
     const int span = p.raster * p.num_n;
-    const int group = t2 / span;
+    const int group = fdiv(t2, p.fd_span);
     const int first_m = group * p.raster;
     const int gsize = min(p.num_m - first_m, p.raster);
     const int local = t2 - group * span;
-    u.m_blk = first_m + local % gsize;
-    u.n_blk = local / gsize;
+    const int nb = gsize == p.raster ? fdiv(local, p.fd_raster) : local / gsize;
+    u.m_blk = first_m + local - nb * gsize;
+    u.n_blk = nb;
   } else {
-    u.m_blk = t2 % p.num_m;
-    u.n_blk = t2 / p.num_m;
+    const int nb = fdiv(t2, p.fd_num_m);
+    u.m_blk = t2 - nb * p.num_m;
+    u.n_blk = nb;
   }
-  u.z = rest % p.batch;
-  u.sp = rest / p.batch;
+  u.sp = fdiv(rest, p.fd_batch);
+  u.z = rest - u.sp * p.batch;
   u.kb0 = u.sp * p.kb_per;
   u.kb1 = min(p.num_kb, u.kb0 + p.kb_per);
   return u;
@@ -289,11 +313,12 @@ struct PixTile {
 __device__ __forceinline__ PixTile pix_tile(const TcArgs& p, int t) {
   PixTile r;
   const int per_img = p.tiles_w * p.tiles_h;
-  const int ti = t / per_img;
+  const int ti = fdiv(t, p.fd_per_img);
   r.img = ti * (p.imgs > 1 ? p.imgs : 1);
   const int rem = t - ti * per_img;
-  r.oh0 = (rem / p.tiles_w) * p.tileH;
-  r.ow0 = (rem % p.tiles_w) * p.Wb;
+  const int th = fdiv(rem, p.fd_tiles_w);
+  r.oh0 = th * p.tileH;
+  r.ow0 = (rem - th * p.tiles_w) * p.Wb;
   return r;
 }
 
@@ -1668,6 +1693,13 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
                    : 0;
   }
   if (p.tail_q > 1 && (p.splits > 1 || (!plain_like<MODE>() && MODE != kConvPixN))) p.tail_q = 0;
+  p.fd_per = make_fdiv(p.num_m * p.num_n);
+  p.fd_span = make_fdiv(p.raster * p.num_n);
+  p.fd_raster = make_fdiv(p.raster);
+  p.fd_num_m = make_fdiv(p.num_m);
+  p.fd_batch = make_fdiv(p.batch);
+  p.fd_per_img = make_fdiv(p.tiles_w * p.tiles_h);
+  p.fd_tiles_w = make_fdiv(p.tiles_w);
   const long long total = p.tail_q > 1 ? (long long)p.tail_start + (long long)p.tail_kb * p.tail_P
                                        : (long long)p.num_m * p.num_n * p.batch * p.splits;
   const int units = sm_count() / CG;
@@ -3379,6 +3411,7 @@ TcConvInfo tc_conv_info(const ConvGeom& g, int precision) {
             c.narrow_cp ? 1
                         : (halo_resident(g, bn, g.C / ek, (TH + g.R) * 16 * kSlabBytes, num_n) ? 1 : 0);
         if (c.narrow_cp) {
+          r.narrow = true;
           r.box_w = 16 - (g.S - 1) / g.stride;
           r.flat = 0;
         }

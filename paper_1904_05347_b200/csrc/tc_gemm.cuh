@@ -68,6 +68,7 @@ constexpr int kConvPrepare = 1, kConvRun = 2, kConvAll = 3;
 // actually compute in, tile and work split.
 struct TcConvInfo {
   int mode = 0;        // enum tk_tc_mode of the operand path
+  bool narrow = false; // halo over 16-byte padded pixels (TK_KERNEL_TC_HALO_NARROW)
   int precision = 0;   // effective enum tk_precision
   int cta_group = 1, tile_m = 0, tile_n = 0, splits = 1, tail_pieces = 0;
   int imgs = 1, flat = 0, box_w = 0, box_h = 0, halo_resident = 0;

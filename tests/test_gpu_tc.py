@@ -296,7 +296,7 @@ def test_tc_conv_narrow_pixels(tk, oracle, shape, prec, mode):
         pytest.skip("not a narrow-halo layer")
     plan = tk.conv2d_plan_info(s, tk.parse_conv_params("im2col"), options=opts)
     if narrow:
-        assert plan["kernel"] == "tc_halo" and plan["precision"] == prec, plan
+        assert plan["kernel"] == "tc_halo_narrow" and plan["precision"] == prec, plan
     x = oracle.fill_random(int(np.prod(conv.in_shape)), 31).reshape(conv.in_shape)
     f = oracle.fill_random(int(np.prod(conv.filt_shape)), 32).reshape(conv.filt_shape)
     want = oracle.conv2d_naive(conv, x, f)
