@@ -61,7 +61,8 @@ constexpr int kThreads = 192;
 constexpr int kAccCols = 256;  // TMEM: 2 x 256 fp32 columns allocated
 constexpr int kMaxAcc = 8;     // accumulator slots when BN <= 64 (512 / 64)
 constexpr int kMaxStages = 8;
-constexpr int kMaxSplits = 16;  // split-K partials summed by splitk_reduce
+constexpr int kMaxSplits = 16;
+constexpr int kHaloPitch = 16;  // halo modes: virtual pitch of the pixel rows (TMEM lanes)  // split-K partials summed by splitk_reduce
 constexpr int kMaxNarrowMma = 32;  // narrow halo: MMAs per tile (two taps each, 7x7 -> 25)
 
 enum TcMode : int {
@@ -151,7 +152,7 @@ struct TcArgs {
   // TMEM accumulator ring: acc_slots slots of acc_cols columns (512 / slots);
   // more slots for narrow tiles let the MMA run further ahead of the
   // epilogue, decoupling their per-tile handshakes.
-  int acc_slots, acc_cols;
+  int acc_slots, acc_cols, acc_shift;  // acc_slots = 1 << acc_shift
   // conv geometry
   int OH, OW, Kout, Wb, tileH, boxH, tiles_w, tiles_h, pad_t, pad_l, cchunks, S;
   // pixN on small planes: one pixel tile = `imgs` whole images (box
@@ -210,7 +211,7 @@ struct TcArgs {
   // Multiply-shift divisors of the unit decode (set by run_kernel): a chain
   // of runtime integer divisions per tile sat on the epilogue's critical
   // path of one-slab tiles (narrow halo).
-  FDiv fd_per, fd_span, fd_raster, fd_num_m, fd_batch, fd_per_img, fd_tiles_w;
+  FDiv fd_per, fd_span, fd_raster, fd_num_m, fd_num_n, fd_batch, fd_per_img, fd_tiles_w;
 };
 
 constexpr int kTraceEvents = 21;
@@ -451,8 +452,8 @@ __device__ __forceinline__ void tma_store_epilogue_multi(const TcArgs& p, uint32
     const int bs = p.epi_ring;
     for (int j0 = 0; j0 < nchunks; j0 += bs) {
       const int nb = min(bs, nchunks - j0);
-      uint8_t* half = stage + (ring % p.epi_slots) * bs * kRows * kSlabBytes;
-      ++ring;
+      uint8_t* half = stage + ring * bs * kRows * kSlabBytes;
+      if (++ring == p.epi_slots) ring = 0;
       if (issuer) ptx::bulk_wait_read_dyn(p.epi_slots - 1);
       ptx::epi_sync(bar);
       // TKB_TMEM_PAIRS: two TMEM loads in flight per wait.
@@ -745,8 +746,8 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = unit; t < total; t += nunits) {
-        const int n_blk = t % p.num_n;
-        const int m_blk = t / p.num_n;
+        const int m_blk = fdiv(t, p.fd_num_n);
+        const int n_blk = t - m_blk * p.num_n;
         const PixTile pt = pix_tile(p, m_blk);
         for (int ch = 0; ch < p.cchunks; ++ch) {
           ptx::mbar_wait_sleep(&empty[stage], phase ^ 1);
@@ -765,7 +766,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
             // from w2 = ow0, rows oh*s - pad_t + px stepping by s -- each
             // box row one contiguous 256-byte run.
             for (int ph = 0; ph < p.nphase; ++ph) {
-              const int px = ph / p.stride, py = ph - (ph / p.stride) * p.stride;
+              const int px = p.stride == 1 ? 0 : ph >> 1, py = p.stride == 1 ? 0 : ph & 1;
               ptx::tma4<CG>(sa + ph * p.phase_bytes, &map_a, fb, pt.ow0 * p.C, py,
                             (pt.oh0 + rank * p.TH) * p.stride - p.pad_t + px, pt.img);
             }
@@ -826,8 +827,8 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       uint32_t phase = 0;
       int local = 0;
       for (int t = unit; t < total; t += nunits, ++local) {
-        const int acc = local % p.acc_slots;
-        const uint32_t acc_phase = (uint32_t)(local / p.acc_slots) & 1u;
+        const int acc = local & (p.acc_slots - 1);
+        const uint32_t acc_phase = (uint32_t)(local >> p.acc_shift) & 1u;
         ptx::mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * p.acc_cols;
@@ -980,8 +981,8 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         const Unit u = decode_unit(p, t);
         if (u.kb0 >= u.kb1) continue;  // empty tail segment
         const int local = nlocal++;
-        const int acc = local % p.acc_slots;
-        const uint32_t acc_phase = (uint32_t)(local / p.acc_slots) & 1u;
+        const int acc = local & (p.acc_slots - 1);
+        const uint32_t acc_phase = (uint32_t)(local >> p.acc_shift) & 1u;
         ptx::mbar_wait_sleep(&tmem_empty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         if (local == kTraceUnit && lane == 0) trace_mark(p, 10);
@@ -1059,11 +1060,11 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       if (u.kb0 >= u.kb1) continue;  // empty tail segment
       const int local = nlocal++;
       if constexpr (kMulti) {
-        if (eg >= p.epi_groups || (local % p.epi_groups) != eg) continue;
+        if (eg >= p.epi_groups || (local & (p.epi_groups - 1)) != eg) continue;  // 1 or 2 groups
       }
       const int m_blk = u.m_blk, n_blk = u.n_blk, z = u.z;
-      const int acc = local % p.acc_slots;
-      const uint32_t acc_phase = (uint32_t)(local / p.acc_slots) & 1u;
+      const int acc = local & (p.acc_slots - 1);
+      const uint32_t acc_phase = (uint32_t)(local >> p.acc_shift) & 1u;
       ptx::mbar_wait_sleep(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
       if (local == 0 && warp == 2 && lane == 0) trace_mark(p, 4);  // first accumulator ready
@@ -1082,9 +1083,9 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         continue;
       }
       if constexpr (halo_like<MODE>()) {
-        const int hn = t % p.num_n, hm = t / p.num_n;
+        const int hm = fdiv(t, p.fd_num_n), hn = t - hm * p.num_n;
         const PixTile pt = pix_tile(p, hm);
-        const int h = row / p.P, w = row - (row / p.P) * p.P;
+        const int h = row / kHaloPitch, w = row % kHaloPitch;
         const int srow = w < p.TW ? h * p.TW + w : -1;
         if (p.direct_store) {
           // Each thread owns one output pixel (TMEM lane): its BN features
@@ -1679,6 +1680,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     p.acc_slots = p.BN <= 64 ? 8 : (p.BN <= 128 ? 4 : 2);
     if (forced == 2 || forced == 4 || forced == 8) p.acc_slots = std::min(p.acc_slots, forced);
     p.acc_cols = 2 * kAccCols / p.acc_slots;
+    p.acc_shift = p.acc_slots == 8 ? 3 : (p.acc_slots == 4 ? 2 : 1);
   }
   if (p.splits < 1 || (!plain_like<MODE>() && MODE != kConvPixN)) {
     p.splits = 1;
@@ -1697,6 +1699,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   p.fd_span = make_fdiv(p.raster * p.num_n);
   p.fd_raster = make_fdiv(p.raster);
   p.fd_num_m = make_fdiv(p.num_m);
+  p.fd_num_n = make_fdiv(p.num_n);
   p.fd_batch = make_fdiv(p.batch);
   p.fd_per_img = make_fdiv(p.tiles_w * p.tiles_h);
   p.fd_tiles_w = make_fdiv(p.tiles_w);
@@ -3048,7 +3051,7 @@ void launch_narrow_halo(const ConvGeom& g, const ConvPlan& c, const float* in, c
                s, W2, g.pad_l, cp, (__nv_bfloat16*)xin);
   const int cg = 2;
   TcArgs p{};
-  p.P = 16;
+  p.P = kHaloPitch;
   p.TH = kRows / p.P;
   p.TW = p.P - (g.S - 1) / s;
   const int rows = p.TH + (g.R - 1) / s + 1;  // phase-box rows (one spare)
@@ -3252,7 +3255,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   if (use_halo) {
     const int cg = 2;
     TcArgs p{};
-    p.P = 16;
+    p.P = kHaloPitch;
     p.TH = kRows / p.P;
     p.TW = p.P - (g.S - 1);
     p.taps = g.R * g.S;
