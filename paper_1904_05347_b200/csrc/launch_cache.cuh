@@ -25,7 +25,8 @@ enum ScratchSlot : int {
   kScratchPackB = 3,
   kScratchSplitA = 4,  // 3xTF32 operand triples
   kScratchSplitB = 5,
-  kScratchSlots = 6
+  kScratchPart = 6,    // split-K partial outputs of a GEMM
+  kScratchSlots = 7
 };
 // `bytes` of device memory usable in stream order on `st` until the next
 // request of the same (stream, slot).  While `st` is being captured into a

@@ -1128,7 +1128,9 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         continue;
       } else if constexpr (plain_like<MODE>()) {
         const int m = m_blk * BM + rank * kRows + row;
-        float* dz = p.d + (long long)z * p.d_batch;
+        // Split-K partials (non-TMA path: dense column-major output, batch 1)
+        // land at part + sp * part_stride in the output's own layout.
+        float* dz = (p.splits > 1 ? p.part + u.sp * p.part_stride : p.d) + (long long)z * p.d_batch;
         const float* cz = p.read_c ? p.c + (long long)z * p.d_batch : nullptr;
         if (p.store_tma) {
           tma_store_epilogue<CG>(p, taddr, epi_mine, local, warp, lane, row, row, empty_base + 8u * acc,
@@ -1140,6 +1142,17 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           float v[32];
           ptx::tmem_ld32(taddr + col, v);
           const int n0 = n_blk * p.BN + col;
+          if (!p.read_c && p.d_sm == 1 && n0 + 32 <= p.N && col + 32 <= p.BN) {
+            // Column-major C, whole 32-column chunk in range: lanes = 32
+            // consecutive rows, each j one coalesced 128-byte store; no
+            // per-element predicates or 64-bit index math.
+            if (m < p.M) {
+              float* dst = dz + m + (long long)n0 * p.d_sn;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) dst[(long long)j * p.d_sn] = p.alpha * v[j];
+            }
+            continue;
+          }
           if (m < p.M) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -2131,30 +2144,32 @@ __global__ void __launch_bounds__(256) pad_phase_kernel(const float* __restrict_
                                                         int cp, T* __restrict__ dst) {
   ptx::griddep_wait();
   ptx::griddep_launch_dependents();
-  const long long total = (long long)N * H * s * W2;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int w2 = (int)(i % W2);
-    const long long r = i / W2;
-    const int py = (int)(r % s);
-    const long long nh = r / s;  // n * H + h
-    const int col = s * w2 + py - pad_l;
-    float v[8];
-    const bool in = col >= 0 && col < W;
-    const float* px = src + (nh * W + (in ? col : 0)) * C;
+  // One destination row (n, h, column phase py) per block iteration, its W2
+  // 16-byte pixels across the threads (no 64-bit index division per pixel).
+  const int rows = N * H * s;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int py = s == 1 ? 0 : (r & 1);
+    const long long nh = s == 1 ? r : (r >> 1);  // n * H + h
+    for (int w2 = threadIdx.x; w2 < W2; w2 += blockDim.x) {
+      const long long i = (long long)r * W2 + w2;
+      const int col = s * w2 + py - pad_l;
+      float v[8];
+      const bool in = col >= 0 && col < W;
+      const float* px = src + (nh * W + (in ? col : 0)) * C;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = in && c < C && c < cp ? __ldg(px + c) : 0.0f;
-    if constexpr (sizeof(T) == 4) {
-      reinterpret_cast<float4*>(dst)[i] = make_float4(v[0], v[1], v[2], v[3]);
-    } else {
-      uint4 u;
-      __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]), b1 = __floats2bfloat162_rn(v[2], v[3]),
-                     b2 = __floats2bfloat162_rn(v[4], v[5]), b3 = __floats2bfloat162_rn(v[6], v[7]);
-      u.x = *reinterpret_cast<uint32_t*>(&b0);
-      u.y = *reinterpret_cast<uint32_t*>(&b1);
-      u.z = *reinterpret_cast<uint32_t*>(&b2);
-      u.w = *reinterpret_cast<uint32_t*>(&b3);
-      reinterpret_cast<uint4*>(dst)[i] = u;
+      for (int c = 0; c < 8; ++c) v[c] = in && c < C && c < cp ? __ldg(px + c) : 0.0f;
+      if constexpr (sizeof(T) == 4) {
+        reinterpret_cast<float4*>(dst)[i] = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+        uint4 u;
+        __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]), b1 = __floats2bfloat162_rn(v[2], v[3]),
+                       b2 = __floats2bfloat162_rn(v[4], v[5]), b3 = __floats2bfloat162_rn(v[6], v[7]);
+        u.x = *reinterpret_cast<uint32_t*>(&b0);
+        u.y = *reinterpret_cast<uint32_t*>(&b1);
+        u.z = *reinterpret_cast<uint32_t*>(&b2);
+        u.w = *reinterpret_cast<uint32_t*>(&b3);
+        reinterpret_cast<uint4*>(dst)[i] = u;
+      }
     }
   }
 }
@@ -2333,6 +2348,13 @@ BoxShape pick_box(const ConvGeom& g, bool pix_on_n, int cg) {
 
 }  // namespace
 
+namespace {
+double split_cost_us(long long units, int num_kb, long long pairs, int cg, int bn, int s,
+                     size_t out_bytes);
+int choose_splits(long long units, int num_kb, long long pairs, int bm, int bn, size_t out_bytes,
+                  size_t cap);
+}  // namespace
+
 void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
   require_tc(g.precision);
   const bool tf32 = g.precision == TK_PREC_TF32;
@@ -2342,11 +2364,22 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
   int cg = g.M > kRows ? 2 : 1;
   if (tc_knobs().cluster == 1 || tc_knobs().cluster == 2) cg = tc_knobs().cluster;
   int bn = g.tile_n > 0 ? g.tile_n : (g.N >= 256 ? 256 : ((g.N + 15) / 16) * 16);
+  // Split-K (no C read, batch 1, dense output): every split stores its
+  // partial product in the output's own layout, splitk_reduce sums them in
+  // split order (deterministic).
+  const int num_kb_all = (g.K + ek - 1) / ek;
+  const size_t out_bytes = (size_t)g.M * g.N * 4;
+  const bool dense = (g.d_sm == 1 && g.d_sn == g.M) || (g.d_sn == 1 && g.d_sm == g.N);
+  const bool split_ok = !(g.c != nullptr && g.beta != 0.0f) && g.batch == 1 && dense &&
+                        ((long long)g.M * g.N) % 4 == 0 &&
+                        (reinterpret_cast<uintptr_t>(g.d) & 15) == 0;
+  const size_t split_cap = std::max<size_t>(out_bytes * 4, (size_t)64 << 20);
+  int splits = 1;
   if (g.tile_n <= 0 && g.N >= 64) {
     // Library tile for a GEMM too small to fill the SMs with 256 x 256
-    // tiles: the (cluster, N tile) whose modelled time (waves of
-    // max(MMA, operand feed) per slab + the stream-K tail) is least.
-    const int num_kb = (g.K + ek - 1) / ek;
+    // tiles: the (cluster, N tile, K splits) whose modelled time (waves of
+    // max(MMA, operand feed) per slab + the stream-K tail or the split-K
+    // reduction) is least.
     double best = 1e30;
     for (int c : {2, 1}) {
       if (tc_knobs().cluster != 0 && c != tc_knobs().cluster) continue;
@@ -2359,14 +2392,26 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
         // measured winners whenever the SMs fill); a later one must beat
         // the model by 15% (4096^3: the model ties cg1/cg2, hardware
         // prefers the pair, 199 vs 225 us).
-        const double t = plan_tail(tiles, num_kb, c, b).cost_us;
+        double t = plan_tail(tiles, num_kb_all, c, b).cost_us;
+        int sp = 1;
+        if (split_ok) {
+          sp = choose_splits(tiles, num_kb_all, sm_count() / c, kRows * c, b, out_bytes, split_cap);
+          if (sp > 1) t = split_cost_us(tiles, num_kb_all, sm_count() / c, c, b, sp, out_bytes);
+        }
         if (t < best * 0.85) {
           best = t;
           cg = c;
           bn = b;
+          splits = sp;
         }
       }
     }
+  } else if (split_ok) {
+    const int c = cg;
+    const int b = std::min(256, (bn + 16 * c - 1) / (16 * c) * (16 * c));
+    const long long tiles =
+        (long long)((g.M + kRows * c - 1) / (kRows * c)) * ((g.N + b - 1) / b) * g.batch;
+    splits = choose_splits(tiles, num_kb_all, sm_count() / c, kRows * c, b, out_bytes, split_cap);
   }
   if (bn > 256) bn = 256;
   const int step = 16 * cg;
@@ -2390,6 +2435,17 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
   p.alpha = g.alpha;
   p.beta = g.beta;
   p.read_c = g.c != nullptr && g.beta != 0.0f;
+  if (splits > 1) {
+    p.kb_per = (p.num_kb + splits - 1) / splits;
+    splits = (p.num_kb + p.kb_per - 1) / p.kb_per;  // no empty split
+  }
+  p.splits = splits;
+  if (splits <= 1) p.kb_per = p.num_kb;
+  Scratch part_buf(st, kScratchPart, splits > 1 ? (size_t)splits * out_bytes : 0);
+  if (splits > 1) {
+    p.part = part_buf.as<float>();
+    p.part_stride = (long long)g.M * g.N;
+  }
   CUtensorMap ma;
   if (g.a_mn) {
     if (!tf32 || g.batch != 1 || g.M % 32 != 0 || (g.lda * 4) % 16 != 0)
@@ -2410,19 +2466,23 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
   if (g.d_sn == 1 && !p.read_c && (g.d_sm * 4) % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(g.d) & 15) == 0 && (bn % 32 == 0 || p.num_n == 1) &&
       (g.batch == 1 || (g.d_batch * 4) % 16 == 0)) {
-    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)g.batch};
+    // (split-K: the partials, batch coordinate = split)
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)(splits > 1 ? splits : g.batch)};
     cuuint64_t strides[2] = {(cuuint64_t)g.d_sm * 4,
-                             (cuuint64_t)(g.d_batch ? g.d_batch : g.d_sm * g.M) * 4};
+                             (cuuint64_t)(splits > 1 ? p.part_stride
+                                                     : (g.d_batch ? g.d_batch : g.d_sm * g.M)) * 4};
     cuuint32_t box[3] = {32, (cuuint32_t)kRows, 1};
-    md = make_map(g.d, 4, 3, dims, strides, box);
+    md = make_map(splits > 1 ? p.part : g.d, 4, 3, dims, strides, box);
     p.store_tma = 1;
     p.epi_bufs = 2;
   }
-  const TailPlan tp = p.read_c ? TailPlan{}
-                               : plan_tail((long long)p.num_m * p.num_n * p.batch, p.num_kb, cg, bn);
+  const TailPlan tp = (p.read_c || splits > 1)
+                         ? TailPlan{}
+                         : plan_tail((long long)p.num_m * p.num_n * p.batch, p.num_kb, cg, bn);
   Scratch tail_buf(st, kScratchTail, tp.q > 1 ? tp.bytes : 0);
   if (tp.q > 1) apply_tail(p, tp, tail_buf.as<float>());
   dispatch<kPlain>(ma, mb, md, p, cg, tf32, st);
+  if (splits > 1) splitk_reduce(p.part, (long long)g.M * g.N, splits, g.d, st);
 }
 
 void launch_split3_rows(const float* src, long long rows, long long kp, float* dst, int pattern,
@@ -2560,6 +2620,18 @@ struct ConvPlan {
 // units run in waves over the SM pairs, and a split adds the reduction pass
 // (launch + every partial read once and the output written, ~4 TB/s).  The
 // partials must stay under `cap` bytes.
+// Modelled time (us) of `units` tiles split s ways over K: waves of
+// (kb / s slabs + 1 us), plus the ordered reduction pass (launch + every
+// partial read once and the output written at ~4 TB/s).
+double split_cost_us(long long units, int num_kb, long long pairs, int cg, int bn, int s,
+                     size_t out_bytes) {
+  const long long waves = (units * s + pairs - 1) / pairs;
+  const int kb = (num_kb + s - 1) / s;
+  double t = (double)waves * (kb * slab_time_us(cg, bn) + 1.0);
+  if (s > 1) t += 2.0 + (double)(s + 1) * out_bytes / 4.0e6;
+  return t;
+}
+
 int choose_splits(long long units, int num_kb, long long pairs, int bm, int bn,
                   size_t out_bytes, size_t cap) {
   const int forced = tc_knobs().split;
@@ -2570,14 +2642,7 @@ int choose_splits(long long units, int num_kb, long long pairs, int bm, int bn,
     while (sp > 1 && (size_t)sp * out_bytes > cap) --sp;
     return sp;
   }
-  const double slab_us = slab_time_us(bm / kRows, bn);
-  auto cost = [&](int s) {
-    const long long waves = (units * s + pairs - 1) / pairs;
-    const int kb = (num_kb + s - 1) / s;
-    double t = (double)waves * (kb * slab_us + 1.0);
-    if (s > 1) t += 2.0 + (double)(s + 1) * out_bytes / 4.0e6;
-    return t;
-  };
+  auto cost = [&](int s) { return split_cost_us(units, num_kb, pairs, bm / kRows, bn, s, out_bytes); };
   int best = 1;
   // No split leaves the balanced tail (plan_tail) to even out the last wave.
   double best_t = std::min(cost(1), plan_tail(units, num_kb, bm / kRows, bn).cost_us);
@@ -3041,8 +3106,8 @@ void launch_narrow_halo(const ConvGeom& g, const ConvPlan& c, const float* in, c
   }
   if (!run) return;
   const int W2 = narrow_w2(g);
-  const long long pixels = (long long)g.N * g.H * s * W2;
-  const int pblocks = (int)std::min<long long>((pixels + 255) / 256, (long long)sm_count() * 16);
+  if ((long long)g.N * g.H * s > 2147483647ll) fail(TK_ERR_CAPABILITY, "narrow halo: too many rows");
+  const int pblocks = (int)std::min<long long>((long long)g.N * g.H * s, (long long)sm_count() * 32);
   if (c.tf32)
     launch_pdl(pad_phase_kernel<float>, (unsigned)pblocks, 256, st, in, g.N, g.H, g.W, g.C, s, W2,
                g.pad_l, cp, (float*)xin);

@@ -51,6 +51,32 @@ def test_tc_gemm_colmajor(tk, oracle, m, n, k, ta, tb, prec):
 
 
 @pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("split", [0, 2, 3, 5])
+@pytest.mark.parametrize("m,n,k,ta,tb", [(1024, 1024, 1024, 0, 0), (512, 768, 640, 1, 0),
+                                         (256, 128, 2048, 0, 1), (384, 200, 300, 1, 1)])
+def test_tc_gemm_split_k(tk, oracle, m, n, k, ta, tb, split, prec):
+    """C = A B (beta 0) with K split over CTAs (split 0 = the cost model's
+    choice, e.g. SGEMM 1024^3): partial products in the output's layout,
+    summed in split order -- within the TF32/BF16 bar and bitwise repeatable."""
+    import torch
+    a = oracle.fill_random(m * k, 4)
+    b = oracle.fill_random(k * n, 5)
+    want = oracle.gemm_naive(m, n, k, 1.0, 0.0, ta, tb, a, b, np.zeros(m * n, np.float32))
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    shape = tk.GemmShape(m, n, k, 1.0, 0.0, "t" if ta else "n", "t" if tb else "n")
+    opts = tk.exec_options(prec, split=split)
+    outs = []
+    for _ in range(2):
+        out = torch.full((m * n,), float("nan"), device="cuda")
+        tk.gemm_dev(da, db, None, out, shape, options=opts)
+        torch.cuda.synchronize()
+        outs.append(out)
+    err = oracle.max_scaled_error(outs[0].cpu().numpy(), want)
+    assert err <= TOL[prec], err
+    assert torch.equal(outs[0].view(torch.int32), outs[1].view(torch.int32))
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
 @pytest.mark.parametrize("shape", [
     (2, 14, 14, 32, 128), (2, 14, 14, 64, 256), (2, 30, 30, 128, 64), (1, 56, 56, 64, 64), (1, 28, 28, 64, 64), (2, 56, 56, 64, 128), (1, 28, 28, 256, 512),
     (3, 17, 23, 32, 96), (1, 112, 112, 64, 128), (2, 7, 7, 512, 512), (1, 9, 9, 3, 16),
