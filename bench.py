@@ -741,6 +741,35 @@ def main():
             secondary[f"vgg16_{p_}"] = {"value": round(step_flops / (ms * 1e-3) / 1e9, 1),
                                          "unit": "GFLOP/s", "ms_per_step": round(ms, 3),
                                          "bit_exact": p_ == "fp32"}
+        # BF16 with bf16 activations in HBM (tk_exec_options.io = bf16): each
+        # layer reads a bf16 input and writes a bf16 output -- a BF16
+        # network's layer-to-layer format (the producing layer's epilogue
+        # writes what the next one reads), so no fp32 -> bf16 conversion pass
+        # and half the output bytes.  Same layers, filters and per-call
+        # filter pack as vgg16_bf16.
+        io_opts = tk.exec_options("bf16", io="bf16")
+        xb_ = [L["x"].to(torch.bfloat16) for L in layers]
+        yb_ = [torch.empty(tuple(L["y"].shape), device=dev, dtype=torch.bfloat16) for L in layers]
+
+        def stack_io_ms(reps):
+            ts = []
+            for _ in range(reps):
+                flush.zero_()
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                for L, xb, yb in zip(layers, xb_, yb_):
+                    tk.conv2d_dev(xb, L["f"], yb, L["shape"], L["algo"], workspace=None,
+                                  stream=stream, options=io_opts)
+                b_.record(stream)
+                b_.synchronize()
+                ts.append(a_.elapsed_time(b_))
+            return float(np.median(ts))
+        stack_io_ms(1)
+        ms = stack_io_ms(3)
+        secondary["vgg16_bf16_io"] = {"value": round(step_flops / (ms * 1e-3) / 1e9, 1),
+                                      "unit": "GFLOP/s", "ms_per_step": round(ms, 3),
+                                      "activations": "bf16 in / bf16 out (tk_exec_options.io)"}
+        del xb_, yb_
         # BASELINE configs[1] at batch 1: the 13 VGG16 layers on one image
         # (latency-bound: 13 launches of small grids), TF32, as one graph.
         b1 = []
@@ -797,11 +826,16 @@ def main():
             rn.append((shp, x, f, y, ws, mult, shp.flops()))
         rn_flops = sum(fl * m for *_, m, fl in rn)
         im2col = tk.parse_conv_params("im2col")
-        for p_ in ("tf32", "bf16"):
+        for p_ in ("tf32", "bf16", "bf16_io"):
             # One workspace per layer instance (each of a shape's `mult`
             # instances is its own layer with its own prepared filter).
-            inst = [(shp, x, f, y, torch.empty(tk.conv2d_workspace_size(shp, im2col, p_) // 4 + 1,
-                                               device=dev))
+            # bf16_io: BF16 with bf16 activations in HBM (see vgg16_bf16_io).
+            io_ = p_ == "bf16_io"
+            o_ = tk.exec_options("bf16" if io_ else p_, io="bf16" if io_ else "fp32")
+            inst = [(shp, x.to(torch.bfloat16) if io_ else x, f,
+                     torch.empty(tuple(y.shape), device=dev, dtype=torch.bfloat16) if io_ else y,
+                     torch.empty(tk.conv2d_workspace_size(shp, im2col, options=o_) // 4 + 1,
+                                 device=dev))
                     for shp, x, f, y, _, mult, _ in rn for _ in range(mult)]
 
             def rn_pass(s_main, s_side):
@@ -811,13 +845,13 @@ def main():
                 ready = []
                 with torch.cuda.stream(s_side):
                     for shp, x, f, y, ws in inst:
-                        tk.conv2d_prepare_dev(f, shp, im2col, ws, precision=p_, stream=s_side)
+                        tk.conv2d_prepare_dev(f, shp, im2col, ws, options=o_, stream=s_side)
                         ev = torch.cuda.Event()
                         ev.record(s_side)
                         ready.append(ev)
                 for (shp, x, f, y, ws), ev in zip(inst, ready):
                     s_main.wait_event(ev)
-                    tk.conv2d_run_dev(x, f, y, shp, im2col, ws, precision=p_, stream=s_main)
+                    tk.conv2d_run_dev(x, f, y, shp, im2col, ws, options=o_, stream=s_main)
                 s_main.wait_stream(s_side)
             side_rn = torch.cuda.Stream(device=dev)
             rn_pass(stream, side_rn)
@@ -848,6 +882,8 @@ def main():
                                             "unit": "GFLOP/s", "ms_per_step": round(ms, 3),
                                             "step_gflop": round(rn_flops / 1e9, 2),
                                             "batch_per_gpu": N}
+            if io_:
+                secondary[f"resnet50_{p_}"]["activations"] = "bf16 in / bf16 out (tk_exec_options.io)"
             if not args.no_graph and p_ == prec:
                 # Kernel time per distinct layer shape (first instance, its
                 # filter prepared by the pass above), as the VGG layers.
@@ -1040,8 +1076,8 @@ def main():
         # Compact digest LAST in the line (a log tail shows it whole).
         summ = {"vgg16_" + prec + "_gflops": round(value, 1), "e2e_gflops": e2e and e2e["value"],
                 "roofline_frac": roofline["frac"]}
-        for key in ("vgg16_tf32", "vgg16_bf16", "vgg16_3xtf32", "vgg16_fp32", "resnet50_tf32",
-                    "resnet50_bf16", "resnet50_tiled_fp32", "sgemm1024_fp32", "sgemm1024_tf32",
+        for key in ("vgg16_tf32", "vgg16_bf16", "vgg16_bf16_io", "vgg16_3xtf32", "vgg16_fp32",
+                    "resnet50_tf32", "resnet50_bf16", "resnet50_bf16_io", "resnet50_tiled_fp32", "sgemm1024_fp32", "sgemm1024_tf32",
                     "sgemm1024_bf16", "gemm4096_tf32", "gemm4096_bf16", "gemm8192_tf32",
                     "gemm8192_bf16"):
             if key in secondary:

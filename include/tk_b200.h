@@ -118,8 +118,21 @@ typedef struct tk_exec_options {
   int tc_mode;       /* conv operand path: enum tk_tc_mode                  */
   int tc_split;      /* 0 = cost model, 1 = never split K (no split-K, no
                         wave tail), n > 1 = n K-splits where supported     */
-  int reserved[2];
+  int io;            /* TK_IO_* flags: activations kept in HBM as bf16
+                        (BF16 precision, im2col algorithm): the in / out
+                        pointers of the conv calls then address bf16 NHWC
+                        tensors (element counts unchanged)                 */
+  int reserved[1];
 } tk_exec_options;
+
+/* tk_exec_options.io: a BF16 network keeps its activations in bf16 between
+ * layers -- the producing layer's epilogue writes bf16 (TK_IO_OUT_BF16) and
+ * the consuming layer reads it without a conversion pass (TK_IO_IN_BF16). */
+enum tk_io_flags {
+  TK_IO_FP32 = 0,
+  TK_IO_IN_BF16 = 1,
+  TK_IO_OUT_BF16 = 2
+};
 
 /* Tensor-core convolution operand paths (tk_exec_options.tc_mode); a mode
  * (or tc_cluster) the shape cannot use is rejected with TK_ERR_CAPABILITY. */

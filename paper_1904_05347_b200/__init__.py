@@ -107,7 +107,11 @@ class ConvParamsC(C.Structure):
 class ExecOptionsC(C.Structure):
     _fields_ = [("precision", C.c_int), ("tc_tile_n", C.c_int), ("tc_stages", C.c_int),
                 ("tc_cluster", C.c_int), ("tc_mode", C.c_int), ("tc_split", C.c_int),
-                ("reserved", C.c_int * 2)]
+                ("io", C.c_int), ("reserved", C.c_int * 1)]
+
+
+# tk_exec_options.io (tk_io_flags): bf16 activations in HBM
+IO_FLAGS = {"fp32": 0, "in_bf16": 1, "out_bf16": 2, "bf16": 3}
 
 
 class ConvPlanInfoC(C.Structure):
@@ -428,10 +432,15 @@ TC_MODES = {"auto": 0, "halo": 1, "pixn": 2, "pixm": 3, "gather": 4, "pointwise"
 
 
 def exec_options(precision="fp32", tile_n=0, stages=0, cluster=0, mode="auto",
-                 split=0) -> ExecOptionsC:
+                 split=0, io="fp32") -> ExecOptionsC:
+    """io: "fp32" (the reference's fp32 NHWC in/out), or -- with precision
+    "bf16" and the im2col algorithm -- "in_bf16" / "out_bf16" / "bf16":
+    the input and/or output activations are bf16 tensors in HBM (a BF16
+    network's layer-to-layer format; no conversion pass)."""
     p = PRECISIONS[precision] if isinstance(precision, str) else int(precision)
     m = TC_MODES[mode] if isinstance(mode, str) else int(mode)
-    return ExecOptionsC(p, tile_n, stages, cluster, m, split)
+    f = IO_FLAGS[io] if isinstance(io, str) else int(io)
+    return ExecOptionsC(p, tile_n, stages, cluster, m, split, f)
 
 
 # ---------------------------------------------------------------------------
@@ -469,17 +478,20 @@ def _need_shape(arr, want, what: str) -> None:
                          f"{'x'.join(map(str, want))}")
 
 
-def _need_dev(t, what: str, count: Optional[int] = None, dtype_f32: bool = True) -> None:
-    """Device operand: a contiguous CUDA tensor (float32 unless a workspace)
-    holding exactly `count` elements (at least, for workspaces: count=None)."""
+def _need_dev(t, what: str, count: Optional[int] = None, dtype_f32: bool = True,
+              bf16: bool = False) -> None:
+    """Device operand: a contiguous CUDA tensor (float32 -- bfloat16 for bf16
+    activations -- unless a workspace) holding exactly `count` elements (at
+    least, for workspaces: count=None)."""
     if t is None:
         return
     if not getattr(t, "is_cuda", False):
         raise ContractError(f"{what} must be a CUDA tensor")
     if dtype_f32:
         import torch
-        if t.dtype != torch.float32:
-            raise ContractError(f"{what} must be float32, got {t.dtype}")
+        want = torch.bfloat16 if bf16 else torch.float32
+        if t.dtype != want:
+            raise ContractError(f"{what} must be {str(want).split('.')[-1]}, got {t.dtype}")
     if not t.is_contiguous():
         raise ContractError(f"{what} must be contiguous")
     if count is not None and t.numel() != count:
@@ -595,10 +607,10 @@ def _stream(stream) -> C.c_void_p:
     return C.c_void_p(s.cuda_stream)
 
 
-def _need_conv_dev(shape: ConvShape, inp, filt, out, workspace) -> None:
-    _need_dev(inp, "conv2d: input", int(np.prod(shape.in_shape)))
+def _need_conv_dev(shape: ConvShape, inp, filt, out, workspace, io: int = 0) -> None:
+    _need_dev(inp, "conv2d: input", int(np.prod(shape.in_shape)), bf16=bool(io & 1))
     _need_dev(filt, "conv2d: filter", int(np.prod(shape.filt_shape)))
-    _need_dev(out, "conv2d: output", int(np.prod(shape.out_shape)))
+    _need_dev(out, "conv2d: output", int(np.prod(shape.out_shape)), bf16=bool(io & 2))
     _need_dev(workspace, "conv2d: workspace", None, dtype_f32=False)
 
 
@@ -606,9 +618,9 @@ def conv2d_dev(inp, filt, out, shape: ConvShape, params: ConvAlgoParams, precisi
                workspace=None, stream=None, tile_n=0, options=None) -> None:
     """options: an exec_options(...) record (tensor-core knobs); overrides
     precision / tile_n when given."""
-    _need_conv_dev(shape, inp, filt, out, workspace)
-    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     opts = options if options is not None else exec_options(precision, tile_n)
+    _need_conv_dev(shape, inp, filt, out, workspace, opts.io)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check(lib().tk_conv2d_dev(C.byref(shape.c()), C.byref(params.c()),
                                C.byref(opts), _dptr(inp), _dptr(filt),
                                _dptr(out), _dptr(workspace), ws_bytes, _stream(stream)))
@@ -628,9 +640,9 @@ def conv2d_prepare_dev(filt, shape: ConvShape, params: ConvAlgoParams, workspace
 def conv2d_run_dev(inp, filt, out, shape: ConvShape, params: ConvAlgoParams, workspace,
                    precision="fp32", stream=None, options=None) -> None:
     """Input-side phase of conv2d_dev; ordered after conv2d_prepare_dev."""
-    _need_conv_dev(shape, inp, filt, out, workspace)
-    ws_bytes = workspace.numel() * workspace.element_size()
     opts = options if options is not None else exec_options(precision)
+    _need_conv_dev(shape, inp, filt, out, workspace, opts.io)
+    ws_bytes = workspace.numel() * workspace.element_size()
     _check(lib().tk_conv2d_run_dev(C.byref(shape.c()), C.byref(params.c()),
                                    C.byref(opts), _dptr(inp), _dptr(filt),
                                    _dptr(out), _dptr(workspace), ws_bytes, _stream(stream)))

@@ -232,6 +232,7 @@ struct KnobScope {
       k.cluster = o->tc_cluster;
       k.mode = o->tc_mode;
       k.split = o->tc_split;
+      k.io = o->io;
     }
     tc_knobs() = k;
   }
@@ -550,7 +551,19 @@ void winograd_dev(const ConvGeom& g, int m, int precision, const float* in, cons
   wino_output_transform(w, prod, out, st);
 }
 
+// tk_exec_options.io (bf16 activations in HBM): BF16 tensor-core convs only.
+void check_io(const tk_conv_params* p, int precision) {
+  const int io = tc_knobs().io;
+  if (io == 0) return;
+  if ((io & ~(TK_IO_IN_BF16 | TK_IO_OUT_BF16)) != 0)
+    fail(TK_ERR_CONTRACT, "conv2d: unknown io flags " + std::to_string(io));
+  if (precision != TK_PREC_BF16 || p->algo != 2)
+    fail(TK_ERR_CAPABILITY, "conv2d: bf16 activations (io flags) need BF16 precision and the "
+                            "im2col algorithm");
+}
+
 size_t conv_workspace(const ConvGeom& g, const tk_conv_params* p, int precision) {
+  check_io(p, precision);
   if (p->algo == 3) return wino_sizes(wino_geom(g, (int)p->tile_rows), precision).bytes();
   if (precision != TK_PREC_FP32_EXACT) return tc_conv_workspace(g, precision);
   return 0;
@@ -561,6 +574,7 @@ void conv_dev(const tilekit::ConvShape& s, const tk_conv_params* p, int precisio
               const float* in, const float* filt, float* out, void* ws, cudaStream_t st,
               int phase = kConvAll) {
   const ConvGeom g = conv_geom(s);
+  check_io(p, precision);
   // Exact FP32 paths read the filter directly: nothing to prepare.
   const bool exact_run = (phase & kConvRun) != 0;
   switch (p->algo) {
@@ -645,6 +659,9 @@ int pipeline_chunks(const ConvGeom& g) {
 void conv_host(const tilekit::ConvShape& s, const tk_conv_params* p, int precision,
                const float* in, const float* filt, float* out) {
   const ConvGeom g = conv_geom(s);
+  if (tc_knobs().io != 0)
+    fail(TK_ERR_CAPABILITY, "conv2d: bf16 activations (io flags) apply to the device-buffer calls; "
+                            "the host-buffer calls take the reference's fp32 tensors");
   if (p->algo == 1) check_tiled_params(s, p);
   if (p->algo == 3) check_winograd(s, p);
   HostPipe& hp = host_pipe();
@@ -1139,6 +1156,7 @@ int tk_conv2d_plan_info(const tk_conv_shape* shape, const tk_conv_params* params
     const tilekit::ConvShape s = conv_shape(shape);
     const ConvGeom g = conv_geom(s);
     const int prec = precision_of(opts);
+    check_io(params, prec);
     tk_conv_plan_info r{};
     r.requested_precision = prec;
     r.tuned = apply_tuned_conv(s, params, opts) ? 1 : 0;

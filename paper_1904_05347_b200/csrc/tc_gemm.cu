@@ -149,6 +149,7 @@ struct TcArgs {
   int epi_slots;               // staging slots in the ring (2..8): bulk stores in flight per CTA
   int direct_store;            // epilogue: st.global straight from the TMEM registers (no TMA store)
   int epi_groups;              // epilogue warpgroups in use (1 or 2); staging split between them
+  int out_bf16;                // output written as bf16 (TK_IO_OUT_BF16; kernels with OB = true)
   // TMEM accumulator ring: acc_slots slots of acc_cols columns (512 / slots);
   // more slots for narrow tiles let the MMA run further ahead of the
   // epilogue, decoupling their per-tile handshakes.
@@ -330,14 +331,42 @@ __device__ __forceinline__ PixTile pix_tile(const TcArgs& p, int t) {
 // thread issues the bulk tensor store(s).  Rows/columns outside the output
 // tensor are clipped by the TMA unit.  Two staging buffers alternate, so the
 // store of tile i overlaps the TMEM drain of tile i+1.
-template <int CG>
+// BF16 output: one staging chunk = 64 accumulator columns = one 128-byte
+// bf16 row per pixel, in the fp32 chunk's swizzled layout (TMA box {64, ...}
+// of a bf16 map).  All lanes load (tcgen05.ld is warp-collective).
+__device__ __forceinline__ void stage_chunk_bf16(const TcArgs& p, uint32_t taddr, uint8_t* buf,
+                                                 int srow) {
+  uint32_t r[2][32];
+  ptx::tmem_ld32_async(taddr, r[0]);
+  ptx::tmem_ld32_async(taddr + 32, r[1]);
+  ptx::tmem_wait_ld();
+  if (srow < 0) return;
+  const uint32_t rowp = ptx::smem(buf + srow * kSlabBytes);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = 8 * c + 2 * q;
+      __nv_bfloat162 b = __floats2bfloat162_rn(p.alpha * __uint_as_float(r[e >> 5][e & 31]),
+                                               p.alpha * __uint_as_float(r[(e + 1) >> 5][(e + 1) & 31]));
+      w[q] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(rowp + ((c ^ (srow & 7)) << 4)),
+                 "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                 : "memory");
+  }
+}
+
+template <int CG, bool OB = false>
 __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t taddr, uint8_t* stage,
                                                    int local, uint32_t warp, uint32_t lane, int row,
                                                    int srow,
                                                    uint32_t empty_cluster_addr, uint64_t* empty_local,
                                                    const CUtensorMap* map_d, int c0, int c1, int c2,
                                                    int c3, int rank_dims, int& ring) {
-  const int nchunks = (p.BN + 31) / 32;
+  constexpr int CW = OB ? 64 : 32;  // output columns per staging chunk (one 128-byte row)
+  const int nchunks = (p.BN + CW - 1) / CW;
   const bool issuer = warp == 2 && lane == 0;
   if (p.epi_ring) {
     // Staging in two halves of epi_ring 32-column chunks each (as little as
@@ -352,6 +381,10 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
       ++ring;
       if (issuer) ptx::bulk_wait_read<1>();
       ptx::named_sync(1, 128);
+      if constexpr (OB) {
+        for (int jj = 0; jj < nb; ++jj)
+          stage_chunk_bf16(p, taddr + (j0 + jj) * 64, half + jj * kRows * kSlabBytes, srow);
+      } else
       for (int jj = 0; jj < nb; ++jj) {
         float v[32];
         ptx::tmem_ld32(taddr + (j0 + jj) * 32, v);
@@ -376,8 +409,8 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
         }
         for (int jj = 0; jj < nb; ++jj) {
           const uint8_t* src = half + jj * kRows * kSlabBytes;
-          if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + 32 * (j0 + jj), c1, c2, c3);
-          else ptx::tma_store_3d(map_d, src, c0 + 32 * (j0 + jj), c1, c2);
+          if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + CW * (j0 + jj), c1, c2, c3);
+          else ptx::tma_store_3d(map_d, src, c0 + CW * (j0 + jj), c1, c2);
         }
         ptx::bulk_commit();
       }
@@ -391,6 +424,10 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
     else ptx::bulk_wait_read<0>();
   }
   ptx::named_sync(1, 128);
+  if constexpr (OB) {
+    for (int j = 0; j < nchunks; ++j)
+      stage_chunk_bf16(p, taddr + j * 64, sbuf + j * kRows * kSlabBytes, srow);
+  } else
   for (int j = 0; j < nchunks; ++j) {
     float v[32];
     ptx::tmem_ld32(taddr + j * 32, v);
@@ -418,8 +455,8 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
     if (local == kTraceUnit) trace_mark(p, 20);  // (overrides: after the TMEM release)
     for (int j = 0; j < nchunks; ++j) {
       const uint8_t* src = sbuf + j * kRows * kSlabBytes;
-      if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + 32 * j, c1, c2, c3);
-      else ptx::tma_store_3d(map_d, src, c0 + 32 * j, c1, c2);
+      if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + CW * j, c1, c2, c3);
+      else ptx::tma_store_3d(map_d, src, c0 + CW * j, c1, c2);
     }
     ptx::bulk_commit();
     if (local == 0) trace_mark(p, 9);  // stores issued (first unit)
@@ -431,14 +468,15 @@ __device__ __forceinline__ void tma_store_epilogue(const TcArgs& p, uint32_t tad
 // store, for one of two epilogue groups (own slots, barrier, bulk groups),
 // with epi_slots staging slots and two TMEM loads per wait.  (Kept apart:
 // these run-time generalities measured 10-20% slower on the other modes.)
-template <int CG>
+template <int CG, bool OB = false>
 __device__ __forceinline__ void tma_store_epilogue_multi(const TcArgs& p, uint32_t taddr, uint8_t* stage,
                                                          int local, uint32_t warp, uint32_t lane, int row,
                                                    int srow,
                                                    uint32_t empty_cluster_addr, uint64_t* empty_local,
                                                    const CUtensorMap* map_d, int c0, int c1, int c2,
                                                    int c3, int rank_dims, int& ring, uint32_t bar) {
-  const int nchunks = (p.BN + 31) / 32;
+  constexpr int CW = OB ? 64 : 32;  // output columns per staging chunk (one 128-byte row)
+  const int nchunks = (p.BN + CW - 1) / CW;
   const bool issuer = (warp & 3) == 2 && lane == 0;  // group leader: warp 2 or 6
   if (p.epi_ring) {
     // Staging in two halves of epi_ring 32-column chunks each (as little as
@@ -457,6 +495,10 @@ __device__ __forceinline__ void tma_store_epilogue_multi(const TcArgs& p, uint32
       if (issuer) ptx::bulk_wait_read_dyn(p.epi_slots - 1);
       ptx::epi_sync(bar);
       // TKB_TMEM_PAIRS: two TMEM loads in flight per wait.
+      if constexpr (OB) {
+        for (int jj = 0; jj < nb; ++jj)
+          stage_chunk_bf16(p, taddr + (j0 + jj) * 64, half + jj * kRows * kSlabBytes, srow);
+      } else {
 #if TKB_TMEM_PAIRS
       for (int jj = 0; jj < nb; jj += 2) {
         uint32_t r[2][32];
@@ -495,6 +537,7 @@ __device__ __forceinline__ void tma_store_epilogue_multi(const TcArgs& p, uint32
         }
       }
 #endif
+      }
       const bool last = j0 + nb == nchunks;
       if (last) ptx::tc_fence_before();
       ptx::fence_proxy_async();
@@ -506,8 +549,8 @@ __device__ __forceinline__ void tma_store_epilogue_multi(const TcArgs& p, uint32
         }
         for (int jj = 0; jj < nb; ++jj) {
           const uint8_t* src = half + jj * kRows * kSlabBytes;
-          if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + 32 * (j0 + jj), c1, c2, c3);
-          else ptx::tma_store_3d(map_d, src, c0 + 32 * (j0 + jj), c1, c2);
+          if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + CW * (j0 + jj), c1, c2, c3);
+          else ptx::tma_store_3d(map_d, src, c0 + CW * (j0 + jj), c1, c2);
         }
         ptx::bulk_commit();
       }
@@ -521,6 +564,10 @@ __device__ __forceinline__ void tma_store_epilogue_multi(const TcArgs& p, uint32
     else ptx::bulk_wait_read<0>();
   }
   ptx::epi_sync(bar);
+  if constexpr (OB) {
+    for (int j = 0; j < nchunks; ++j)
+      stage_chunk_bf16(p, taddr + j * 64, sbuf + j * kRows * kSlabBytes, srow);
+  } else
   for (int j = 0; j < nchunks; ++j) {
     float v[32];
     ptx::tmem_ld32(taddr + j * 32, v);
@@ -548,8 +595,8 @@ __device__ __forceinline__ void tma_store_epilogue_multi(const TcArgs& p, uint32
     if (local == kTraceUnit) trace_mark(p, 20);  // (overrides: after the TMEM release)
     for (int j = 0; j < nchunks; ++j) {
       const uint8_t* src = sbuf + j * kRows * kSlabBytes;
-      if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + 32 * j, c1, c2, c3);
-      else ptx::tma_store_3d(map_d, src, c0 + 32 * j, c1, c2);
+      if (rank_dims == 4) ptx::tma_store_4d(map_d, src, c0 + CW * j, c1, c2, c3);
+      else ptx::tma_store_3d(map_d, src, c0 + CW * j, c1, c2);
     }
     ptx::bulk_commit();
     if (local == 0) trace_mark(p, 9);  // stores issued (first unit)
@@ -657,7 +704,7 @@ __device__ __forceinline__ void gather_producer(const TcArgs& p, uint8_t* base, 
   }
 }
 
-template <int MODE, int CG, bool TF32>
+template <int MODE, int CG, bool TF32, bool OB>
 __global__ void __launch_bounds__(threads_of<MODE>(), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
@@ -1113,16 +1160,16 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           continue;
         }
         if constexpr (kMulti)
-          tma_store_epilogue_multi<CG>(p, taddr, epi_mine, local, warp, lane, row, srow,
+          tma_store_epilogue_multi<CG, OB>(p, taddr, epi_mine, local, warp, lane, row, srow,
                                        empty_base + 8u * acc, &tmem_empty[acc], &map_d, hn * p.BN,
                                        pt.ow0, pt.oh0 + rank * p.TH, pt.img, 4, ering, ebar);
         else
-          tma_store_epilogue<CG>(p, taddr, epi_mine, local, warp, lane, row, srow,
+          tma_store_epilogue<CG, OB>(p, taddr, epi_mine, local, warp, lane, row, srow,
                                  empty_base + 8u * acc, &tmem_empty[acc], &map_d, hn * p.BN,
                                  pt.ow0, pt.oh0 + rank * p.TH, pt.img, 4, ering);
         continue;
       } else if constexpr (MODE == kConvGather) {
-        tma_store_epilogue<CG>(p, taddr, epi_mine, local, warp, lane, row, row, empty_base + 8u * acc,
+        tma_store_epilogue<CG, OB>(p, taddr, epi_mine, local, warp, lane, row, row, empty_base + 8u * acc,
                                &tmem_empty[acc], &map_d, n_blk * p.BN, m_blk * BM + rank * kRows,
                                0, 0, 3, ering);
         continue;
@@ -1133,7 +1180,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
         float* dz = (p.splits > 1 ? p.part + u.sp * p.part_stride : p.d) + (long long)z * p.d_batch;
         const float* cz = p.read_c ? p.c + (long long)z * p.d_batch : nullptr;
         if (p.store_tma) {
-          tma_store_epilogue<CG>(p, taddr, epi_mine, local, warp, lane, row, row, empty_base + 8u * acc,
+          tma_store_epilogue<CG, OB>(p, taddr, epi_mine, local, warp, lane, row, row, empty_base + 8u * acc,
                                  &tmem_empty[acc], &map_d, n_blk * p.BN,
                                  m_blk * BM + rank * kRows, u.sp * p.batch + z, 0, 3, ering);
           continue;
@@ -1194,17 +1241,21 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           const bool ok = n < p.BN && oh < p.OH && ow < p.OW && img < p.Nimg;
           const long long pix_off =
               ok ? (((long long)img * p.OH + oh) * p.OW + ow) * p.Kout : -1ll;
-#pragma unroll
           float* dst = p.splits > 1 ? p.part + u.sp * p.part_stride : p.d;
+#pragma unroll
           for (int j = 0; j < 32; ++j) {
             const long long o = __shfl_sync(0xffffffffu, pix_off, j);
-            if (o >= 0 && m_ok) dst[o + m] = v[j];
+            if constexpr (OB) {  // (OB kernels run only without split partials)
+              if (o >= 0 && m_ok) reinterpret_cast<__nv_bfloat16*>(p.d)[o + m] = __float2bfloat16_rn(v[j]);
+            } else {
+              if (o >= 0 && m_ok) dst[o + m] = v[j];
+            }
           }
         }
 
       } else {
         const PixTile pt = pix_tile(p, m_blk);
-        tma_store_epilogue<CG>(p, taddr, epi_mine, local, warp, lane, row, row, empty_base + 8u * acc,
+        tma_store_epilogue<CG, OB>(p, taddr, epi_mine, local, warp, lane, row, row, empty_base + 8u * acc,
                                &tmem_empty[acc], &map_d, n_blk * p.BN, pt.ow0,
                                pt.oh0 + rank * p.boxH, pt.img, 4, ering);
         continue;
@@ -1358,6 +1409,26 @@ CUtensorMap map_rows2d(const void* base, int esize, long long K, long long rows,
   return make_map(base, esize, 2, dims, strides, box);
 }
 
+// Epilogue output maps.  fp32: 32-feature boxes; bf16 activations out
+// (TcArgs::out_bf16): 64-feature boxes -- the same 128-byte staging rows.
+// Rows [pix][K] with the split partials as the third dimension:
+CUtensorMap out_map_rows(const void* base, bool ob, int K, long long pix, int splits) {
+  const int es = ob ? 2 : 4;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)pix, (cuuint64_t)splits};
+  cuuint64_t strides[2] = {(cuuint64_t)K * es, (cuuint64_t)(pix * K * es)};
+  cuuint32_t box[3] = {(cuuint32_t)(ob ? 64 : 32), (cuuint32_t)kRows, 1};
+  return make_map(base, es, 3, dims, strides, box);
+}
+// The NHWC output plane, box {32 | 64 features, bw, bh, 1}:
+CUtensorMap out_map_nhwc(const void* base, bool ob, const ConvGeom& g, int bw, int bh) {
+  const int es = ob ? 2 : 4;
+  cuuint64_t dims[4] = {(cuuint64_t)g.K, (cuuint64_t)g.OW, (cuuint64_t)g.OH, (cuuint64_t)g.N};
+  cuuint64_t strides[3] = {(cuuint64_t)g.K * es, (cuuint64_t)g.OW * g.K * es,
+                           (cuuint64_t)g.OH * g.OW * g.K * es};
+  cuuint32_t box[4] = {(cuuint32_t)(ob ? 64 : 32), (cuuint32_t)bw, (cuuint32_t)bh, 1};
+  return make_map(base, es, 4, dims, strides, box);
+}
+
 // NHWC activations, box {slab channels, Wb, Hb, 1}.
 // With stride s > 1 the box traverses W and H with element stride s: it
 // spans s*wb x s*hb input pixels and lands the wb x hb pixels a stride-s
@@ -1470,7 +1541,7 @@ void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStrea
 // (float4 along the column-major partial).  pixN: row = output feature,
 // column = pixel of the tile's box (features are contiguous in NHWC: float4
 // stores); plain: row = M index, column = N index.
-template <int MODE, int CG>
+template <int MODE, int CG, bool OB>
 __global__ void __launch_bounds__(256) tail_reduce_kernel(TcArgs p) {
   ptx::griddep_wait();
   ptx::griddep_launch_dependents();
@@ -1513,6 +1584,14 @@ __global__ void __launch_bounds__(256) tail_reduce_kernel(TcArgs p) {
       img = pt.img + ii;
     }
     if (oh >= p.OH || ow >= p.OW || img >= p.Nimg) return;
+    if constexpr (OB) {
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.d) +
+                         (((long long)img * p.OH + oh) * p.OW + ow) * p.Kout + m;
+      const float v[4] = {a.x, a.y, a.z, a.w};
+      for (int i = 0; i < 4; ++i)
+        if (m + i < p.Kout) o[i] = __float2bfloat16_rn(v[i]);
+      return;
+    }
     float* o = p.d + (((long long)img * p.OH + oh) * p.OW + ow) * p.Kout + m;
     if (m + 3 < p.Kout && (p.Kout & 3) == 0) {
       *reinterpret_cast<float4*>(o) = a;
@@ -1526,9 +1605,12 @@ __global__ void __launch_bounds__(256) tail_reduce_kernel(TcArgs p) {
     if (n >= p.N) return;
     const float v[4] = {a.x, a.y, a.z, a.w};
     for (int i = 0; i < 4; ++i)
-      if (m + i < p.M)
-        p.d[(long long)u.z * p.d_batch + (long long)(m + i) * p.d_sm + (long long)n * p.d_sn] =
-            p.alpha * v[i];
+      if (m + i < p.M) {
+        const long long off =
+            (long long)u.z * p.d_batch + (long long)(m + i) * p.d_sm + (long long)n * p.d_sn;
+        if constexpr (OB) reinterpret_cast<__nv_bfloat16*>(p.d)[off] = __float2bfloat16_rn(p.alpha * v[i]);
+        else p.d[off] = p.alpha * v[i];
+      }
   }
 }
 
@@ -1610,7 +1692,7 @@ void apply_tail(TcArgs& p, const TailPlan& t, float* buf) {
   p.tail_part = buf;
 }
 
-template <int MODE, int CG, bool TF32>
+template <int MODE, int CG, bool TF32, bool OB = false>
 void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, TcArgs p,
                 int stages_req, cudaStream_t st) {
   const int b_bytes_h = (p.BN / CG) * kSlabBytes;
@@ -1686,7 +1768,11 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   p.stages = stages;
   const size_t smem =
       1024 + (size_t)stages * stage_bytes + fres_bytes + 1024 + epi_bytes + ktab_bytes;
-  auto fn = tc_gemm_kernel<MODE, CG, TF32>;
+  if (OB && !p.store_tma && MODE != kConvPixN)
+    fail(TK_ERR_CAPABILITY, "tc_gemm: bf16 output needs the TMA-store epilogue");
+  if (OB && p.BN % 64 != 0 && MODE != kConvPixN)
+    fail(TK_ERR_CAPABILITY, "tc_gemm: bf16 output needs tiles of 64-feature multiples");
+  auto fn = tc_gemm_kernel<MODE, CG, TF32, OB>;
   func_smem((const void*)fn, smem);
   {
     const int forced = xp.tc_acc;
@@ -1750,7 +1836,7 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     if (p.tail_q > 1) {
       const long long rem = total_tiles_of(p) - p.tail_start;
       const long long blocks = rem * CG * ((p.BN + 7) / 8);
-      launch_pdl(tail_reduce_kernel<MODE, CG>, (unsigned)blocks, 256, st, p);
+      launch_pdl(tail_reduce_kernel<MODE, CG, OB>, (unsigned)blocks, 256, st, p);
     }
   }
   if (trace) {
@@ -1784,6 +1870,14 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
 template <int MODE>
 void dispatch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
               const TcArgs& p, int cg, bool tf32, cudaStream_t st) {
+  if constexpr (MODE != kConvGather) {
+    if (p.out_bf16) {  // bf16 activations out (BF16 operands only)
+      if (tf32) fail(TK_ERR_CAPABILITY, "tc_gemm: bf16 output needs BF16 precision");
+      if (cg == 2) run_kernel<MODE, 2, false, true>(ma, mb, md, p, 0, st);
+      else run_kernel<MODE, 1, false, true>(ma, mb, md, p, 0, st);
+      return;
+    }
+  }
   if (cg == 2) {
     if (tf32) run_kernel<MODE, 2, true>(ma, mb, md, p, 0, st);
     else run_kernel<MODE, 2, false>(ma, mb, md, p, 0, st);
@@ -2138,8 +2232,8 @@ __global__ void __launch_bounds__(256) pack_filter_narrow_kernel(const float* __
 // with xs[n][h][py][w2] = x[n][h][s*w2 + py - pad_l] (zero outside the row,
 // channels past C zero): a stride-s window's column phase is contiguous and
 // the left padding is baked in (tap y reads phase y % s at w2 = ow + y / s).
-template <typename T>
-__global__ void __launch_bounds__(256) pad_phase_kernel(const float* __restrict__ src, int N, int H,
+template <typename T, typename S>
+__global__ void __launch_bounds__(256) pad_phase_kernel(const S* __restrict__ src, int N, int H,
                                                         int W, int C, int s, int W2, int pad_l,
                                                         int cp, T* __restrict__ dst) {
   ptx::griddep_wait();
@@ -2155,9 +2249,12 @@ __global__ void __launch_bounds__(256) pad_phase_kernel(const float* __restrict_
       const int col = s * w2 + py - pad_l;
       float v[8];
       const bool in = col >= 0 && col < W;
-      const float* px = src + (nh * W + (in ? col : 0)) * C;
+      const S* px = src + (nh * W + (in ? col : 0)) * C;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) v[c] = in && c < C && c < cp ? __ldg(px + c) : 0.0f;
+      for (int c = 0; c < 8; ++c) {
+        if constexpr (sizeof(S) == 4) v[c] = in && c < C && c < cp ? __ldg(px + c) : 0.0f;
+        else v[c] = in && c < C && c < cp ? __bfloat162float(px[c]) : 0.0f;
+      }
       if constexpr (sizeof(T) == 4) {
         reinterpret_cast<float4*>(dst)[i] = make_float4(v[0], v[1], v[2], v[3]);
       } else {
@@ -2198,9 +2295,10 @@ void to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st)
 
 // out[i] = sum_s part[s*stride + i] in split order (deterministic), 4
 // elements per thread (n % 4 == 0, 16-byte aligned rows).
+template <bool OB>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __restrict__ part,
                                                             long long stride4, int splits,
-                                                            float4* __restrict__ out, long long n4) {
+                                                            void* __restrict__ out, long long n4) {
   ptx::griddep_wait();
   ptx::griddep_launch_dependents();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
@@ -2219,58 +2317,80 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float4* __rest
         a.w += v[s].w;
       }
     }
-    out[i] = a;
+    if constexpr (OB) {  // bf16 activations out
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+      uint2 u;
+      u.x = *reinterpret_cast<const uint32_t*>(&lo);
+      u.y = *reinterpret_cast<const uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(out)[i] = u;
+    } else {
+      reinterpret_cast<float4*>(out)[i] = a;
+    }
   }
 }
 
-void splitk_reduce(const float* part, long long n, int splits, float* out, cudaStream_t st) {
+void splitk_reduce(const float* part, long long n, int splits, void* out, cudaStream_t st,
+                   bool out_bf16 = false) {
   if (splits < 1 || splits > kMaxSplits)
     fail(TK_ERR_CAPABILITY, "split-K: " + std::to_string(splits) + " splits (at most " +
                                 std::to_string(kMaxSplits) + ")");
   const long long n4 = n / 4;
   const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)sm_count() * 8);
-  launch_pdl(splitk_reduce_kernel, (unsigned)blocks, 256, st, reinterpret_cast<const float4*>(part),
-             n4, splits, reinterpret_cast<float4*>(out), n4);
+  if (out_bf16)
+    launch_pdl(splitk_reduce_kernel<true>, (unsigned)blocks, 256, st,
+               reinterpret_cast<const float4*>(part), n4, splits, out, n4);
+  else
+    launch_pdl(splitk_reduce_kernel<false>, (unsigned)blocks, 256, st,
+               reinterpret_cast<const float4*>(part), n4, splits, out, n4);
 }
 
 // Pointwise (1x1) conv operand: the input pixels the strided window visits,
 // compacted to [N*OH*OW][C] and converted to T (fp32 copy or bf16), 4
 // channels per thread.  Stride 1 + bf16 is a plain conversion.
-template <typename T>
-__global__ void __launch_bounds__(256) pointwise_gather_kernel(const float* __restrict__ in,
-                                                               ConvGeom g, T* __restrict__ out,
-                                                               long long n4) {
+template <typename T, typename S>
+__global__ void __launch_bounds__(256) pointwise_gather_kernel(const S* __restrict__ in, ConvGeom g,
+                                                               FDiv fd_c4, T* __restrict__ out) {
+  // One output row (n, oh) per block iteration, its OW x C/4 chunks across
+  // the threads (one division per row, multiply-shift per chunk).
+  ptx::griddep_wait();
+  ptx::griddep_launch_dependents();
   const int c4 = g.C / 4;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long pix = i / c4;
-    const int c = (int)(i - pix * c4) * 4;
-    const int ow = (int)(pix % g.OW);
-    const long long t = pix / g.OW;
-    const int oh = (int)(t % g.OH);
-    const int n = (int)(t / g.OH);
-    const float4 v = __ldg(reinterpret_cast<const float4*>(
-        in + (((long long)n * g.H + (long long)oh * g.stride) * g.W + (long long)ow * g.stride) * g.C +
-        c));
-    if constexpr (sizeof(T) == 4) {
-      reinterpret_cast<float4*>(out)[i] = v;
-    } else {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-      uint2 u;
-      u.x = *reinterpret_cast<uint32_t*>(&lo);
-      u.y = *reinterpret_cast<uint32_t*>(&hi);
-      reinterpret_cast<uint2*>(out)[i] = u;
+  const int per_row = g.OW * c4;
+  const int rows = g.N * g.OH;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int n = r / g.OH, oh = r - n * g.OH;
+    const S* src = in + ((long long)n * g.H + (long long)oh * g.stride) * g.W * g.C;
+    for (int i = threadIdx.x; i < per_row; i += blockDim.x) {
+      const int ow = fdiv(i, fd_c4), c = (i - ow * c4) * 4;
+      const long long o = (long long)r * per_row + i;
+      const S* sp = src + (long long)ow * g.stride * g.C + c;
+      if constexpr (sizeof(S) == 2) {  // bf16 activations in: a strided copy
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(sp));
+        reinterpret_cast<uint2*>(out)[o] = u;
+      } else {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(sp));
+        if constexpr (sizeof(T) == 4) {
+          reinterpret_cast<float4*>(out)[o] = v;
+        } else {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+          uint2 u;
+          u.x = *reinterpret_cast<uint32_t*>(&lo);
+          u.y = *reinterpret_cast<uint32_t*>(&hi);
+          reinterpret_cast<uint2*>(out)[o] = u;
+        }
+      }
     }
   }
 }
 
-template <typename T>
-void pointwise_gather(const float* in, const ConvGeom& g, T* out, cudaStream_t st) {
-  const long long n4 = (long long)g.N * g.OH * g.OW * (g.C / 4);
-  const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)sm_count() * 16);
-  pointwise_gather_kernel<T><<<blocks, 256, 0, st>>>(in, g, out, n4);
-  note_launch();
-  TKB_CUDA(cudaGetLastError());
+template <typename T, typename S = float>
+void pointwise_gather(const S* in, const ConvGeom& g, T* out, cudaStream_t st) {
+  static_assert(sizeof(S) == 4 || sizeof(T) == 2, "bf16 input compacts to bf16");
+  const long long rows = (long long)g.N * g.OH;
+  if (rows > 2147483647ll || (long long)g.OW * (g.C / 4) > 2147483647ll)
+    fail(TK_ERR_CAPABILITY, "pointwise gather: plane too large");
+  const int blocks = (int)std::min<long long>(rows, (long long)sm_count() * 16);
+  launch_pdl(pointwise_gather_kernel<T, S>, (unsigned)blocks, 256, st, in, g, make_fdiv(g.C / 4), out);
 }
 
 // Row-major patch matrix [pixel][kp] (K-major, zero padded to kp): one
@@ -2615,6 +2735,11 @@ struct ConvPlan {
   int narrow_cp = 0;  // narrow halo (16-byte pixels): channels after padding (4 / 8)
 };
 
+// bf16 activations in HBM (tk_exec_options.io, BF16 convs): the input needs
+// no conversion pass / the epilogue writes bf16.
+inline bool io_in_bf16() { return (tc_knobs().io & TK_IO_IN_BF16) != 0; }
+inline bool io_out_bf16() { return (tc_knobs().io & TK_IO_OUT_BF16) != 0; }
+
 // Split-K count from a small cost model (times in us, B200 at ~1.9 GHz):
 // a unit of kb slabs costs kb * max(MMA, operand-feed) + 1 (fill + epilogue),
 // units run in waves over the SM pairs, and a split adds the reduction pass
@@ -2751,7 +2876,7 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
     c.tf32 = tf32;
     c.kp = K;
     c.filt_bytes = align256((size_t)g.K * K * esize);
-    c.in_bytes = tf32 ? 0 : align256((size_t)g.N * g.H * g.W * g.C * 2);
+    c.in_bytes = (tf32 || io_in_bf16()) ? 0 : align256((size_t)g.N * g.H * g.W * g.C * 2);
     size_pixels_gemm(c);
     return c;
   }
@@ -2760,7 +2885,7 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
     c.tf32 = tf32;
     c.kp = (g.C + ek - 1) / ek * ek;
     c.filt_bytes = align256((size_t)g.K * c.kp * esize);
-    c.in_bytes = (g.stride != 1 || !tf32) ? align256((size_t)pix * g.C * esize) : 0;
+    c.in_bytes = (g.stride != 1 || (!tf32 && !io_in_bf16())) ? align256((size_t)pix * g.C * esize) : 0;
     size_pixels_gemm(c);
     return c;
   }
@@ -2769,7 +2894,7 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
     c.tf32 = tf32;
     c.kp = K;
     c.filt_bytes = align256((size_t)g.K * K * esize);
-    c.in_bytes = tf32 ? 0 : align256((size_t)g.N * g.H * g.W * g.C * 2);
+    c.in_bytes = (tf32 || io_in_bf16()) ? 0 : align256((size_t)g.N * g.H * g.W * g.C * 2);
     // Halo mode: small-feature stride-1 layers whose tap re-reads of the
     // input would otherwise dominate the L2->SM traffic.
     const bool halo_ok = g.stride == 1 && g.R * g.S <= 9 && g.S <= 3 && g.K % 32 == 0 &&
@@ -2941,11 +3066,15 @@ void launch_pointwise(const ConvGeom& g, const ConvPlan& c, const float* in, con
   const void* a = in;
   if (c.in_bytes) {
     if (c.tf32) pointwise_gather<float>(in, g, (float*)cursor, st);
+    else if (io_in_bf16())
+      pointwise_gather<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(in), g,
+                                      (__nv_bfloat16*)cursor, st);
     else pointwise_gather<__nv_bfloat16>(in, g, (__nv_bfloat16*)cursor, st);
     a = cursor;
     cursor += c.in_bytes;
   }
   float* dst = c.splits > 1 ? part : out;
+  const bool ob = io_out_bf16() && c.splits == 1;  // (split partials stay fp32)
   if (pix > 2147483647ll) fail(TK_ERR_CAPABILITY, "tc_conv: too many output pixels");
   TcArgs p{};
   p.M = (int)pix;
@@ -2968,14 +3097,12 @@ void launch_pointwise(const ConvGeom& g, const ConvPlan& c, const float* in, con
   apply_tail(p, c.tail, reinterpret_cast<float*>(reinterpret_cast<char*>(part) + c.part_bytes));
   const CUtensorMap ma = map_rows(a, esize, g.C, pix, 1, 0, kRows);
   const CUtensorMap mb = map_rows(ft, esize, c.kp, g.K, 1, 0, c.bn / c.cg);
-  cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)pix, (cuuint64_t)c.splits};
-  cuuint64_t strides[2] = {(cuuint64_t)g.K * 4, (cuuint64_t)(pix * g.K * 4)};
-  cuuint32_t box[3] = {32, (cuuint32_t)kRows, 1};
-  const CUtensorMap md = make_map(dst, 4, 3, dims, strides, box);
+  const CUtensorMap md = out_map_rows(dst, ob, g.K, pix, c.splits);
+  p.out_bf16 = ob;
   p.store_tma = 1;
   p.epi_bufs = 2;
   dispatch<kPlain>(ma, mb, md, p, c.cg, c.tf32, st);
-  if (c.splits > 1) splitk_reduce(part, pix * g.K, c.splits, out, st);
+  if (c.splits > 1) splitk_reduce(part, pix * g.K, c.splits, out, st, io_out_bf16());
 }
 
 }  // namespace
@@ -3001,11 +3128,12 @@ void launch_im2col_conv(const ConvGeom& g, const ConvPlan& c, const float* in, c
   if (!run) return;
   const long long pix = (long long)g.N * g.OH * g.OW;
   const void* a = in;
-  if (!c.tf32) {
+  if (!c.tf32 && !io_in_bf16()) {
     to_bf16(in, (__nv_bfloat16*)cursor, (long long)g.N * g.H * g.W * g.C, st);
     a = cursor;
   }
   float* dst = c.splits > 1 ? part : out;
+  const bool ob = io_out_bf16() && c.splits == 1;  // (split partials stay fp32)
   if (pix > 2147483647ll) fail(TK_ERR_CAPABILITY, "tc_conv: too many output pixels");
   TcArgs p{};
   p.M = (int)pix;
@@ -3036,14 +3164,12 @@ void launch_im2col_conv(const ConvGeom& g, const ConvPlan& c, const float* in, c
   apply_tail(p, c.tail, reinterpret_cast<float*>(reinterpret_cast<char*>(part) + c.part_bytes));
   const CUtensorMap ma = map_nhwc_im2col(a, esize, g, kRows);
   const CUtensorMap mb = map_rows2d(ft, esize, c.kp, g.K, c.bn / c.cg);
-  cuuint64_t dims[3] = {(cuuint64_t)g.K, (cuuint64_t)pix, (cuuint64_t)c.splits};
-  cuuint64_t strides[2] = {(cuuint64_t)g.K * 4, (cuuint64_t)(pix * g.K * 4)};
-  cuuint32_t box[3] = {32, (cuuint32_t)kRows, 1};
-  const CUtensorMap md = make_map(dst, 4, 3, dims, strides, box);
+  const CUtensorMap md = out_map_rows(dst, ob, g.K, pix, c.splits);
+  p.out_bf16 = ob;
   p.store_tma = 1;
   p.epi_bufs = 2;
   dispatch<kConvIm2col>(ma, mb, md, p, c.cg, c.tf32, st);
-  if (c.splits > 1) splitk_reduce(part, pix * g.K, c.splits, out, st);
+  if (c.splits > 1) splitk_reduce(part, pix * g.K, c.splits, out, st, io_out_bf16());
 }
 
 ConvGeom tripled(const ConvGeom& g) {
@@ -3109,11 +3235,15 @@ void launch_narrow_halo(const ConvGeom& g, const ConvPlan& c, const float* in, c
   if ((long long)g.N * g.H * s > 2147483647ll) fail(TK_ERR_CAPABILITY, "narrow halo: too many rows");
   const int pblocks = (int)std::min<long long>((long long)g.N * g.H * s, (long long)sm_count() * 32);
   if (c.tf32)
-    launch_pdl(pad_phase_kernel<float>, (unsigned)pblocks, 256, st, in, g.N, g.H, g.W, g.C, s, W2,
-               g.pad_l, cp, (float*)xin);
+    launch_pdl(pad_phase_kernel<float, float>, (unsigned)pblocks, 256, st, in, g.N, g.H, g.W, g.C,
+               s, W2, g.pad_l, cp, (float*)xin);
+  else if (io_in_bf16())
+    launch_pdl(pad_phase_kernel<__nv_bfloat16, __nv_bfloat16>, (unsigned)pblocks, 256, st,
+               reinterpret_cast<const __nv_bfloat16*>(in), g.N, g.H, g.W, g.C, s, W2, g.pad_l, cp,
+               (__nv_bfloat16*)xin);
   else
-    launch_pdl(pad_phase_kernel<__nv_bfloat16>, (unsigned)pblocks, 256, st, in, g.N, g.H, g.W, g.C,
-               s, W2, g.pad_l, cp, (__nv_bfloat16*)xin);
+    launch_pdl(pad_phase_kernel<__nv_bfloat16, float>, (unsigned)pblocks, 256, st, in, g.N, g.H,
+               g.W, g.C, s, W2, g.pad_l, cp, (__nv_bfloat16*)xin);
   const int cg = 2;
   TcArgs p{};
   p.P = kHaloPitch;
@@ -3167,14 +3297,11 @@ void launch_narrow_halo(const ConvGeom& g, const ConvPlan& c, const float* in, c
                   CU_TENSOR_MAP_SWIZZLE_NONE);
   }
   const CUtensorMap mb = map_rows2d(ft, esize, c.kp, g.K, p.BN / cg);
-  cuuint64_t dims[4] = {(cuuint64_t)g.K, (cuuint64_t)g.OW, (cuuint64_t)g.OH, (cuuint64_t)g.N};
-  cuuint64_t strides[3] = {(cuuint64_t)g.K * 4, (cuuint64_t)g.OW * g.K * 4,
-                           (cuuint64_t)g.OH * g.OW * g.K * 4};
-  cuuint32_t box[4] = {32, (cuuint32_t)p.TW, (cuuint32_t)p.TH, 1};
-  const CUtensorMap md = make_map(out, 4, 4, dims, strides, box);
+  p.out_bf16 = io_out_bf16();
+  const CUtensorMap md = out_map_nhwc(out, p.out_bf16, g, p.TW, p.TH);
   p.store_tma = 1;
   p.epi_bufs = 1;
-  p.direct_store = experiments().direct_store;
+  p.direct_store = p.out_bf16 ? 0 : experiments().direct_store;
   {
     const int b_bytes_h = (p.BN / cg) * kSlabBytes;
     const int fres = p.taps * b_bytes_h;
@@ -3247,6 +3374,9 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
   }
 
   if (plan.kind == kGatherPlan) {
+    if (tc_knobs().io != 0)
+      fail(TK_ERR_CAPABILITY, "tc_conv: bf16 activations need a BF16 operand path (the gather "
+                              "producers read fp32)");
     // Gather mode: the pixel operand is built in shared memory by producer
     // warps (any channel count / stride), the filter streams by TMA, the
     // output leaves through a TMA store.  fp32 operands, kind::tf32.
@@ -3309,9 +3439,9 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     cursor += align256((size_t)g.K * kp * 2);
     if (prep) pack_filter<__nv_bfloat16>(filt, (int)K, g.K, (int)kp, ft, false, st);
     __nv_bfloat16* xb = reinterpret_cast<__nv_bfloat16*>(cursor);
-    if (run) to_bf16(in, xb, (long long)g.N * g.H * g.W * g.C, st);
+    if (run && !io_in_bf16()) to_bf16(in, xb, (long long)g.N * g.H * g.W * g.C, st);
     fa = ft;
-    xin = xb;
+    if (!io_in_bf16()) xin = xb;
   }
 
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + plan.filt_bytes + plan.in_bytes);
@@ -3353,11 +3483,8 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     p.S = g.S;
     const CUtensorMap ma = map_nhwc(xin, esize, g, p.P, p.TH + g.R);
     const CUtensorMap mb = map_rows2d(fa, esize, kp, g.K, p.BN / cg);
-    cuuint64_t dims[4] = {(cuuint64_t)g.K, (cuuint64_t)g.OW, (cuuint64_t)g.OH, (cuuint64_t)g.N};
-    cuuint64_t strides[3] = {(cuuint64_t)g.K * 4, (cuuint64_t)g.OW * g.K * 4,
-                             (cuuint64_t)g.OH * g.OW * g.K * 4};
-    cuuint32_t box[4] = {32, (cuuint32_t)p.TW, (cuuint32_t)p.TH, 1};
-    const CUtensorMap md = make_map(out, 4, 4, dims, strides, box);
+    p.out_bf16 = io_out_bf16();
+    const CUtensorMap md = out_map_nhwc(out, p.out_bf16, g, p.TW, p.TH);
     p.store_tma = 1;
     p.epi_bufs = 1;
     p.resident = halo_resident(g, p.BN, p.cchunks, p.halo_bytes, p.num_n) ? 1 : 0;
@@ -3410,8 +3537,9 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     const CUtensorMap mb =
         plan.imgs > 1 ? map_nhwc(xin, esize, g, bx.wb, bx.tileH, g.stride, plan.imgs / cg)
                       : map_nhwc(xin, esize, g, bx.wb, bx.boxH, g.stride);
+    p.out_bf16 = io_out_bf16() && p.splits == 1;  // (split partials stay fp32)
     dispatch<kConvPixN>(ma, mb, ma, p, cg, tf32, st);
-    if (p.splits > 1) splitk_reduce(part, p.part_stride, p.splits, out, st);
+    if (p.splits > 1) splitk_reduce(part, p.part_stride, p.splits, out, st, io_out_bf16());
   } else {
     p.BN = (g.K + 16 * cg - 1) / (16 * cg) * (16 * cg);
     p.M = kRows * cg * pix_tiles;
@@ -3421,11 +3549,8 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     const CUtensorMap ma = map_nhwc(xin, esize, g, bx.wb, bx.boxH, g.stride);
     const CUtensorMap mb = map_rows2d(fa, esize, kp, g.K, p.BN / cg);
     if (g.K % 4 != 0) fail(TK_ERR_CAPABILITY, "tc_conv: output features must be a multiple of 4");
-    cuuint64_t dims[4] = {(cuuint64_t)g.K, (cuuint64_t)g.OW, (cuuint64_t)g.OH, (cuuint64_t)g.N};
-    cuuint64_t strides[3] = {(cuuint64_t)g.K * 4, (cuuint64_t)g.OW * g.K * 4,
-                             (cuuint64_t)g.OH * g.OW * g.K * 4};
-    cuuint32_t box[4] = {32, (cuuint32_t)bx.wb, (cuuint32_t)bx.boxH, 1};
-    const CUtensorMap md = make_map(out, 4, 4, dims, strides, box);
+    p.out_bf16 = io_out_bf16();
+    const CUtensorMap md = out_map_nhwc(out, p.out_bf16, g, bx.wb, bx.boxH);
     p.store_tma = 1;
     p.epi_bufs = 2;
     dispatch<kConvPixM>(ma, mb, md, p, cg, tf32, st);

@@ -47,6 +47,7 @@ void launch_split3_rows(const float* src, long long rows, long long kp, float* d
 // calling thread; zero = automatic.
 struct TcKnobs {
   int stages = 0, cluster = 0, mode = 0, split = 0;
+  int io = 0;  // TK_IO_* (bf16 activations in HBM; BF16 tensor-core convs only)
 };
 TcKnobs& tc_knobs();
 

@@ -156,3 +156,76 @@ def test_plan_reports_effective_precision(tk, idx):  # host-only: runs on CPU to
         assert plan["precision"] == "tf32"
     else:
         assert plan["precision"] == "bf16"
+
+
+# bf16 activations in HBM (tk_exec_options.io): the layer reads a bf16 input
+# and/or writes a bf16 output -- a BF16 network's layer-to-layer format, no
+# conversion pass.  Checked against the oracle on the bf16-rounded input;
+# the bar is the BF16 one plus the output's own rounding (2^-9 of |y|).
+TOL_BF16_IO = 5e-3 + 2.0 ** -9
+_want_b = {}
+
+
+def _oracle_bf16_in(oracle, idx, img, xb):
+    key = (idx, img)
+    if key not in _want_b:
+        name, r, s, h, c, k = LAYERS[idx]
+        conv = oracle.Conv(1, h, h, c, k, r, r, s, True)
+        _, f = _host_inputs(None, idx)
+        xi = xb[img:img + 1].float().cpu().numpy()
+        _want_b[key] = oracle.conv2d_naive(conv, xi, f)
+    return _want_b[key]
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("io", ["bf16", "in_bf16", "out_bf16"])
+@pytest.mark.parametrize("idx", range(len(LAYERS)), ids=[lay[0] for lay in LAYERS])
+def test_bench_layer_bf16_activations(tk, oracle, idx, io):
+    import torch
+    name, r, s, h, c, k = LAYERS[idx]
+    if io != "bf16" and idx % 3:
+        pytest.skip("mixed in/out formats on every third layer")
+    shape = tk.ConvShape(N, h, h, c, k, r, r, s, True)
+    algo = tk.parse_conv_params("im2col")
+    opts = tk.exec_options("bf16", io=io)
+    x, f = _device_inputs(idx)
+    xb = x.to(torch.bfloat16)
+    xin = xb if io in ("bf16", "in_bf16") else xb.float()  # same values either way
+    ws = torch.empty(max(tk.conv2d_workspace_size(shape, algo, options=opts), 4) // 4 + 1,
+                     device="cuda")
+    ydt = torch.bfloat16 if io in ("bf16", "out_bf16") else torch.float32
+    y = torch.full(shape.out_shape, float("nan"), device="cuda", dtype=ydt)
+    tk.conv2d_prepare_dev(f, shape, algo, ws, options=opts)
+    tk.conv2d_run_dev(xin, f, y, shape, algo, ws, options=opts)
+    torch.cuda.synchronize()
+    assert not bool(torch.isnan(y.float()).any()), (name, io)
+    for img in IMAGES:
+        want = _oracle_bf16_in(oracle, idx, img, xb)
+        got = y[img:img + 1].float().cpu().numpy()
+        err = oracle.max_scaled_error(got, want)
+        assert err <= TOL_BF16_IO, (name, io, img, err)
+    # the fp32-activation BF16 run on the same (bf16-exact) values agrees to
+    # the output rounding
+    if io == "bf16":
+        y32 = torch.empty(shape.out_shape, device="cuda")
+        tk.conv2d_dev(xb.float(), f, y32, shape, algo, options=tk.exec_options("bf16"))
+        torch.cuda.synchronize()
+        d = (y.float() - y32).abs().max().item() / y32.abs().max().item()
+        assert d <= 2.0 ** -8, (name, d)
+
+
+def test_bf16_activations_need_bf16_im2col(tk):  # host-only checks: CPU too
+    """The io flags are a BF16 tensor-core feature of the device-buffer
+    calls: TF32 / FP32 / Winograd requests with them are rejected
+    (CapabilityError) before anything runs."""
+    shape = tk.ConvShape(1, 8, 8, 64, 64, 3, 3, 1, True)
+    for prec, algo in (("tf32", "im2col"), ("fp32", "im2col"), ("bf16", "winograd_t2x2")):
+        with pytest.raises(tk.CapabilityError):
+            tk.conv2d_workspace_size(shape, tk.parse_conv_params(algo),
+                                     options=tk.exec_options(prec, io="bf16"))
+    im = tk.parse_conv_params("im2col")
+    assert tk.conv2d_workspace_size(shape, im, options=tk.exec_options("bf16", io="bf16")) > 0
+    # no conversion copy of the input in the workspace when it arrives in bf16
+    assert tk.conv2d_workspace_size(shape, im, options=tk.exec_options("bf16", io="in_bf16")) < \
+        tk.conv2d_workspace_size(shape, im, options=tk.exec_options("bf16"))
