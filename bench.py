@@ -1018,12 +1018,15 @@ def main():
                     tk.gemm_dev(gb, ga, None, gc, gshape, cfg, precision=p_, stream=cap)
             gg.replay()
             torch.cuda.synchronize()
-            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a_.record(stream)
-            gg.replay()
-            b_.record(stream)
-            b_.synchronize()
-            dms = a_.elapsed_time(b_) / 20
+            reps_ = []
+            for _ in range(5):  # median of 5 replays (a single one swings with the clock)
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                gg.replay()
+                b_.record(stream)
+                b_.synchronize()
+                reps_.append(a_.elapsed_time(b_) / 20)
+            dms = float(np.median(reps_))
             del gg
             pk = {"fp32": 148 * 128 * 1.965e9 / 1e12, "tf32": peaks["bf16_tflops"] / 2.0,
                   "bf16": peaks["bf16_tflops"]}[p_]
@@ -1032,7 +1035,7 @@ def main():
                 "ms": round(dms, 4), "frac_of_peak": round(2 * n ** 3 / (dms * 1e-3) / 1e12 / pk, 4),
                 "api_ms": round(ms, 4),
                 "api_gflops": round(2 * n ** 3 / (ms * 1e-3) / 1e9, 1),
-                "note": "value/ms: device time (graph of 20 calls); api_*: one tk_gemm_dev call "
+                "note": "value/ms: device time (graph of 20 calls, median of 5 replays); api_*: one tk_gemm_dev call "
                         "between events (host work included); L2-resident operands (12.6 MB); "
                         "fp32 peak = FMUL+FADD issue cap 37.2 TF/s"}
 

@@ -43,6 +43,8 @@ struct ExecOptions {
   int tc_cluster = 0;  // 1 = one SM, 2 = CTA pair, 0 = auto
   TcMode tc_mode = TcMode::Auto;
   int tc_split = 0;    // 0 = cost model, 1 = never split K, n > 1 = n splits
+  int io = TK_IO_FP32; // TK_IO_IN_BF16 | TK_IO_OUT_BF16: bf16 activations in HBM
+                       // (BF16 im2col convs on device buffers; see tk_b200.h)
 
   tk_exec_options c() const {
     tk_exec_options o{};
@@ -52,6 +54,7 @@ struct ExecOptions {
     o.tc_cluster = tc_cluster;
     o.tc_mode = static_cast<int>(tc_mode);
     o.tc_split = tc_split;
+    o.io = io;
     return o;
   }
 

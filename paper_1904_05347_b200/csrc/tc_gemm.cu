@@ -2238,34 +2238,51 @@ __global__ void __launch_bounds__(256) pad_phase_kernel(const S* __restrict__ sr
                                                         int cp, T* __restrict__ dst) {
   ptx::griddep_wait();
   ptx::griddep_launch_dependents();
-  // One destination row (n, h, column phase py) per block iteration, its W2
-  // 16-byte pixels across the threads (no 64-bit index division per pixel).
-  const int rows = N * H * s;
-  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
-    const int py = s == 1 ? 0 : (r & 1);
-    const long long nh = s == 1 ? r : (r >> 1);  // n * H + h
+  // U destination rows (n, h, column phase py) per block
+  // iteration, their W2 16-byte pixels across the threads: every thread has
+  // the loads of several rows in flight before it stores (one row's 12-byte
+  // pixel per thread left the pass latency-bound at ~4.4 TB/s).
+  // Block b owns the contiguous rows [b rows / B, (b + 1) rows / B): one
+  // resident wave, no half-empty second one.
+  constexpr int U = 4;
+  const int rows_all = N * H * s;
+  const int rb = (int)((long long)blockIdx.x * rows_all / gridDim.x);
+  const int rows = (int)((long long)(blockIdx.x + 1) * rows_all / gridDim.x);
+  for (int r0 = rb; r0 < rows; r0 += U) {
     for (int w2 = threadIdx.x; w2 < W2; w2 += blockDim.x) {
-      const long long i = (long long)r * W2 + w2;
-      const int col = s * w2 + py - pad_l;
-      float v[8];
-      const bool in = col >= 0 && col < W;
-      const S* px = src + (nh * W + (in ? col : 0)) * C;
+      float v[U][8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if constexpr (sizeof(S) == 4) v[c] = in && c < C && c < cp ? __ldg(px + c) : 0.0f;
-        else v[c] = in && c < C && c < cp ? __bfloat162float(px[c]) : 0.0f;
+      for (int u = 0; u < U; ++u) {
+        const int r = r0 + u;
+        const int py = s == 1 ? 0 : (r & 1);
+        const long long nh = s == 1 ? r : (r >> 1);  // n * H + h
+        const int col = s * w2 + py - pad_l;
+        const bool in = r < rows && col >= 0 && col < W;
+        const S* px = src + (in ? (nh * W + col) * C : 0);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if constexpr (sizeof(S) == 4) v[u][c] = in && c < C && c < cp ? __ldg(px + c) : 0.0f;
+          else v[u][c] = in && c < C && c < cp ? __bfloat162float(px[c]) : 0.0f;
+        }
       }
-      if constexpr (sizeof(T) == 4) {
-        reinterpret_cast<float4*>(dst)[i] = make_float4(v[0], v[1], v[2], v[3]);
-      } else {
-        uint4 u;
-        __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]), b1 = __floats2bfloat162_rn(v[2], v[3]),
-                       b2 = __floats2bfloat162_rn(v[4], v[5]), b3 = __floats2bfloat162_rn(v[6], v[7]);
-        u.x = *reinterpret_cast<uint32_t*>(&b0);
-        u.y = *reinterpret_cast<uint32_t*>(&b1);
-        u.z = *reinterpret_cast<uint32_t*>(&b2);
-        u.w = *reinterpret_cast<uint32_t*>(&b3);
-        reinterpret_cast<uint4*>(dst)[i] = u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (r0 + u >= rows) break;
+        const long long i = (long long)(r0 + u) * W2 + w2;
+        if constexpr (sizeof(T) == 4) {
+          reinterpret_cast<float4*>(dst)[i] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+        } else {
+          uint4 q;
+          __nv_bfloat162 b0 = __floats2bfloat162_rn(v[u][0], v[u][1]),
+                         b1 = __floats2bfloat162_rn(v[u][2], v[u][3]),
+                         b2 = __floats2bfloat162_rn(v[u][4], v[u][5]),
+                         b3 = __floats2bfloat162_rn(v[u][6], v[u][7]);
+          q.x = *reinterpret_cast<uint32_t*>(&b0);
+          q.y = *reinterpret_cast<uint32_t*>(&b1);
+          q.z = *reinterpret_cast<uint32_t*>(&b2);
+          q.w = *reinterpret_cast<uint32_t*>(&b3);
+          reinterpret_cast<uint4*>(dst)[i] = q;
+        }
       }
     }
   }
@@ -3233,16 +3250,18 @@ void launch_narrow_halo(const ConvGeom& g, const ConvPlan& c, const float* in, c
   if (!run) return;
   const int W2 = narrow_w2(g);
   if ((long long)g.N * g.H * s > 2147483647ll) fail(TK_ERR_CAPABILITY, "narrow halo: too many rows");
-  const int pblocks = (int)std::min<long long>((long long)g.N * g.H * s, (long long)sm_count() * 32);
+  const unsigned pthreads = (unsigned)std::min(256, (W2 + 31) / 32 * 32);
+  const int pblocks = (int)std::min<long long>((long long)g.N * g.H * s,
+                                               (long long)sm_count() * (2048 / pthreads));
   if (c.tf32)
-    launch_pdl(pad_phase_kernel<float, float>, (unsigned)pblocks, 256, st, in, g.N, g.H, g.W, g.C,
+    launch_pdl(pad_phase_kernel<float, float>, (unsigned)pblocks, pthreads, st, in, g.N, g.H, g.W, g.C,
                s, W2, g.pad_l, cp, (float*)xin);
   else if (io_in_bf16())
-    launch_pdl(pad_phase_kernel<__nv_bfloat16, __nv_bfloat16>, (unsigned)pblocks, 256, st,
+    launch_pdl(pad_phase_kernel<__nv_bfloat16, __nv_bfloat16>, (unsigned)pblocks, pthreads, st,
                reinterpret_cast<const __nv_bfloat16*>(in), g.N, g.H, g.W, g.C, s, W2, g.pad_l, cp,
                (__nv_bfloat16*)xin);
   else
-    launch_pdl(pad_phase_kernel<__nv_bfloat16, float>, (unsigned)pblocks, 256, st, in, g.N, g.H,
+    launch_pdl(pad_phase_kernel<__nv_bfloat16, float>, (unsigned)pblocks, pthreads, st, in, g.N, g.H,
                g.W, g.C, s, W2, g.pad_l, cp, (__nv_bfloat16*)xin);
   const int cg = 2;
   TcArgs p{};
