@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <string>
 
@@ -26,6 +27,30 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 
 #define TKB_CUDA(x) ::tkb::cuda_check((x), #x)
+
+// Checked builds (`make checked` -> libtilekit_b200_checked.so, built with
+// -DTKB_CHECKED=1): device-side invariants of the hand-written indexing --
+// shared-memory layout, staging / TMEM / tail / split slots, gather and pad
+// source ranges -- as the stand-in for compute-sanitizer, which this GPU
+// pool does not allow.  A violated check prints its site and traps, so the
+// launch fails and the C ABI reports TK_ERR_CUDA.  Free in release builds.
+#ifndef TKB_CHECKED
+#define TKB_CHECKED 0
+#endif
+#if TKB_CHECKED
+#define TKB_DCHECK(cond)                                                                   \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("TKB_DCHECK failed: %s (%s:%d, block %d thread %d)\n", #cond, __FILE__,      \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                 \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define TKB_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 // Counts kernel launches (tk_launch_count); bumped by every launcher.
 void note_launch(int n = 1);

@@ -460,6 +460,7 @@ __global__ void exact_gemm_loc_kernel(ExactArgs p, int wg_r, int wg_c, int stage
       const int n = n0 + own_index<W, BL>(tn, wg_c, j);
       if (n >= p.N) continue;
       const long long off = row_off + (long long)n * p.d_sn;
+      TKB_DCHECK(off >= 0 && (!CONV || off < (long long)p.M * p.N));
       float v = __fmul_rn(p.alpha, acc[i][j]);
       if (p.read_c) v = __fadd_rn(v, __fmul_rn(p.beta, gc[off]));
       gd[off] = v;

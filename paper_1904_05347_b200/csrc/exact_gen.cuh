@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(SMALL ? 256 : 1024, SMALL ? 2 : 1)
       const int n = n0 + j * wg_c + tn;
       if (n >= p.N) continue;
       const long long off = row_off + (long long)n * p.d_sn;
+      TKB_DCHECK(off >= 0 && (!CONV || off < (long long)p.M * p.N));
       float v = __fmul_rn(p.alpha, acc[i][j]);
       if (p.read_c) v = __fadd_rn(v, __fmul_rn(p.beta, gc[off]));
       gd[off] = v;

@@ -254,6 +254,7 @@ __device__ __forceinline__ Unit decode_tile(const TcArgs& p, int t) {
   }
   u.sp = fdiv(rest, p.fd_batch);
   u.z = rest - u.sp * p.batch;
+  TKB_DCHECK(u.sp < p.splits && u.m_blk < p.num_m && u.n_blk < p.num_n);
   u.kb0 = u.sp * p.kb_per;
   u.kb1 = min(p.num_kb, u.kb0 + p.kb_per);
   return u;
@@ -291,11 +292,16 @@ __device__ __forceinline__ Unit decode_unit(const TcArgs& p, int t) {
   return decode_tile(p, t);
 }
 
+__host__ __device__ inline long long total_tiles_of_dev(const TcArgs& p) {
+  return (long long)p.num_m * p.num_n * p.batch;
+}
+
 // Tail piece epilogue: this thread's accumulator row (TMEM lane `row`) into
 // the slot's column-major [BN][128] partial tile (lanes = consecutive rows:
 // coalesced 128-byte stores per column).
 __device__ __forceinline__ void store_tail_piece(const TcArgs& p, uint32_t taddr, int slot,
                                                  uint32_t rank, int cg, int row) {
+  TKB_DCHECK(slot >= 0 && slot < (int)(total_tiles_of_dev(p) - p.tail_start) * p.tail_q);
   float* dst = p.tail_part + ((long long)slot * cg + rank) * ((long long)p.BN * 128);
   for (int col = 0; col < p.BN; col += 32) {
     float v[32];
@@ -491,6 +497,7 @@ __device__ __forceinline__ void tma_store_epilogue_multi(const TcArgs& p, uint32
     for (int j0 = 0; j0 < nchunks; j0 += bs) {
       const int nb = min(bs, nchunks - j0);
       uint8_t* half = stage + ring * bs * kRows * kSlabBytes;
+      TKB_DCHECK(ring < p.epi_slots && (ring + 1) * bs * kRows * kSlabBytes <= p.epi_bytes / p.epi_groups);
       if (++ring == p.epi_slots) ring = 0;
       if (issuer) ptx::bulk_wait_read_dyn(p.epi_slots - 1);
       ptx::epi_sync(bar);
@@ -733,6 +740,20 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
   // gather mode: K -> {element offset (x*W + y)*C + c, (x << 16) | y} table,
   // K padded to whole slabs with out-of-window markers.
   int2* ktab = reinterpret_cast<int2*>(epi_stage + p.epi_bytes);
+#if TKB_CHECKED
+  if (threadIdx.x == 0) {
+    uint32_t dsmem;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsmem));
+    const long long end = (reinterpret_cast<uint8_t*>(ktab) - smem_raw) +
+                          (MODE == kConvGather ? (long long)p.num_kb * 32 * 8 : 0);
+    TKB_DCHECK(end <= (long long)dsmem);                        // layout fits the allocation
+    TKB_DCHECK(reinterpret_cast<uint8_t*>(tmem_slot + 1) <= epi_stage);  // barriers before staging
+    TKB_DCHECK(stage_bytes % 1024 == 0 && (reinterpret_cast<uintptr_t>(base) & 1023) == 0);
+    TKB_DCHECK(p.stages >= 2 && p.stages <= kMaxStages && p.acc_slots <= kMaxAcc);
+    TKB_DCHECK(p.acc_slots * p.acc_cols <= 2 * kAccCols && p.BN <= p.acc_cols);  // TMEM ring
+    TKB_DCHECK(p.splits >= 1 && p.splits <= kMaxSplits);
+  }
+#endif
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
   const uint32_t rank = CG == 2 ? ptx::cluster_rank() : 0;
@@ -859,6 +880,7 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
           for (int x = px; x < p.R; x += s)
             for (int y = py; y < p.S; y += s) {
               const uint32_t off = ph * p.phase_bytes + ((x / s) * p.P + y / s) * 16;
+              TKB_DCHECK((q >> 1) < kMaxNarrowMma && off < (uint32_t)p.halo_tx);
               if ((q & 1) == 0) {
                 mma_off[q >> 1] = off;
                 mma_lbo[q >> 1] = 0;  // (odd last tap: paired with zero filter rows)
@@ -2259,6 +2281,7 @@ __global__ void __launch_bounds__(256) pad_phase_kernel(const S* __restrict__ sr
         const int col = s * w2 + py - pad_l;
         const bool in = r < rows && col >= 0 && col < W;
         const S* px = src + (in ? (nh * W + col) * C : 0);
+        TKB_DCHECK(!in || nh < (long long)N * H);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           if constexpr (sizeof(S) == 4) v[u][c] = in && c < C && c < cp ? __ldg(px + c) : 0.0f;
@@ -2381,6 +2404,8 @@ __global__ void __launch_bounds__(256) pointwise_gather_kernel(const S* __restri
       const int ow = fdiv(i, fd_c4), c = (i - ow * c4) * 4;
       const long long o = (long long)r * per_row + i;
       const S* sp = src + (long long)ow * g.stride * g.C + c;
+      TKB_DCHECK(ow < g.OW && (long long)oh * g.stride < g.H && (long long)ow * g.stride < g.W &&
+                 n < g.N);
       if constexpr (sizeof(S) == 2) {  // bf16 activations in: a strided copy
         const uint2 u = __ldg(reinterpret_cast<const uint2*>(sp));
         reinterpret_cast<uint2*>(out)[o] = u;
