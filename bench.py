@@ -972,24 +972,32 @@ def main():
             gb = torch.rand(n * n, device=dev) * 2 - 1
             gc = torch.empty(n * n, device=dev)
             gshape = tk.GemmShape(n, n, n)
-            for p_ in ("tf32", "bf16", "3xtf32"):
+            for p_ in ("tf32", "bf16", "bf16_io", "3xtf32"):
                 if p_ == "3xtf32" and n != 8192:
                     continue
+                # bf16_io: bf16 operands in HBM (exec_options io="in_bf16"),
+                # the fp32 -> bf16 conversion of A and B not in the timed call
+                io_ = p_ == "bf16_io"
+                o_ = tk.exec_options("bf16" if io_ else p_, io="in_bf16" if io_ else "fp32")
+                ga_, gb_ = (ga.to(torch.bfloat16), gb.to(torch.bfloat16)) if io_ else (ga, gb)
                 for _ in range(2):
-                    tk.gemm_dev(ga, gb, None, gc, gshape, None, precision=p_, stream=stream)
+                    tk.gemm_dev(ga_, gb_, None, gc, gshape, None, stream=stream, options=o_)
                 ts = []
                 for _ in range(5):
                     a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     a_.record(stream)
-                    tk.gemm_dev(ga, gb, None, gc, gshape, None, precision=p_, stream=stream)
+                    tk.gemm_dev(ga_, gb_, None, gc, gshape, None, stream=stream, options=o_)
                     b_.record(stream)
                     b_.synchronize()
                     ts.append(a_.elapsed_time(b_))
                 ms = float(np.median(ts))
                 tf = 2 * n ** 3 / (ms * 1e-3) / 1e12
-                pk = peaks["bf16_tflops"] / {"tf32": 2.0, "bf16": 1.0, "3xtf32": 6.0}[p_]
+                pk = peaks["bf16_tflops"] / {"tf32": 2.0, "bf16": 1.0, "bf16_io": 1.0, "3xtf32": 6.0}[p_]
                 secondary[f"gemm{n}_{p_}"] = {"value": round(tf * 1e3, 1), "unit": "GFLOP/s",
                                               "ms": round(ms, 4), "frac_of_peak": round(tf / pk, 4)}
+                if io_:
+                    secondary[f"gemm{n}_{p_}"]["operands"] = "bf16 in HBM (A packed bf16 -> bf16)"
+                del ga_, gb_
             del ga, gb, gc
         n = 1024
         ga = torch.rand(n * n, device=dev) * 2 - 1
@@ -1081,8 +1089,8 @@ def main():
                 "roofline_frac": roofline["frac"]}
         for key in ("vgg16_tf32", "vgg16_bf16", "vgg16_bf16_io", "vgg16_3xtf32", "vgg16_fp32",
                     "resnet50_tf32", "resnet50_bf16", "resnet50_bf16_io", "resnet50_tiled_fp32", "sgemm1024_fp32", "sgemm1024_tf32",
-                    "sgemm1024_bf16", "gemm4096_tf32", "gemm4096_bf16", "gemm8192_tf32",
-                    "gemm8192_bf16"):
+                    "sgemm1024_bf16", "gemm4096_tf32", "gemm4096_bf16", "gemm4096_bf16_io",
+                    "gemm8192_tf32", "gemm8192_bf16", "gemm8192_bf16_io"):
             if key in secondary:
                 v = secondary[key]
                 summ[key] = {"gflops": v["value"], "ms": v.get("ms_per_step", v.get("ms"))}

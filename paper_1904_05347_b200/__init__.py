@@ -695,17 +695,18 @@ def tuning_db_size() -> int:
 def gemm_dev(a, b, c, out, shape: GemmShape, cfg: Optional[GemmConfig] = None,
              precision="fp32", stream=None, tile_n=0, options=None) -> None:
     """options: an exec_options(...) record (tensor-core knobs); overrides
-    precision / tile_n when given."""
+    precision / tile_n when given.  exec_options("bf16", io="in_bf16"): A and
+    B are bfloat16 tensors (bf16 operands in HBM); C and out stay float32."""
+    opts = options if options is not None else exec_options(precision, tile_n)
     na, nb, nc = _gemm_sizes(shape)
-    _need_dev(a, "gemm: operand A", na)
-    _need_dev(b, "gemm: operand B", nb)
+    _need_dev(a, "gemm: operand A", na, bf16=bool(opts.io & 1))
+    _need_dev(b, "gemm: operand B", nb, bf16=bool(opts.io & 1))
     if shape.beta != 0.0:
         if c is None:
             raise ContractError("gemm: beta != 0 needs operand C")
         _need_dev(c, "gemm: operand C", nc)
     _need_dev(out, "gemm: output", nc)
     cfg_c = C.byref(cfg.c()) if cfg is not None else None
-    opts = options if options is not None else exec_options(precision, tile_n)
     _check(lib().tk_gemm_dev(C.byref(shape.c()), cfg_c, C.byref(opts),
                              _dptr(a), _dptr(b), _dptr(c), _dptr(out), _stream(stream)))
 

@@ -847,6 +847,9 @@ int tk_gemm_dev(const tk_gemm_shape* shape, const tk_gemm_config* cfg, const tk_
     const tilekit::GemmShape g = gemm_shape(shape);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int prec = precision_of(opts);
+    if (tc_knobs().io != 0 && (tc_knobs().io != TK_IO_IN_BF16 || prec != TK_PREC_BF16))
+      fail(TK_ERR_CAPABILITY, "gemm: io flags: bf16 operands (TK_IO_IN_BF16) with BF16 precision "
+                              "only; C and the output stay fp32");
     if (prec == TK_PREC_FP32_EXACT) {
       const ExactLaunch L = cfg ? exact_launch_of(gemm_config(cfg)) : exact_auto((long long)g.m, (long long)g.n);
       launch_exact(gemm_args(g, d_a, d_b, d_c, d_out), L, false, 1, st);
@@ -863,6 +866,8 @@ int tk_gemm_ex(const tk_gemm_shape* shape, const tk_exec_options* opts, const fl
                const float* b, const float* c, float* out) {
   return guarded([&] {
     KnobScope knobs(opts);
+    if (tc_knobs().io != 0)
+      fail(TK_ERR_CAPABILITY, "gemm: io flags apply to the device-buffer call (tk_gemm_dev)");
     const tilekit::GemmShape g = gemm_shape(shape);
     cudaStream_t st = host_stream();
     const size_t na = g.m * g.k, nb = g.k * g.n, nc = g.m * g.n;

@@ -2018,9 +2018,23 @@ __device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v, int) {
   return __float2bfloat16_rn(v);
 }
 
+// Pack sources: fp32 operands, or bf16 ones (bf16 operands in HBM,
+// tk_exec_options.io) -- read as float, 4 consecutive elements at a time.
+__device__ __forceinline__ float src_f(const float* p) { return *p; }
+__device__ __forceinline__ float src_f(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float4 src_f4(const float* p) {
+  return __ldcs(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ float4 src_f4(const __nv_bfloat16* p) {
+  const uint2 u = __ldcs(reinterpret_cast<const uint2*>(p));
+  const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
+  const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+  return make_float4(__low2float(lo), __high2float(lo), __low2float(hi), __high2float(hi));
+}
+
 // dst[r][kk] (row length kp, zero for kk >= k) = src[r*rs + kk*ks].
-template <typename T>
-__global__ void __launch_bounds__(256) pack_kmajor_kernel(const float* __restrict__ src,
+template <typename T, typename S = float>
+__global__ void __launch_bounds__(256) pack_kmajor_kernel(const S* __restrict__ src,
                                                           long long rs, long long ks, long long rows,
                                                           long long k, long long kp,
                                                           T* __restrict__ dst, int tf32_round) {
@@ -2030,12 +2044,12 @@ __global__ void __launch_bounds__(256) pack_kmajor_kernel(const float* __restric
   if (ks == 1) {
     for (int i = ty; i < 32; i += 8) {
       const long long r = r0 + i, kk = k0 + tx;
-      tile[i][tx] = (r < rows && kk < k) ? src[r * rs + kk] : 0.0f;
+      tile[i][tx] = (r < rows && kk < k) ? src_f(src + r * rs + kk) : 0.0f;
     }
   } else {
     for (int i = ty; i < 32; i += 8) {
       const long long r = r0 + tx, kk = k0 + i;
-      tile[tx][i] = (r < rows && kk < k) ? src[r * rs + kk * ks] : 0.0f;
+      tile[tx][i] = (r < rows && kk < k) ? src_f(src + r * rs + kk * ks) : 0.0f;
     }
   }
   __syncthreads();
@@ -2047,8 +2061,8 @@ __global__ void __launch_bounds__(256) pack_kmajor_kernel(const float* __restric
 
 // Row-contiguous source (ks == 1): dst[r][kk] = src[r*rs + kk], 4 elements
 // per thread, vector loads and stores, zero tail up to kp.
-template <typename T>
-__global__ void __launch_bounds__(256) pack_rows_kernel(const float* __restrict__ src, long long rs,
+template <typename T, typename S = float>
+__global__ void __launch_bounds__(256) pack_rows_kernel(const S* __restrict__ src, long long rs,
                                                         long long rows, long long k, long long kp,
                                                         T* __restrict__ dst, int tf32_round) {
   const long long per_row = kp / 4;
@@ -2057,11 +2071,11 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const float* __restrict_
        i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / per_row, kk = (i - r * per_row) * 4;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (kk + 3 < k) v = __ldcs(reinterpret_cast<const float4*>(src + r * rs + kk));
+    if (kk + 3 < k) v = src_f4(src + r * rs + kk);
     else {
-      if (kk < k) v.x = src[r * rs + kk];
-      if (kk + 1 < k) v.y = src[r * rs + kk + 1];
-      if (kk + 2 < k) v.z = src[r * rs + kk + 2];
+      if (kk < k) v.x = src_f(src + r * rs + kk);
+      if (kk + 1 < k) v.y = src_f(src + r * rs + kk + 1);
+      if (kk + 2 < k) v.z = src_f(src + r * rs + kk + 2);
     }
     T* d = dst + r * kp + kk;
     if constexpr (sizeof(T) == 4) {
@@ -2079,8 +2093,8 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const float* __restrict_
 
 // dst[r][kk] = src[r + kk*ks] for a 64-row x 64-k tile per block: float4
 // loads along r, float4 (fp32) / 8-byte (bf16) stores along kk.
-template <typename T>
-__global__ void __launch_bounds__(256) pack_transpose_kernel(const float* __restrict__ src,
+template <typename T, typename S = float>
+__global__ void __launch_bounds__(256) pack_transpose_kernel(const S* __restrict__ src,
                                                              long long ks, long long rows,
                                                              long long k, long long kp,
                                                              T* __restrict__ dst, int tf32_round) {
@@ -2092,7 +2106,7 @@ __global__ void __launch_bounds__(256) pack_transpose_kernel(const float* __rest
     const int kk = t / 16 + 16 * j, r4 = (t % 16) * 4;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (k0 + kk < k && r0 + r4 < rows)  // rows % 4 == 0: whole float4 in range
-      v = __ldcs(reinterpret_cast<const float4*>(src + (k0 + kk) * ks + r0 + r4));
+      v = src_f4(src + (k0 + kk) * ks + r0 + r4);
     tile[kk][r4] = v.x;
     tile[kk][r4 + 1] = v.y;
     tile[kk][r4 + 2] = v.z;
@@ -2118,17 +2132,18 @@ __global__ void __launch_bounds__(256) pack_transpose_kernel(const float* __rest
   }
 }
 
-template <typename T>
-void pack_kmajor(const float* src, long long rs, long long ks, long long rows, long long k,
+template <typename T, typename S = float>
+void pack_kmajor(const S* src, long long rs, long long ks, long long rows, long long k,
                  long long kp, T* dst, bool tf32_round, cudaStream_t st) {
-  const bool src16 = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  // (vector paths: 4 source elements = 16 bytes fp32 / 8 bytes bf16)
+  const bool src16 = (reinterpret_cast<uintptr_t>(src) & (4 * sizeof(S) - 1)) == 0;
   // Column-contiguous source (a column-major operand read along its rows):
   // 64 x 64 tiles transposed through shared memory with 16-byte accesses
   // on both sides.
   if (rs == 1 && ks % 4 == 0 && rows % 4 == 0 && kp % 4 == 0 && src16) {
     dim3 grid((unsigned)((kp + 63) / 64), (unsigned)((rows + 63) / 64));
     if (grid.y > 65535) fail(TK_ERR_CAPABILITY, "pack: too many rows");
-    pack_transpose_kernel<T><<<grid, 256, 0, st>>>(src, ks, rows, k, kp, dst, tf32_round ? 1 : 0);
+    pack_transpose_kernel<T, S><<<grid, 256, 0, st>>>(src, ks, rows, k, kp, dst, tf32_round ? 1 : 0);
     note_launch();
     TKB_CUDA(cudaGetLastError());
     return;
@@ -2136,14 +2151,14 @@ void pack_kmajor(const float* src, long long rs, long long ks, long long rows, l
   if (ks == 1 && rs % 4 == 0 && kp % 4 == 0 && src16) {
     const long long n = rows * (kp / 4);
     const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)sm_count() * 16);
-    pack_rows_kernel<T><<<blocks, 256, 0, st>>>(src, rs, rows, k, kp, dst, tf32_round ? 1 : 0);
+    pack_rows_kernel<T, S><<<blocks, 256, 0, st>>>(src, rs, rows, k, kp, dst, tf32_round ? 1 : 0);
     note_launch();
     TKB_CUDA(cudaGetLastError());
     return;
   }
   dim3 grid((unsigned)((kp + 31) / 32), (unsigned)((rows + 31) / 32));
   if (grid.y > 65535) fail(TK_ERR_CAPABILITY, "pack: too many rows");
-  pack_kmajor_kernel<T><<<grid, dim3(32, 8), 0, st>>>(src, rs, ks, rows, k, kp, dst, tf32_round);
+  pack_kmajor_kernel<T, S><<<grid, dim3(32, 8), 0, st>>>(src, rs, ks, rows, k, kp, dst, tf32_round);
   note_launch();
   TKB_CUDA(cudaGetLastError());
 }
@@ -2690,9 +2705,14 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
   const long long kp = tf32 ? (long long)((k + 3) / 4 * 4) : (long long)((k + 7) / 8 * 8);
   // TF32 operands already K-major with 16-byte rows are used in place;
   // everything else is packed (and converted for BF16).
+  // bf16 operands in HBM (tk_exec_options.io, BF16 only): a and b address
+  // bf16 column-major matrices; K-major ones with 16-byte rows are used in
+  // place, the rest are packed bf16 -> bf16 (no conversion).
+  const bool in16 = (tc_knobs().io & TK_IO_IN_BF16) != 0;
+  if (in16 && tf32) fail(TK_ERR_CAPABILITY, "gemm: bf16 operands (io flags) need BF16 precision");
   auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  const bool a_ok = tf32 && ta && kp == (long long)k && aligned(a);
-  const bool b_ok = tf32 && !tb && kp == (long long)k && aligned(b);
+  const bool a_ok = (tf32 || in16) && ta && kp == (long long)k && aligned(a);
+  const bool b_ok = (tf32 || in16) && !tb && kp == (long long)k && aligned(b);
   // Column-major, untransposed A is MN-major: the tensor core reads it in
   // place (no transpose pass) when M is a multiple of 32.
   const bool mn_on = experiments().a_mn;
@@ -2704,6 +2724,9 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
   void* pb = spb.get();
   auto pack = [&](const float* src, long long rs, long long ks, long long rows, void* dst) {
     if (tf32) pack_kmajor<float>(src, rs, ks, rows, (long long)k, kp, (float*)dst, false, st);
+    else if (in16)
+      pack_kmajor<__nv_bfloat16, __nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(src), rs, ks,
+                                                rows, (long long)k, kp, (__nv_bfloat16*)dst, false, st);
     else pack_kmajor<__nv_bfloat16>(src, rs, ks, rows, (long long)k, kp, (__nv_bfloat16*)dst, false, st);
   };
   if (!a_ok && !a_mn) {

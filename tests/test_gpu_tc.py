@@ -50,6 +50,34 @@ def test_tc_gemm_colmajor(tk, oracle, m, n, k, ta, tb, prec):
     assert err <= TOL[prec], err
 
 
+@pytest.mark.parametrize("m,n,k,ta,tb", [(1024, 1024, 1024, 0, 0), (512, 384, 256, 1, 0),
+                                         (256, 200, 100, 1, 1), (300, 128, 72, 0, 1),
+                                         (4096, 256, 512, 0, 0)])
+def test_tc_gemm_bf16_operands(tk, oracle, m, n, k, ta, tb):
+    """BF16 GEMM on bf16 operands in HBM (exec_options io="in_bf16"): no
+    fp32 -> bf16 conversion; K-major operands read in place, the others
+    packed bf16 -> bf16.  Same bits as the fp32-operand BF16 GEMM on the same
+    (bf16-exact) values, and within the BF16 bar of the oracle."""
+    import torch
+    a = oracle.fill_random(m * k, 6)
+    b = oracle.fill_random(k * n, 7)
+    c = oracle.fill_random(m * n, 8)
+    da16 = torch.from_numpy(a).cuda().to(torch.bfloat16)
+    db16 = torch.from_numpy(b).cuda().to(torch.bfloat16)
+    a16, b16 = da16.float().cpu().numpy(), db16.float().cpu().numpy()
+    want = oracle.gemm_naive(m, n, k, 1.25, 0.5, ta, tb, a16, b16, c)
+    shape = tk.GemmShape(m, n, k, 1.25, 0.5, "t" if ta else "n", "t" if tb else "n")
+    dc = torch.from_numpy(c).cuda()
+    out = torch.full((m * n,), float("nan"), device="cuda")
+    tk.gemm_dev(da16, db16, dc, out, shape, options=tk.exec_options("bf16", io="in_bf16"))
+    ref = torch.full((m * n,), float("nan"), device="cuda")
+    tk.gemm_dev(da16.float(), db16.float(), dc, ref, shape, precision="bf16")
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
+    err = oracle.max_scaled_error(out.cpu().numpy(), want)
+    assert err <= 1e-5, err  # bf16-exact operands: only fp32 accumulation order differs
+
+
 @pytest.mark.parametrize("prec", ["tf32", "bf16"])
 @pytest.mark.parametrize("split", [0, 2, 3, 5])
 @pytest.mark.parametrize("m,n,k,ta,tb", [(1024, 1024, 1024, 0, 0), (512, 768, 640, 1, 0),
