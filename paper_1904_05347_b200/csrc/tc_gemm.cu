@@ -1000,7 +1000,8 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
             dx = tap / p.S - p.pad_t;
           }
           if constexpr (MODE == kPlain) {
-            if (p.a_mn) ptx::tma3<CG>(sa, &map_a, fb, 0, k0, (m_blk * BM + rank * kRows) / 32);
+            if (p.a_mn)  // MN-major A: M blocks of 32 tf32 / 64 bf16 (128 bytes)
+              ptx::tma3<CG>(sa, &map_a, fb, 0, k0, (m_blk * BM + rank * kRows) / (TF32 ? 32 : 64));
             else ptx::tma3<CG>(sa, &map_a, fb, k0, m_blk * BM + rank * kRows, z);
             ptx::tma3<CG>(sb, &map_b, fb, k0, n_blk * p.BN + rank * b_rows, z);
           } else if constexpr (MODE == kConvIm2col) {
@@ -1042,7 +1043,8 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       const bool a_mn = MODE == kPlain && p.a_mn;
       const uint32_t idesc = ptx::idesc(BM, p.BN, TF32) | (a_mn ? (1u << 15) : 0u);
       const uint64_t kdesc = ptx::desc_sw128(0);
-      const uint64_t kdesc_mn = ptx::desc_sw128_mn(0, 4096, 512);
+      const uint64_t kdesc_mn =
+          TF32 ? ptx::desc_sw128_mn(0, 4096, 512) : ptx::desc_sw128_mn16(0, 8192, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int nlocal = 0;
@@ -1066,7 +1068,9 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
             const uint32_t sa = ptx::smem(base + stage * stage_bytes);
             const uint64_t ad = (a_mn ? kdesc_mn : kdesc) + (sa >> 4);
             const uint64_t bd = kdesc + ((sa + (uint32_t)a_bytes) >> 4);
-            const uint64_t a_step = a_mn ? 64 : 2;  // K = 8: one 1 KiB atom / 32 bytes
+            // K step of one MMA (32 bytes of K): MN-major tf32 two 512-B
+            // atoms (1 KiB), MN-major bf16 two 1-KiB atoms (2 KiB), K-major 32 B
+            const uint64_t a_step = a_mn ? (TF32 ? 64 : 128) : 2;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               ptx::mma_cg<CG, TF32>(d_tmem, ad + a_step * kk, bd + 2 * kk, idesc,
@@ -2624,7 +2628,18 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
     p.part_stride = (long long)g.M * g.N;
   }
   CUtensorMap ma;
-  if (g.a_mn) {
+  if (g.a_mn && !tf32) {
+    // bf16 MN-major A: view {64 (M inner), K (stride lda), M / 64 (stride
+    // 128 B)}, box {64, 64, 2}, the canonical 128-byte swizzle
+    if (g.batch != 1 || g.M % 64 != 0 || (g.lda * 2) % 16 != 0)
+      fail(TK_ERR_CAPABILITY, "tc_gemm: MN-major bf16 A needs batch 1, M % 64 == 0");
+    const long long ak = g.a_k > 0 ? std::min<long long>(g.a_k, g.K) : g.K;
+    cuuint64_t dims[3] = {64, (cuuint64_t)ak, (cuuint64_t)(g.M / 64)};
+    cuuint64_t strides[2] = {(cuuint64_t)g.lda * 2, 128};
+    cuuint32_t box[3] = {64, 64, (cuuint32_t)(kRows / 64)};
+    ma = make_map(g.a, 2, 3, dims, strides, box);
+    p.a_mn = 1;
+  } else if (g.a_mn) {
     if (!tf32 || g.batch != 1 || g.M % 32 != 0 || (g.lda * 4) % 16 != 0)
       fail(TK_ERR_CAPABILITY, "tc_gemm: MN-major A needs TF32, batch 1, M % 32 == 0");
     // view {32 (M inner), K (stride lda), M / 32 (stride 128 B)}, box {32, 32, 4}
@@ -2716,7 +2731,10 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
   // Column-major, untransposed A is MN-major: the tensor core reads it in
   // place (no transpose pass) when M is a multiple of 32.
   const bool mn_on = experiments().a_mn;
-  const bool a_mn = mn_on && tf32 && !ta && m % 32 == 0 && aligned(a) && m <= (1ull << 31);
+  // (bf16 operands in HBM: the same in-place read of an untransposed A, in
+  // 64-element M blocks)
+  const bool a_mn = mn_on && !ta && aligned(a) && m <= (1ull << 31) &&
+                    ((tf32 && m % 32 == 0) || (in16 && m % 64 == 0));
   const size_t esz = tf32 ? 4 : 2;
   Scratch spa(st, kScratchPackA, (!a_ok && !a_mn) ? (size_t)m * kp * esz : 0);
   Scratch spb(st, kScratchPackB, !b_ok ? (size_t)n * kp * esz : 0);

@@ -221,6 +221,21 @@ __device__ __forceinline__ uint64_t desc_sw128_mn(uint32_t smem_addr, uint32_t l
   return d;
 }
 
+// MN-major 16-bit operand (bf16), the canonical 128-byte-swizzled layout
+// (layout type 2; TMA CU_TENSOR_MAP_SWIZZLE_128B): 64 elements of M per
+// 128-byte row, K rows 128 B apart in 8-row atoms `sbo` bytes apart, M blocks
+// of 64 `lbo` bytes apart.  One K = 16 MMA reads two atoms.
+__device__ __forceinline__ uint64_t desc_sw128_mn16(uint32_t smem_addr, uint32_t lbo,
+                                                    uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 // K-major operand without swizzle (the "interleaved" canonical layout):
 // 8-row x 16-byte core matrices, `sbo` bytes between 8-row groups (M/N),
 // `lbo` bytes between the two core matrices of a 32-byte K step.  Used for
