@@ -619,7 +619,7 @@ void conv_dev(const tilekit::ConvShape& s, const tk_conv_params* p, int precisio
 // serves every chunk.
 struct HostPipe {
   cudaStream_t compute = nullptr, copy_in = nullptr, copy_out = nullptr;
-  static constexpr int kMaxChunks = 8;
+  static constexpr int kMaxChunks = 32;
   cudaEvent_t ready = nullptr, in_done[kMaxChunks] = {}, run_done[kMaxChunks] = {},
               out_done = nullptr;
   HostPipe() {
@@ -650,9 +650,12 @@ HostPipe& host_pipe() {
 // Number of equal batch chunks: the largest divisor of the batch <= 8 that
 // keeps every chunk's copies >= 2 MiB (a copy's fixed cost is ~10 us).
 int pipeline_chunks(const ConvGeom& g) {
+  const Experiments& xp = experiments();
+  const int max_chunks = xp.pipe_chunks > 0 ? std::min(xp.pipe_chunks, HostPipe::kMaxChunks) : 8;
+  const size_t min_bytes = xp.pipe_min_kb > 0 ? (size_t)xp.pipe_min_kb << 10 : (2u << 20);
   const size_t per_image = 4 * ((size_t)g.H * g.W * g.C + (size_t)g.OH * g.OW * g.K);
-  for (int n = HostPipe::kMaxChunks; n > 1; --n)
-    if (g.N % n == 0 && per_image * (size_t)(g.N / n) >= (2u << 20)) return n;
+  for (int n = max_chunks; n > 1; --n)
+    if (g.N % n == 0 && per_image * (size_t)(g.N / n) >= min_bytes) return n;
   return 1;
 }
 

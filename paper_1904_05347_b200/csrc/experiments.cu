@@ -29,6 +29,10 @@ const Experiments& experiments() {
     x.enabled = true;
     x.pdl = env_flag("TK_PDL", true);
     x.tail = env_flag("TK_TAIL", true);
+    x.tail_force = env_flag("TK_TAIL_FORCE", false);
+    x.red_gbs = env_int("TK_RED_GBS", 4000);
+    x.pipe_chunks = env_int("TK_PIPE_CHUNKS", 0);
+    x.pipe_min_kb = env_int("TK_PIPE_MIN_KB", 0);
     x.tc_stages = env_int("TK_TC_STAGES", 0);
     x.tc_epi = env_int("TK_TC_EPI", 0);
     x.epi_ring = env_flag("TK_EPI_RING", true);

@@ -15,6 +15,10 @@ struct Experiments {
   bool enabled = false;
   bool pdl = true;              // TK_PDL=0: no programmatic dependent launch
   bool tail = true;             // TK_TAIL=0: no stream-K tail
+  bool tail_force = false;      // TK_TAIL_FORCE=1: take the tail wherever it applies
+  double red_gbs = 4000.0;      // TK_RED_GBS: reduction-pass rate the split/tail models assume
+  int pipe_chunks = 0;          // TK_PIPE_CHUNKS: max batch chunks of the host-buffer pipeline
+  int pipe_min_kb = 0;          // TK_PIPE_MIN_KB: smallest chunk copy (KiB)
   int tc_stages = 0;            // TK_TC_STAGES: operand ring depth cap
   int tc_epi = 0;               // TK_TC_EPI: staging buffers cap
   bool epi_ring = true;         // TK_EPI_RING=0: whole-tile epilogue staging

@@ -1696,8 +1696,8 @@ TailPlan plan_tail(long long tiles, int num_kb, int cg, int bn) {
   // pieces written: ~ one per pair plus one per tile; read once, tiles written once
   const double red_bytes = (double)(pairs + rem) * tile_bytes * 2 + (double)rem * tile_bytes;
   const double cost = (double)full * (num_kb * slab + 1.0) + per * slab + 1.0 * segs + 2.0 +
-                      red_bytes / 4.0e6;
-  if (cost >= base * 0.97) return t;  // demand a win beyond the model's noise
+                      red_bytes / (experiments().red_gbs * 1e3);
+  if (cost >= base * 0.97 && !experiments().tail_force) return t;  // a win beyond the model's noise
   t.start = (int)(tiles - rem);
   t.q = std::max(q, 2);
   t.kb = segs;
@@ -2836,7 +2836,7 @@ double split_cost_us(long long units, int num_kb, long long pairs, int cg, int b
   const long long waves = (units * s + pairs - 1) / pairs;
   const int kb = (num_kb + s - 1) / s;
   double t = (double)waves * (kb * slab_time_us(cg, bn) + 1.0);
-  if (s > 1) t += 2.0 + (double)(s + 1) * out_bytes / 4.0e6;
+  if (s > 1) t += 2.0 + (double)(s + 1) * out_bytes / (experiments().red_gbs * 1e3);
   return t;
 }
 
