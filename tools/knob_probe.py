@@ -1,7 +1,9 @@
 """A/B of an experiment knob on conv layers, timed as bench.py times layers
 (graph of 4 x [256 MiB L2 eviction, run phase] minus the eviction alone).
 Each knob value runs in its own process (the library reads TK_* once).
-    python tools/knob_probe.py TK_EPI_SLOTS 2,4,6,8 vgg_conv1_1,conv1 [tf32]"""
+    python tools/knob_probe.py TK_EPI_SLOTS 2,4,6,8 vgg_conv1_1,conv1 [tf32]
+    python tools/knob_probe.py PROBE_OPTS mode=im2col:split=3,default res4a_branch2b
+(PROBE_OPTS values use ':' between options; the worker reads them with ',')."""
 import json
 import os
 import subprocess
@@ -56,9 +58,17 @@ if len(sys.argv) > 1 and sys.argv[1] == "--worker":
         x = torch.rand(shp.in_shape, device="cuda") * 2 - 1
         f = torch.rand(shp.filt_shape, device="cuda") * 2 - 1
         y = torch.empty(shp.out_shape, device="cuda")
-        ws = torch.empty(tk.conv2d_workspace_size(shp, im, prec) // 4 + 1, device="cuda")
-        tk.conv2d_prepare_dev(f, shp, im, ws, precision=prec, stream=st)
-        out[name] = round((graph_ms(lambda: tk.conv2d_run_dev(x, f, y, shp, im, ws, precision=prec,
+        # PROBE_OPTS="mode=im2col,split=3,cluster=1": per-call exec options
+        kw = dict(kv.split("=") for kv in os.environ.get("PROBE_OPTS", "").split(",") if kv)
+        opts = tk.exec_options(prec, mode=kw.get("mode", "auto"), split=int(kw.get("split", 0)),
+                               cluster=int(kw.get("cluster", 0)), stages=int(kw.get("stages", 0)))
+        try:
+            ws = torch.empty(tk.conv2d_workspace_size(shp, im, options=opts) // 4 + 1, device="cuda")
+        except tk.TilekitError:
+            out[name] = None
+            continue
+        tk.conv2d_prepare_dev(f, shp, im, ws, options=opts, stream=st)
+        out[name] = round((graph_ms(lambda: tk.conv2d_run_dev(x, f, y, shp, im, ws, options=opts,
                                                               stream=st)) - base) * 1e3, 1)
     print(json.dumps(out))
     sys.exit(0)
@@ -66,7 +76,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "--worker":
 knob, values, layers = sys.argv[1], sys.argv[2].split(","), sys.argv[3]
 prec = sys.argv[4] if len(sys.argv) > 4 else "tf32"
 for v in values:
-    env = dict(os.environ, TK_EXPERIMENTS="1", **({knob: v} if v != "default" else {}))
+    env = dict(os.environ, TK_EXPERIMENTS="1",
+               **({knob: v.replace(":", ",")} if v != "default" else {}))
     r = subprocess.run([sys.executable, __file__, "--worker", layers, prec], env=env,
                        capture_output=True, text=True)
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
