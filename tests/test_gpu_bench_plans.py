@@ -229,3 +229,33 @@ def test_bf16_activations_need_bf16_im2col(tk):  # host-only checks: CPU too
     # no conversion copy of the input in the workspace when it arrives in bf16
     assert tk.conv2d_workspace_size(shape, im, options=tk.exec_options("bf16", io="in_bf16")) < \
         tk.conv2d_workspace_size(shape, im, options=tk.exec_options("bf16"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(2, 20, 20, 3, 32, 3, 1), (2, 14, 14, 64, 96, 3, 1),
+                                   (2, 9, 9, 256, 48, 1, 1), (1, 30, 30, 3, 64, 7, 2),
+                                   (3, 17, 13, 128, 256, 3, 1)])
+def test_bf16_output_ragged_features(tk, oracle, shape):
+    """bf16 output on feature counts whose tiles are not 64-feature
+    multiples: either the exact result (within the BF16 + output-rounding
+    bar) or a CapabilityError -- never unwritten or garbage elements."""
+    import torch
+    N, H, C, K, R, st = shape[0], shape[1], shape[3], shape[4], shape[5], shape[6]
+    W = shape[2]
+    s = tk.ConvShape(N, H, W, C, K, R, R, st, True)
+    conv = oracle.Conv(N, H, W, C, K, R, R, st, True)
+    x = oracle.fill_random(int(np.prod(conv.in_shape)), 41).reshape(conv.in_shape)
+    f = oracle.fill_random(int(np.prod(conv.filt_shape)), 42).reshape(conv.filt_shape)
+    xb = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    want = oracle.conv2d_naive(conv, xb.float().cpu().numpy(), f)
+    opts = tk.exec_options("bf16", io="bf16")
+    y = torch.full(s.out_shape, float("nan"), device="cuda", dtype=torch.bfloat16)
+    try:
+        tk.conv2d_dev(xb, torch.from_numpy(f).cuda(), y, s, tk.parse_conv_params("im2col"),
+                      options=opts)
+        torch.cuda.synchronize()
+    except tk.CapabilityError:
+        return
+    got = y.float().cpu().numpy()
+    assert not np.isnan(got).any()
+    assert oracle.max_scaled_error(got, want) <= TOL_BF16_IO
