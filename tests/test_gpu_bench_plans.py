@@ -232,13 +232,17 @@ def test_bf16_activations_need_bf16_im2col(tk):  # host-only checks: CPU too
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("io", ["bf16", "in_bf16", "out_bf16"])
 @pytest.mark.parametrize("shape", [(2, 20, 20, 3, 32, 3, 1), (2, 14, 14, 64, 96, 3, 1),
                                    (2, 9, 9, 256, 48, 1, 1), (1, 30, 30, 3, 64, 7, 2),
-                                   (3, 17, 13, 128, 256, 3, 1)])
-def test_bf16_output_ragged_features(tk, oracle, shape):
-    """bf16 output on feature counts whose tiles are not 64-feature
-    multiples: either the exact result (within the BF16 + output-rounding
-    bar) or a CapabilityError -- never unwritten or garbage elements."""
+                                   (3, 17, 13, 128, 256, 3, 1), (2, 11, 11, 12, 64, 1, 1),
+                                   (2, 10, 10, 20, 64, 3, 1), (2, 12, 12, 8, 128, 1, 2),
+                                   (1, 8, 8, 4, 64, 3, 2)])
+def test_bf16_output_ragged_features(tk, oracle, shape, io):
+    """bf16 activations on ragged channel / feature counts (tiles that are
+    not 64-feature multiples, channel rows that are not 16-byte multiples):
+    either the exact result (within the BF16 + output-rounding bar) or a
+    CapabilityError -- never unwritten or garbage elements."""
     import torch
     N, H, C, K, R, st = shape[0], shape[1], shape[3], shape[4], shape[5], shape[6]
     W = shape[2]
@@ -248,10 +252,12 @@ def test_bf16_output_ragged_features(tk, oracle, shape):
     f = oracle.fill_random(int(np.prod(conv.filt_shape)), 42).reshape(conv.filt_shape)
     xb = torch.from_numpy(x).cuda().to(torch.bfloat16)
     want = oracle.conv2d_naive(conv, xb.float().cpu().numpy(), f)
-    opts = tk.exec_options("bf16", io="bf16")
-    y = torch.full(s.out_shape, float("nan"), device="cuda", dtype=torch.bfloat16)
+    opts = tk.exec_options("bf16", io=io)
+    ydt = torch.bfloat16 if io in ("bf16", "out_bf16") else torch.float32
+    y = torch.full(s.out_shape, float("nan"), device="cuda", dtype=ydt)
+    xi = xb if io in ("bf16", "in_bf16") else xb.float()
     try:
-        tk.conv2d_dev(xb, torch.from_numpy(f).cuda(), y, s, tk.parse_conv_params("im2col"),
+        tk.conv2d_dev(xi, torch.from_numpy(f).cuda(), y, s, tk.parse_conv_params("im2col"),
                       options=opts)
         torch.cuda.synchronize()
     except tk.CapabilityError:
