@@ -36,3 +36,23 @@ def test_every_mode_under_device_checks():
     out = r.stdout + r.stderr
     assert r.returncode == 0 and "all ok" in r.stdout, out[-4000:]
     assert "TKB_DCHECK failed" not in out
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(1200)
+@pytest.mark.parametrize("lib", ["release", "checked"])
+def test_forced_stream_k_tail(lib):
+    """The stream-K tail (balanced last wave: partial pieces + ordered
+    reduction) is rarely chosen by the cost model on the bench shapes, so
+    run every kernel mode and every bench layer with it forced
+    (TK_EXPERIMENTS=1 TK_TAIL_FORCE=1): oracle parity per mode, finite
+    outputs per bench layer, and -- with the checked build -- the slot
+    invariants."""
+    env = dict(os.environ, TK_EXPERIMENTS="1", TK_TAIL_FORCE="1")
+    if lib == "checked":
+        assert os.path.exists(CHECKED), "checked build missing: __graft_entry__.build() makes it"
+        env["TK_LIB_PATH"] = CHECKED
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_cases.py"), "--bench"],
+                       env=env, capture_output=True, text=True, timeout=1100, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "all ok" in r.stdout, out[-4000:]
