@@ -32,7 +32,6 @@ const Experiments& experiments() {
     x.tail_force = env_flag("TK_TAIL_FORCE", false);
     x.red_gbs = env_int("TK_RED_GBS", 4000);
     x.pipe_chunks = env_int("TK_PIPE_CHUNKS", 0);
-    x.tail_tma = env_flag("TK_TAIL_TMA", true);
     x.pipe_min_kb = env_int("TK_PIPE_MIN_KB", 0);
     x.tc_stages = env_int("TK_TC_STAGES", 0);
     x.tc_epi = env_int("TK_TC_EPI", 0);

@@ -17,7 +17,6 @@ struct Experiments {
   bool tail = true;             // TK_TAIL=0: no stream-K tail
   bool tail_force = false;      // TK_TAIL_FORCE=1: take the tail wherever it applies
   double red_gbs = 4000.0;      // TK_RED_GBS: reduction-pass rate the split/tail models assume
-  bool tail_tma = true;         // TK_TAIL_TMA=0: column-wise tail pieces for every mode
   int pipe_chunks = 0;          // TK_PIPE_CHUNKS: max batch chunks of the host-buffer pipeline
   int pipe_min_kb = 0;          // TK_PIPE_MIN_KB: smallest chunk copy (KiB)
   int tc_stages = 0;            // TK_TC_STAGES: operand ring depth cap

@@ -206,10 +206,6 @@ struct TcArgs {
   int tail_start, tail_q, tail_kb, tail_P;
   long long tail_W;
   float* tail_part;
-  // tail_tma (plain-family TMA-store modes): pieces leave through the TMA-store
-  // staging as row-major [slot][rank][128][BN] tiles (map_t); tail_reduce_rows
-  // sums them row-wise into the output.  Otherwise the column-wise piece store.
-  int tail_tma;
   // Timeline probe (TK_TC_TRACE=1, experiments only): per CTA, globaltimer
   // stamps of kTraceEvents milestones.
   unsigned long long* trace;
@@ -719,8 +715,7 @@ template <int MODE, int CG, bool TF32, bool OB>
 __global__ void __launch_bounds__(threads_of<MODE>(), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
-                   const __grid_constant__ CUtensorMap map_d,
-                   const __grid_constant__ CUtensorMap map_t, TcArgs p) {
+                   const __grid_constant__ CUtensorMap map_d, TcArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -1150,14 +1145,6 @@ __global__ void __launch_bounds__(threads_of<MODE>(), 1)
       if (local == kTraceUnit && warp == 2 && lane == 0) trace_mark(p, 13);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * p.acc_cols;
 
-      if constexpr (plain_like<MODE>()) {
-        if (u.slot >= 0 && p.tail_tma) {  // fp32 piece through the TMA-store staging
-          tma_store_epilogue<CG, false>(p, taddr, epi_mine, local, warp, lane, row, row,
-                                        empty_base + 8u * acc, &tmem_empty[acc], &map_t, 0,
-                                        (u.slot * CG + (int)rank) * kRows, 0, 0, 3, ering);
-          continue;
-        }
-      }
       if ((plain_like<MODE>() || MODE == kConvPixN) && u.slot >= 0) {
         store_tail_piece(p, taddr, u.slot, rank, CG, row);
         ptx::tc_fence_before();
@@ -1661,80 +1648,6 @@ __global__ void __launch_bounds__(256) tail_reduce_kernel(TcArgs p) {
   }
 }
 
-// Row-major pieces (TcArgs::tail_tma, plain-family modes): block = (tail
-// tile r, CTA rank, kTailRows rows); thread = 4 consecutive columns of one
-// row, every piece's load in flight before the ordered sum (a loop of
-// dependent loads made this pass latency-bound).  The pieces of tile r are
-// slots r*tail_q .. r*tail_q + pieces - 1 (range order); the sum goes to
-// output rows m, columns n (bf16 when OB).
-constexpr int kTailRows = 8;
-constexpr int kTailBatch = 4;  // piece loads in flight per thread
-template <int MODE, int CG, bool OB>
-__global__ void __launch_bounds__(256) tail_reduce_rows_kernel(TcArgs p) {
-  ptx::griddep_wait();
-  ptx::griddep_launch_dependents();
-  constexpr int kGroups = kRows / kTailRows;
-  const int r = blockIdx.x / (CG * kGroups);
-  const int rem = blockIdx.x - r * CG * kGroups;
-  const int rank = rem / kGroups;
-  const int row0 = (rem - rank * kGroups) * kTailRows;
-  __shared__ int s_pieces;
-  __shared__ Unit s_u;
-  if (threadIdx.x == 0) {
-    const long long nk = p.num_kb;
-    s_pieces = tail_owner(p, (r + 1) * nk - 1) - tail_owner(p, r * nk) + 1;
-    s_u = decode_tile(p, p.tail_start + r);
-  }
-  __syncthreads();
-  const int pieces = s_pieces;
-  if (pieces < 2) return;  // stored directly by its only segment
-  const Unit u = s_u;
-  // BN is 64 / 128 / 256 on the TMA-store paths: columns of float4 by shifts
-  const int c4n = p.BN >> 2, c4s = __ffs(c4n) - 1;
-  const long long piece = (long long)CG * kRows * p.BN;  // one slot: CG ranks x 128 rows
-  const float* base = p.tail_part + (long long)r * p.tail_q * piece +
-                      ((long long)rank * kRows + row0) * p.BN;
-  const int m0 = u.m_blk * kRows * CG + rank * kRows + row0;
-  const int n0 = u.n_blk * p.BN;
-  const long long zoff = (long long)u.z * p.d_batch;
-  for (int i = threadIdx.x; i < (kTailRows << c4s); i += blockDim.x) {
-    const int rr = i >> c4s, c = (i & (c4n - 1)) << 2;
-    const float* src = base + (long long)rr * p.BN + c;
-    float4 a = __ldcs(reinterpret_cast<const float4*>(src));
-    for (int q0 = 1; q0 < pieces; q0 += kTailBatch) {
-      float4 b[kTailBatch];
-#pragma unroll
-      for (int q = 0; q < kTailBatch; ++q)
-        if (q0 + q < pieces) b[q] = __ldcs(reinterpret_cast<const float4*>(src + (long long)(q0 + q) * piece));
-#pragma unroll
-      for (int q = 0; q < kTailBatch; ++q) {
-        if (q0 + q < pieces) {
-          a.x += b[q].x;
-          a.y += b[q].y;
-          a.z += b[q].z;
-          a.w += b[q].w;
-        }
-      }
-    }
-    const int m = m0 + rr, n = n0 + c;
-    if (m >= p.M || n >= p.N) continue;
-    const long long off = zoff + (long long)m * p.d_sm + (long long)n * p.d_sn;
-    const float v[4] = {p.alpha * a.x, p.alpha * a.y, p.alpha * a.z, p.alpha * a.w};
-    if constexpr (OB) {
-      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.d) + off;
-      for (int j = 0; j < 4; ++j)
-        if (n + j < p.N) o[(long long)j * p.d_sn] = __float2bfloat16_rn(v[j]);
-    } else {
-      float* o = p.d + off;
-      if (p.d_sn == 1 && n + 3 < p.N && ((reinterpret_cast<uintptr_t>(o) & 15) == 0))
-        *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
-      else
-        for (int j = 0; j < 4; ++j)
-          if (n + j < p.N) o[(long long)j * p.d_sn] = v[j];
-    }
-  }
-}
-
 inline long long total_tiles_of(const TcArgs& p) { return (long long)p.num_m * p.num_n * p.batch; }
 
 // Sustained dense TF32 tensor-core rate per SM and clock the cost models use:
@@ -1915,8 +1828,6 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
                    : 0;
   }
   if (p.tail_q > 1 && (p.splits > 1 || (!plain_like<MODE>() && MODE != kConvPixN))) p.tail_q = 0;
-  p.tail_tma = (p.tail_q > 1 && plain_like<MODE>() && p.store_tma && xp.tail_tma &&
-                (p.BN == 64 || p.BN == 128 || p.BN == 256)) ? 1 : 0;
   p.fd_per = make_fdiv(p.num_m * p.num_n);
   p.fd_span = make_fdiv(p.raster * p.num_n);
   p.fd_raster = make_fdiv(p.raster);
@@ -1953,26 +1864,13 @@ void run_kernel(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     TKB_CUDA(cudaMemset(trace, 0, (size_t)grid * kTraceEvents * 8));
     p.trace = trace;
   }
-  CUtensorMap mt = md;
-  if (p.tail_tma) {
-    const long long rows = (total_tiles_of(p) - p.tail_start) * p.tail_q * CG * kRows;
-    cuuint64_t dims[3] = {(cuuint64_t)p.BN, (cuuint64_t)rows, 1};
-    cuuint64_t strides[2] = {(cuuint64_t)p.BN * 4, (cuuint64_t)(rows * p.BN * 4)};
-    cuuint32_t box[3] = {32, (cuuint32_t)kRows, 1};
-    mt = make_map(p.tail_part, 4, 3, dims, strides, box);
-  }
-  TKB_CUDA(cudaLaunchKernelEx(&cfg, fn, ma, mb, md, mt, p));
+  TKB_CUDA(cudaLaunchKernelEx(&cfg, fn, ma, mb, md, p));
   note_launch();
   if constexpr (plain_like<MODE>() || MODE == kConvPixN) {
     if (p.tail_q > 1) {
       const long long rem = total_tiles_of(p) - p.tail_start;
-      if (p.tail_tma) {
-        const long long blocks = rem * CG * (kRows / kTailRows);
-        launch_pdl(tail_reduce_rows_kernel<MODE, CG, OB>, (unsigned)blocks, 256, st, p);
-      } else {
-        const long long blocks = rem * CG * ((p.BN + 7) / 8);
-        launch_pdl(tail_reduce_kernel<MODE, CG, OB>, (unsigned)blocks, 256, st, p);
-      }
+      const long long blocks = rem * CG * ((p.BN + 7) / 8);
+      launch_pdl(tail_reduce_kernel<MODE, CG, OB>, (unsigned)blocks, 256, st, p);
     }
   }
   if (trace) {
