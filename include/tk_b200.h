@@ -229,6 +229,11 @@ TK_API int tk_gemm_dev(const tk_gemm_shape* shape, const tk_gemm_config* cfg,
 /* gemm with B200 execution options on HOST buffers (precision etc.). */
 TK_API int tk_gemm_ex(const tk_gemm_shape* shape, const tk_exec_options* opts, const float* a,
                       const float* b, const float* c, float* out);
+/* gemm_batched_strided (gemm.hpp:451-479) on device buffers: C_g = A_g B_g,
+ * column-major members at the given element strides, C zeroed (not read).
+ * opts->precision FP32_EXACT: the bit-exact SIMT path; TF32 / BF16: one
+ * batched tensor-core GEMM (A_g packed K-major, B_g read in place when it
+ * can be); 3XTF32: the split-precision GEMM per member. */
 TK_API int tk_gemm_batched_strided_dev(const float* d_a, size_t stride_a,
                                 const float* d_b, size_t stride_b, float* d_c,
                                 size_t stride_c, size_t batch, size_t m,

@@ -536,6 +536,20 @@ def gemm_batched_strided(a, b, batch, m, n, k):
     return c, int(cnt.value)
 
 
+def gemm_batched_strided_dev(a, b, c, batch, m, n, k, precision="fp32", stream=None,
+                             options=None) -> None:
+    """gemm_batched_strided (gemm.hpp:451-479) on device buffers: C_g = A_g B_g
+    over packed column-major members (strides m*k, k*n, m*n).  fp32: the
+    bit-exact SIMT path; tf32 / bf16 / 3xtf32: one batched tensor-core GEMM
+    (3xTF32 member by member)."""
+    opts = options if options is not None else exec_options(precision)
+    _need_dev(a, "gemm_batched_strided: operand A", batch * m * k)
+    _need_dev(b, "gemm_batched_strided: operand B", batch * k * n)
+    _need_dev(c, "gemm_batched_strided: output", batch * m * n)
+    _check(lib().tk_gemm_batched_strided_dev(_dptr(a), m * k, _dptr(b), k * n, _dptr(c), m * n,
+                                             batch, m, n, k, C.byref(opts), _stream(stream)))
+
+
 def conv2d(inp, filt, shape: ConvShape, params: ConvAlgoParams, precision="fp32") -> np.ndarray:
     """conv2d selector (winograd.hpp:304); precision != fp32 uses tensor cores."""
     inp, filt = _f32(inp), _f32(filt)

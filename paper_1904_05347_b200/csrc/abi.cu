@@ -941,10 +941,20 @@ int tk_gemm_batched_strided_dev(const float* d_a, size_t sa, const float* d_b, s
                                 float* d_c, size_t sc, size_t batch, size_t m, size_t n, size_t k,
                                 const tk_exec_options* opts, void* stream) {
   return guarded([&] {
+    KnobScope knobs(opts);
     require_gpu();
-    if (precision_of(opts) != TK_PREC_FP32_EXACT)
-      fail(TK_ERR_CAPABILITY, "gemm_batched_strided: column-major batched GEMM is FP32-exact only");
     if (batch == 0 || m == 0 || n == 0) return;  // nothing to write (reference: 0 multiplies)
+    if (precision_of(opts) != TK_PREC_FP32_EXACT) {  // tensor cores (TF32 / BF16 / 3xTF32)
+      if (tc_knobs().io != 0) fail(TK_ERR_CAPABILITY, "gemm_batched_strided: io flags not supported");
+      if (k == 0) {  // C_g = 0
+        for (size_t g = 0; g < batch; ++g)
+          TKB_CUDA(cudaMemsetAsync(d_c + g * sc, 0, m * n * 4, static_cast<cudaStream_t>(stream)));
+        return;
+      }
+      launch_tc_batched_colmajor(m, n, k, batch, d_a, (long long)sa, d_b, (long long)sb, d_c,
+                                 (long long)sc, precision_of(opts), static_cast<cudaStream_t>(stream));
+      return;
+    }
     if (m > 2147483647ull || n > 2147483647ull || k > 2147483647ull || batch > 65535ull)
       fail(TK_ERR_CAPABILITY, "gemm_batched_strided: dimensions exceed the 32-bit index range");
     ExactArgs p{};

@@ -2690,6 +2690,58 @@ void launch_split3_rows(const float* src, long long rows, long long kp, float* d
   split3_rows(src, rows, kp, dst, pattern, st);
 }
 
+void launch_tc_batched_colmajor(size_t m, size_t n, size_t k, size_t batch, const float* a,
+                                long long sa, const float* b, long long sb, float* d, long long sc,
+                                int precision, cudaStream_t st) {
+  require_tc(precision);
+  if (m > 2147483647ull || n > 2147483647ull || k > 2147483647ull || batch > 2147483647ull)
+    fail(TK_ERR_CAPABILITY, "gemm_batched_strided: dimensions exceed the 32-bit index range");
+  if (precision == TK_PREC_3XTF32) {  // the split-precision path, member by member
+    for (size_t g = 0; g < batch; ++g)
+      launch_tc_colmajor_gemm(m, n, k, 1.0f, 0.0f, false, false, a + g * sa, b + g * sb, nullptr,
+                              d + g * sc, precision, 0, st);
+    return;
+  }
+  const bool tf32 = precision == TK_PREC_TF32;
+  const long long kp = tf32 ? (long long)((k + 3) / 4 * 4) : (long long)((k + 7) / 8 * 8);
+  const size_t esz = tf32 ? 4 : 2;
+  // B_g (k x n column-major) is K-major already: read in place when its rows
+  // and batch stride are 16-byte multiples (TF32).
+  const bool b_ok = tf32 && kp == (long long)k && (reinterpret_cast<uintptr_t>(b) & 15) == 0 &&
+                    (sb * 4) % 16 == 0;
+  Scratch spa(st, kScratchPackA, batch * m * (size_t)kp * esz);
+  Scratch spb(st, kScratchPackB, b_ok ? 0 : batch * n * (size_t)kp * esz);
+  char* pa = static_cast<char*>(spa.get());
+  char* pb = static_cast<char*>(spb.get());
+  for (size_t g = 0; g < batch; ++g) {
+    const float* ag = a + g * sa;
+    void* dst = pa + g * m * (size_t)kp * esz;  // A_g^T: rows m, K contiguous
+    if (tf32) pack_kmajor<float>(ag, 1, (long long)m, (long long)m, (long long)k, kp, (float*)dst, false, st);
+    else pack_kmajor<__nv_bfloat16>(ag, 1, (long long)m, (long long)m, (long long)k, kp, (__nv_bfloat16*)dst, false, st);
+    if (!b_ok) {
+      const float* bg = b + g * sb;
+      void* bd = pb + g * n * (size_t)kp * esz;
+      if (tf32) pack_kmajor<float>(bg, (long long)k, 1, (long long)n, (long long)k, kp, (float*)bd, false, st);
+      else pack_kmajor<__nv_bfloat16>(bg, (long long)k, 1, (long long)n, (long long)k, kp, (__nv_bfloat16*)bd, false, st);
+    }
+  }
+  TcGemm t;
+  t.M = (int)m;
+  t.N = (int)n;
+  t.K = (int)kp;
+  t.batch = (int)batch;
+  t.a = reinterpret_cast<const float*>(pa);
+  t.a_batch = (long long)m * kp;
+  t.b = b_ok ? b : reinterpret_cast<const float*>(pb);
+  t.b_batch = b_ok ? sb : (long long)n * kp;
+  t.d = d;
+  t.d_sm = 1;
+  t.d_sn = (long long)m;
+  t.d_batch = sc;
+  t.precision = precision;
+  launch_tc_gemm(t, st);
+}
+
 void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float beta, bool ta,
                              bool tb, const float* a, const float* b, const float* c, float* d,
                              int precision, int tile_n, cudaStream_t st) {

@@ -58,6 +58,14 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
                              bool tb, const float* a, const float* b, const float* c, float* d,
                              int precision, int tile_n, cudaStream_t st);
 
+// Batched column-major C_g = A_g B_g (C zeroed: beta 0), g < batch, operand
+// strides in elements (the reference gemm_batched_strided, gemm.hpp:451-479)
+// on tensor cores: A_g packed K-major for all g, B_g read in place when it
+// already is (TF32, k % 4 == 0), one batched launch; 3xTF32 per member.
+void launch_tc_batched_colmajor(size_t m, size_t n, size_t k, size_t batch, const float* a,
+                                long long sa, const float* b, long long sb, float* d, long long sc,
+                                int precision, cudaStream_t st);
+
 // Implicit-GEMM convolution on tensor cores (NHWC in, HWCK filter, NHWC
 // out).  Workspace: packed filter (+ patch matrix on the fallback path).
 size_t tc_conv_workspace(const ConvGeom& g, int precision);

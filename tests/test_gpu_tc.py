@@ -362,3 +362,29 @@ def test_tc_conv_narrow_pixels(tk, oracle, shape, prec, mode):
     assert not np.isnan(got).any(), plan
     err = oracle.max_scaled_error(got, want)
     assert err <= TOL[plan["precision"]], (err, plan)
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16", "3xtf32"])
+@pytest.mark.parametrize("batch,m,n,k", [(16, 1568, 128, 64), (36, 200, 96, 33), (1, 256, 256, 256),
+                                         (5, 77, 130, 8), (3, 64, 64, 0)])
+def test_tc_gemm_batched_strided(tk, oracle, batch, m, n, k, prec):
+    """gemm_batched_strided (gemm.hpp:451-479) on tensor cores: every member
+    C_g = A_g B_g within the precision's bar against the oracle's GEMM;
+    k = 0 gives zeros (C is not read)."""
+    import torch
+    a = oracle.fill_random(batch * m * k, 9) if k else np.zeros(0, np.float32)
+    b = oracle.fill_random(batch * k * n, 10) if k else np.zeros(0, np.float32)
+    out = torch.full((batch * m * n,), float("nan"), device="cuda")
+    tk.gemm_batched_strided_dev(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), out,
+                                batch, m, n, k, precision=prec)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    tol = {"tf32": TOL_TF32, "bf16": TOL_BF16, "3xtf32": 5e-5}[prec]
+    for g in range(batch):
+        cg = got[g * m * n:(g + 1) * m * n]
+        if k == 0:
+            assert np.all(cg == 0)
+            continue
+        want = oracle.gemm_naive(m, n, k, 1.0, 0.0, 0, 0, a[g * m * k:(g + 1) * m * k],
+                                 b[g * k * n:(g + 1) * k * n], np.zeros(m * n, np.float32))
+        assert oracle.max_scaled_error(cg, want) <= tol, (g, prec)
