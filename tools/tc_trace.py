@@ -1,7 +1,7 @@
 """Timeline of one tensor-core launch (TK_TC_TRACE): per-CTA globaltimer
 stamps of setup, first/last slab arrival, accumulator hand-off, epilogue
 drain / store issue, and exit.
-    python tools/tc_trace.py gemm M,N,K [tf32|bf16] [tile_n]
+    python tools/tc_trace.py gemm M,N,K [tf32|bf16] [tile_n] [split]
     python tools/tc_trace.py conv N,H,C,K,R[,stride] [tf32|bf16]"""
 import os
 import sys
@@ -21,13 +21,15 @@ prec = sys.argv[3] if len(sys.argv) > 3 else "tf32"
 if kind == "gemm":
     m, n, k = dims
     tn = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    sp = int(sys.argv[5]) if len(sys.argv) > 5 else 0
     a = torch.rand(m * k, device="cuda") - 0.5
     b = torch.rand(k * n, device="cuda") - 0.5
     c = torch.empty(m * n, device="cuda")
     shape = tk.GemmShape(m, n, k, 1.0, 0.0, "t", "n")
 
     def run():
-        tk.gemm_dev(a, b, None, c, shape, None, precision=prec, tile_n=tn)
+        tk.gemm_dev(a, b, None, c, shape, None,
+                    options=tk.exec_options(prec, tile_n=tn, split=sp))
 else:
     N, H, C, K, R = dims[:5]
     S = dims[5] if len(dims) > 5 else 1
