@@ -2,7 +2,7 @@
 once outside the timing, the run phase replayed from a CUDA graph, L2
 flushed before every replay), for the VGG-16 and ResNet-50 layer tables.
 
-    python tools/layer_times.py [vgg16|resnet50|all] [tf32|bf16] [batch] [--only NAME]
+    python tools/layer_times.py [vgg16|resnet50|all] [tf32|bf16] [batch] [--only NAME] [--io bf16]
 """
 import argparse
 import os
@@ -24,6 +24,8 @@ ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--mode", default="auto", help="tensor-core operand path (tk.TC_MODES)")
 ap.add_argument("--split", type=int, default=0)
 ap.add_argument("--algo", default="im2col", help="conv algorithm (parse_conv_params grammar)")
+ap.add_argument("--io", default="fp32", help="activation format: fp32 | bf16 | in_bf16 | out_bf16 "
+                                            "(bf16 needs the bf16 precision)")
 ap.add_argument("--flush", default="read", choices=["read", "write"],
                 help="evict L2 by reading (clean lines) or writing (dirty lines whose "
                      "write-back then lands on the timed kernel) a 256 MiB buffer")
@@ -48,7 +50,11 @@ for name, r, s, h, c, k in rows:
     x = torch.rand(shp.in_shape, device="cuda") * 2 - 1
     f = torch.rand(shp.filt_shape, device="cuda") * 2 - 1
     y = torch.empty(shp.out_shape, device="cuda")
-    opts = tk.exec_options(a.prec, mode=a.mode, split=a.split)
+    if a.io in ("bf16", "in_bf16"):
+        x = x.to(torch.bfloat16)
+    if a.io in ("bf16", "out_bf16"):
+        y = y.to(torch.bfloat16)
+    opts = tk.exec_options(a.prec, mode=a.mode, split=a.split, io=a.io)
     try:
         ws = torch.empty(max(tk.conv2d_workspace_size(shp, p, options=opts), 4) // 4 + 1,
                          device="cuda")
