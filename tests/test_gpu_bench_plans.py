@@ -137,6 +137,40 @@ def test_bench_layer_batch32(tk, oracle, idx, prec, knob_source):
         assert torch.equal(y.view(torch.int32), y2.view(torch.int32)), (name, plan)
 
 
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+@pytest.mark.parametrize("vi", range(len(VGG16)), ids=[v[0] for v in VGG16])
+def test_vgg_batch1_plans(tk, oracle, vi, prec, knob_source):
+    """BASELINE configs[1] at batch 1 (bench.py's vgg16_batch1 leg): the
+    rules' plans and the tuning DB's batch-1 records (halo for conv3_x,
+    im2col with K split 8 for conv5, ...) against the oracle."""
+    import torch
+    name, h, c, k, _ = VGG16[vi]
+    shape = tk.ConvShape(1, h, h, c, k, 3, 3, 1, True)
+    algo = tk.parse_conv_params("im2col")
+    plan = tk.conv2d_plan_info(shape, algo, prec)
+    if knob_source == "tuned" and not plan["tuned"]:
+        pytest.skip("the DB keeps the rules' plan for this shape")
+    gen = torch.Generator(device="cuda").manual_seed(2000 + vi)
+    x = torch.rand((1, h, h, c), device="cuda", generator=gen) * 2 - 1
+    f = torch.rand((3, 3, c, k), device="cuda", generator=gen) * 2 - 1
+    ws = torch.empty(max(tk.conv2d_workspace_size(shape, algo, prec), 4) // 4 + 1, device="cuda")
+    ys = []
+    for _ in range(2):
+        y = torch.full(shape.out_shape, float("nan"), device="cuda")
+        tk.conv2d_prepare_dev(f, shape, algo, ws, precision=prec)
+        tk.conv2d_run_dev(x, f, y, shape, algo, ws, precision=prec)
+        torch.cuda.synchronize()
+        ys.append(y)
+    want = oracle.conv2d_naive(oracle.Conv(1, h, h, c, k, 3, 3, 1, True), x.cpu().numpy(),
+                               f.cpu().numpy())
+    bar = TOL[plan["precision"]] if plan["precision"] in TOL else TOL[prec]
+    err = oracle.max_scaled_error(ys[0].cpu().numpy(), want)
+    assert err <= bar, (name, prec, err, plan)
+    assert torch.equal(ys[0].view(torch.int32), ys[1].view(torch.int32)), (name, plan)
+
+
 def torch_isnan_any(y):
     import torch
     return torch.isnan(y).any().item()

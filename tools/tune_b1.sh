@@ -1,0 +1,7 @@
+# configs[1] batch 1: profile pass (plain, then under ncu: one tool per call)
+A="--batch 1 --which vgg16 --splits 4,8,16"
+python tools/tune_ncu.py --profile-pass $A --out gpurun_out/tune_b1_launches.json > gpurun_out/tune_b1_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,dram__throughput.avg.pct_of_peak_sustained_elapsed \
+    -k 'regex:tc_gemm|exact_gemm|tail_reduce|splitk_reduce|pack_filter|to_bf16|pointwise_gather|split3|pad_phase' --csv --log-file gpurun_out/tune_b1_ncu.csv \
+    python tools/tune_ncu.py --profile-pass $A --out gpurun_out/tune_b1_launches.json > gpurun_out/tune_b1_ncu.log 2>&1
+echo DONE $?

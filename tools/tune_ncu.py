@@ -45,10 +45,11 @@ sys.path.insert(0, ROOT)
 
 from bench import RESNET50, VGG16  # noqa: E402
 
-N = 32
+N = 32  # batch (--batch)
 LAYERS = [(name, 3, 1, h, c, k) for name, h, c, k, _ in VGG16] + \
          [(name, r, s, h, c, k) for name, r, s, h, c, k, _ in RESNET50]
 PRECISIONS = ("tf32", "bf16")
+EXTRA_SPLITS = ()  # --splits: forced K-split counts added to every mode (small batches)
 KNOBS = [  # (mode, cluster, split)
     ("auto", 0, 0), ("auto", 0, 1), ("halo", 0, 0), ("pixn", 0, 0), ("pixn", 1, 0),
     ("pixn", 2, 0), ("pixn", 0, 1), ("pixm", 0, 0), ("pointwise", 0, 0), ("pointwise", 0, 1),
@@ -69,6 +70,8 @@ def config_name(prec, mode, cluster, split):
     s += SUFFIX_MODE[mode]
     if split == 1:
         s += "_nosplit"
+    elif split > 1:
+        s += f"_k{split}"
     return s
 
 
@@ -81,7 +84,9 @@ def candidates(tk):
         shape = tk.ConvShape(N, h, h, c, k, r, r, s, True)
         for prec in PRECISIONS:
             seen = {}
-            for mode, cl, sp in KNOBS:
+            knobs = list(KNOBS) + [(m, 0, sp) for m in ("auto", "halo", "pixn", "im2col")
+                                   for sp in EXTRA_SPLITS]
+            for mode, cl, sp in knobs:
                 opts = tk.exec_options(prec, cluster=cl, mode=mode, split=sp)
                 try:
                     plan = tk.conv2d_plan_info(shape, im, options=opts)
@@ -306,7 +311,17 @@ def main():
     ap.add_argument("--curate", metavar="ALL_NDJSON")
     ap.add_argument("--out", default="runs/tune_launches.json")
     ap.add_argument("--db", default="profiles/r02_tune_ncu.ndjson")
+    ap.add_argument("--batch", type=int, default=32, help="images per layer (bench: 32; configs[1]: 1)")
+    ap.add_argument("--which", default="all", choices=["all", "vgg16", "resnet50"])
+    ap.add_argument("--splits", default="", help="extra forced K splits, e.g. 4,8,16")
     args = ap.parse_args()
+    global N, LAYERS, EXTRA_SPLITS
+    N = args.batch
+    if args.which == "vgg16":
+        LAYERS = LAYERS[:len(VGG16)]
+    elif args.which == "resnet50":
+        LAYERS = LAYERS[len(VGG16):]
+    EXTRA_SPLITS = tuple(int(v) for v in args.splits.split(",") if v)
     if args.profile_pass:
         profile_pass(args.out)
     elif args.shortlist:
