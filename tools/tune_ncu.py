@@ -50,6 +50,7 @@ LAYERS = [(name, 3, 1, h, c, k) for name, h, c, k, _ in VGG16] + \
          [(name, r, s, h, c, k) for name, r, s, h, c, k, _ in RESNET50]
 PRECISIONS = ("tf32", "bf16")
 EXTRA_SPLITS = ()  # --splits: forced K-split counts added to every mode (small batches)
+SPLITS_ONLY = False  # --splits-only: the rules against the split candidates only
 KNOBS = [  # (mode, cluster, split)
     ("auto", 0, 0), ("auto", 0, 1), ("halo", 0, 0), ("pixn", 0, 0), ("pixn", 1, 0),
     ("pixn", 2, 0), ("pixn", 0, 1), ("pixm", 0, 0), ("pointwise", 0, 0), ("pointwise", 0, 1),
@@ -84,8 +85,8 @@ def candidates(tk):
         shape = tk.ConvShape(N, h, h, c, k, r, r, s, True)
         for prec in PRECISIONS:
             seen = {}
-            knobs = list(KNOBS) + [(m, 0, sp) for m in ("auto", "halo", "pixn", "im2col")
-                                   for sp in EXTRA_SPLITS]
+            knobs = ([("auto", 0, 0)] if SPLITS_ONLY else list(KNOBS)) + \
+                [(m, 0, sp) for m in ("auto", "halo", "pixn", "im2col") for sp in EXTRA_SPLITS]
             for mode, cl, sp in knobs:
                 opts = tk.exec_options(prec, cluster=cl, mode=mode, split=sp)
                 try:
@@ -314,8 +315,11 @@ def main():
     ap.add_argument("--batch", type=int, default=32, help="images per layer (bench: 32; configs[1]: 1)")
     ap.add_argument("--which", default="all", choices=["all", "vgg16", "resnet50"])
     ap.add_argument("--splits", default="", help="extra forced K splits, e.g. 4,8,16")
+    ap.add_argument("--splits-only", action="store_true",
+                    help="candidates = the rules + the --splits variants only")
     args = ap.parse_args()
-    global N, LAYERS, EXTRA_SPLITS
+    global N, LAYERS, EXTRA_SPLITS, SPLITS_ONLY
+    SPLITS_ONLY = args.splits_only
     N = args.batch
     if args.which == "vgg16":
         LAYERS = LAYERS[:len(VGG16)]
