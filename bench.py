@@ -128,8 +128,11 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch layer by layer")
-    ap.add_argument("--tuning-db", default=os.path.join(ROOT, "profiles", "r02_tune_ncu.ndjson"),
-                    help="NDJSON tuning DB loaded into the library (tools/tune_ncu.py); "
+    ap.add_argument("--tuning-db", default=",".join(
+                        os.path.join(ROOT, "profiles", f) for f in ("r02_tune_ncu.ndjson",
+                                                                    "r02_tune_gemm.ndjson")),
+                    help="comma-separated NDJSON tuning DBs loaded into the library "
+                         "(tools/tune_ncu.py conv plans, tools/tune_gemm.py GEMM tiles); "
                          "'none' = the built-in rules only")
     ap.add_argument("--no-multi", action="store_true",
                     help="skip the multi-GPU verification gather and the GEMM column-panel leg "
@@ -348,8 +351,10 @@ def main():
     # The tuner's DB (lookup_best on the launch path): calls with automatic
     # knobs take the fastest recorded knobs of their shape.
     db_records = 0
-    if args.tuning_db != "none" and os.path.exists(args.tuning_db):
-        db_records = tk.tuning_db_load(args.tuning_db)
+    db_paths = [] if args.tuning_db == "none" else \
+        [p_ for p_ in args.tuning_db.split(",") if p_ and os.path.exists(p_)]
+    for p_ in db_paths:
+        db_records += tk.tuning_db_load(p_)
 
     # Resident inputs: one independent seeded input + filter per layer
     # instance (the reference `layers` harness, tilekit_cli.cpp:374-403).
@@ -1097,7 +1102,7 @@ def main():
                        "algorithm": "im2col implicit GEMM",
                        "precision": prec, "step_gflop": round(step_flops / 1e9, 2),
                        "l2": "flushed between steps (256 MiB write, outside events)",
-                       "tuning_db": (os.path.relpath(args.tuning_db, ROOT) if db_records else None),
+                       "tuning_db": ([os.path.relpath(p_, ROOT) for p_ in db_paths] if db_records else None),
                        "tuning_db_entries": db_records},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches),

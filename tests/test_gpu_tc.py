@@ -388,3 +388,52 @@ def test_tc_gemm_batched_strided(tk, oracle, batch, m, n, k, prec):
         want = oracle.gemm_naive(m, n, k, 1.0, 0.0, 0, 0, a[g * m * k:(g + 1) * m * k],
                                  b[g * k * n:(g + 1) * k * n], np.zeros(m * n, np.float32))
         assert oracle.max_scaled_error(cg, want) <= tol, (g, prec)
+
+
+def _tuned_gemm_cases():
+    import json
+    import os
+    import re
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                        "r02_tune_gemm.ndjson")
+    if not os.path.exists(path):
+        return []
+    out = []
+    for line in open(path):
+        r = json.loads(line)
+        if r["config"].endswith(("@tf32", "@bf16")):
+            continue  # the rules' own record
+        m, n, k = (int(v) for v in re.match(r"gemm_nn_m(\d+)_n(\d+)_k(\d+)", r["problem"]).groups())
+        if m * n * k <= 1 << 28:  # the oracle's naive GEMM stays quick
+            out.append((m, n, k, r["precision"], r["config"]))
+    return out[::4]  # a quarter of the tuned shapes, every tile / split kind among them
+
+
+@pytest.mark.parametrize("m,n,k,prec,config", _tuned_gemm_cases())
+def test_tc_gemm_tuned_db(tk, oracle, m, n, k, prec, config):
+    """GEMMs whose tile / cluster / K split comes from the per-shape tuning DB
+    (profiles/r02_tune_gemm.ndjson, tools/tune_gemm.py) on the launch path:
+    within the bar and bitwise repeatable."""
+    import os
+    import torch
+    db = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                      "r02_tune_gemm.ndjson")
+    tk.tuning_db_clear()
+    tk.tuning_db_load(db)
+    try:
+        a = oracle.fill_random(m * k, 21)
+        b = oracle.fill_random(k * n, 22)
+        want = oracle.gemm_naive(m, n, k, 1.0, 0.0, 0, 0, a, b, np.zeros(m * n, np.float32))
+        da, db_ = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        shape = tk.GemmShape(m, n, k)
+        outs = []
+        for _ in range(2):
+            out = torch.full((m * n,), float("nan"), device="cuda")
+            tk.gemm_dev(da, db_, None, out, shape, precision=prec)
+            torch.cuda.synchronize()
+            outs.append(out)
+        err = oracle.max_scaled_error(outs[0].cpu().numpy(), want)
+        assert err <= TOL[prec], (config, err)
+        assert torch.equal(outs[0].view(torch.int32), outs[1].view(torch.int32)), config
+    finally:
+        tk.tuning_db_clear()

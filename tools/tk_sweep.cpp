@@ -4,7 +4,15 @@
 // batch 32 (data/*.csv), each at one precision, written as the reference's
 // CSV report (`reference roofline` workflow, tilekit_cli.cpp:305-345).
 //
-//   tk_sweep fp32|tf32|bf16 <out.csv> [grid|squares|layers|all]
+//   tk_sweep fp32|tf32|bf16 <out.csv> [grid|squares|layers|all] [db.ndjson[,db2...]]
+//
+// With tuning DBs (tools/tune_gemm.py, tools/tune_ncu.py) loaded, every
+// tensor-core point runs its per-shape tuned knobs (tk_tuning_db_load:
+// lookup_best on the launch path) -- configs[3]'s "per-shape tuned tile
+// parameters".
+//
+// Build: g++ -std=c++20 -O2 -I include tools/tk_sweep.cpp -o tools/tk_sweep
+//        -L paper_1904_05347_b200 -ltilekit_b200 -Wl,-rpath,$PWD/paper_1904_05347_b200
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -15,10 +23,24 @@ using namespace tilekit;
 
 int main(int argc, char** argv) {
   if (argc < 3) {
-    std::fprintf(stderr, "usage: tk_sweep fp32|tf32|bf16 out.csv [grid|squares|layers|all]\n");
+    std::fprintf(stderr, "usage: tk_sweep fp32|tf32|bf16 out.csv [grid|squares|layers|all] [db.ndjson,...]\n");
     return 2;
   }
   const std::string prec = argv[1], out = argv[2], which = argc > 3 ? argv[3] : "all";
+  if (argc > 4) {
+    std::string dbs = argv[4];
+    for (std::size_t p = 0; p <= dbs.size();) {
+      const std::size_t e = std::min(dbs.find(',', p), dbs.size());
+      const std::string path = dbs.substr(p, e - p);
+      std::size_t n = 0;
+      if (!path.empty() && tk_tuning_db_load(path.c_str(), nullptr, &n) != TK_OK) {
+        std::fprintf(stderr, "tuning DB %s: %s\n", path.c_str(), tk_last_error());
+        return 2;
+      }
+      std::printf("tuning DB %s: %zu records\n", path.c_str(), n);
+      p = e + 1;
+    }
+  }
   const DeviceSpec dev = b200_device();
   BenchOptions opts;
   opts.warmup = 3;
