@@ -98,6 +98,22 @@ def plan_str(tk, shape, algo, prec):
     return s
 
 
+def gemm_plan_str(tk, shape, options):
+    """Compact tk_gemm_plan_info (e.g. "tc_plain/tf32 cg2 256x64 A,B in place")."""
+    d = tk.gemm_plan_info(shape, options=options)
+    s = f"{d['kernel']}/{d['precision']} cg{d['cta_group']} {d['tile_m']}x{d['tile_n']}"
+    if d["splits"] > 1:
+        s += f" split{d['splits']}"
+    if d["tail_pieces"]:
+        s += f" tail{d['tail_pieces']}"
+    placed = [n for n, f in (("A", d["a_in_place"]), ("B", d["b_in_place"])) if f]
+    if d["kernel"] != "exact_simt":
+        s += f" {','.join(placed)} in place" if placed else " packed"
+    if d.get("tuned"):
+        s += " [db]"
+    return s
+
+
 def bound_frac(flops, nbytes, ms, peak_tf, hbm_gbs):
     """Roofline verdict of one layer: HBM-bound when its operational
     intensity (conv_flops / compulsory fp32 bytes) is under the ridge
@@ -1025,7 +1041,8 @@ def main():
                 pk = peaks["bf16_tflops"] / {"tf32": 2.0, "bf16": 1.0, "bf16_io": 1.0, "3xtf32": 6.0}[p_]
                 secondary[f"gemm{n}_{p_}"] = {"value": round(tf * 1e3, 1), "unit": "GFLOP/s",
                                               "ms": round(ms, 4), "frac_of_peak": round(tf / pk, 4),
-                                              "api_ms": round(api_ms, 4)}
+                                              "api_ms": round(api_ms, 4),
+                                              "plan": gemm_plan_str(tk, gshape, o_)}
                 if io_:
                     secondary[f"gemm{n}_{p_}"]["operands"] = "bf16 in HBM (A MN-major and B K-major, read in place)"
                 del ga_, gb_
@@ -1074,6 +1091,7 @@ def main():
                 "ms": round(dms, 4), "frac_of_peak": round(2 * n ** 3 / (dms * 1e-3) / 1e12 / pk, 4),
                 "api_ms": round(ms, 4),
                 "api_gflops": round(2 * n ** 3 / (ms * 1e-3) / 1e9, 1),
+                "plan": gemm_plan_str(tk, gshape, tk.exec_options(p_)),
                 "note": "value/ms: device time (graph of 20 calls, median of 5 replays); api_*: one tk_gemm_dev call "
                         "between events (host work included); L2-resident operands (12.6 MB); "
                         "fp32 peak = FMUL+FADD issue cap 37.2 TF/s"}

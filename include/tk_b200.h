@@ -183,6 +183,24 @@ typedef struct tk_conv_plan_info {
   int reserved[3];
 } tk_conv_plan_info;
 
+/* The plan of one GEMM call (tk_gemm_plan_info): what tk_gemm_dev will run
+ * for this shape, config and options (operands assumed 16-byte aligned). */
+typedef struct tk_gemm_plan {
+  int kernel;              /* TK_KERNEL_EXACT, or TK_KERNEL_TC_IM2COL's neighbour
+                              TK_KERNEL_TC_PLAIN (9): the tensor-core GEMM      */
+  int precision;           /* effective enum tk_precision                    */
+  int requested_precision; /* tk_exec_options.precision of the call          */
+  int cta_group;           /* SMs per tensor-core tile (1 or 2); 1 for SIMT  */
+  int tile_m, tile_n;      /* MMA tile (TC) or CTA output tile (SIMT)        */
+  int splits;              /* split-K partial sums (1 = none)                */
+  int tail_pieces;         /* stream-K tail: max pieces per tile (0 = none)  */
+  int a_in_place, b_in_place; /* operand read where it lies (no pack pass)   */
+  int k_depth;             /* contraction depth of the MMAs (3 kp: 3xTF32)   */
+  int tuned;               /* 1: knobs from the loaded tuning DB             */
+  int reserved[4];
+} tk_gemm_plan;
+#define TK_KERNEL_TC_PLAIN 9
+
 /* ---- library --------------------------------------------------------- */
 TK_API const char* tk_last_error(void);
 TK_API int tk_abi_version(void);
@@ -223,6 +241,12 @@ TK_API int tk_gemm_batched_strided(const float* a, size_t stride_a, const float*
                             uint64_t* multiplies);
 /* Device-buffer GEMM.  cfg may be NULL (library choice); opts may be NULL
  * (exact FP32).  Tensor-core precisions ignore cfg. */
+/* What tk_gemm_dev would run for (shape, cfg, opts): kernel family,
+ * effective precision, CTA group, tile, split-K, stream-K tail, which
+ * operands are read in place, whether a tuning-DB record chose the knobs.
+ * Nothing is launched or allocated. */
+TK_API int tk_gemm_plan_info(const tk_gemm_shape* shape, const tk_gemm_config* cfg,
+                             const tk_exec_options* opts, tk_gemm_plan* out);
 TK_API int tk_gemm_dev(const tk_gemm_shape* shape, const tk_gemm_config* cfg,
                 const tk_exec_options* opts, const float* d_a, const float* d_b,
                 const float* d_c, float* d_out, void* stream);

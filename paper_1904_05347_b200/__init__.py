@@ -121,8 +121,15 @@ class ConvPlanInfoC(C.Structure):
         [("reserved", C.c_int * 3)]
 
 
+class GemmPlanC(C.Structure):
+    _fields_ = [(n, C.c_int) for n in (
+        "kernel", "precision", "requested_precision", "cta_group", "tile_m", "tile_n", "splits",
+        "tail_pieces", "a_in_place", "b_in_place", "k_depth", "tuned")] + \
+        [("reserved", C.c_int * 4)]
+
+
 KERNELS = {0: "exact_simt", 1: "tc_halo", 2: "tc_pixn", 3: "tc_pixm", 4: "tc_gather",
-           5: "tc_pointwise", 6: "tc_im2col", 7: "winograd", 8: "tc_halo_narrow"}
+           5: "tc_pointwise", 6: "tc_im2col", 7: "winograd", 8: "tc_halo_narrow", 9: "tc_plain"}
 PRECISION_NAMES = {v: k for k, v in PRECISIONS.items()}
 
 
@@ -136,7 +143,7 @@ EXPORTS = [
     "tk_conv2d_dev", "tk_conv2d_workspace_size", "tk_conv2d_ex", "tk_im2col_dev",
     "tk_bench_gemm", "tk_bench_conv2d", "tk_gemm_ex", "tk_conv2d_prepare_dev",
     "tk_conv2d_run_dev", "tk_conv2d_plan_info", "tk_tuning_db_load", "tk_tuning_db_clear",
-    "tk_tuning_db_size",
+    "tk_tuning_db_size", "tk_gemm_plan_info",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -196,6 +203,8 @@ def lib() -> C.CDLL:
         "tk_conv2d_plan_info": [C.POINTER(ConvShapeC), C.POINTER(ConvParamsC),
                                 C.POINTER(ExecOptionsC), C.POINTER(ConvPlanInfoC)],
         "tk_tuning_db_load": [C.c_char_p, C.c_char_p, C.POINTER(C.c_size_t)],
+        "tk_gemm_plan_info": [C.POINTER(GemmShapeC), C.POINTER(GemmConfigC),
+                              C.POINTER(ExecOptionsC), C.POINTER(GemmPlanC)],
         "tk_tuning_db_clear": [],
         "tk_tuning_db_size": [C.POINTER(C.c_size_t)],
         "tk_gemm_ex": [C.POINTER(GemmShapeC), C.POINTER(ExecOptionsC), _vp, _vp, _vp, _vp],
@@ -681,6 +690,23 @@ def conv2d_plan_info(shape: ConvShape, params: ConvAlgoParams, precision="fp32",
     _check(lib().tk_conv2d_plan_info(C.byref(shape.c()), C.byref(params.c()), C.byref(opts),
                                      C.byref(info)))
     d = {f: getattr(info, f) for f, _ in ConvPlanInfoC._fields_ if f != "reserved"}
+    d["kernel"] = KERNELS[d["kernel"]]
+    d["precision"] = PRECISION_NAMES[d["precision"]]
+    d["requested_precision"] = PRECISION_NAMES[d["requested_precision"]]
+    return d
+
+
+def gemm_plan_info(shape: GemmShape, cfg: Optional[GemmConfig] = None, precision="fp32",
+                   options=None) -> dict:
+    """The plan gemm_dev runs for this call (tk_gemm_plan_info): kernel
+    family, effective precision, CTA group, tile, split-K / stream-K tail,
+    which operands are read in place, whether the tuning DB chose the knobs.
+    Host-side only (operands assumed 16-byte aligned)."""
+    info = GemmPlanC()
+    opts = options if options is not None else exec_options(precision)
+    _check(lib().tk_gemm_plan_info(C.byref(shape.c()), C.byref(cfg.c()) if cfg is not None else None,
+                                   C.byref(opts), C.byref(info)))
+    d = {f: getattr(info, f) for f, _ in GemmPlanC._fields_ if f != "reserved"}
     d["kernel"] = KERNELS[d["kernel"]]
     d["precision"] = PRECISION_NAMES[d["precision"]]
     d["requested_precision"] = PRECISION_NAMES[d["requested_precision"]]

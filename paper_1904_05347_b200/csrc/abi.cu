@@ -264,12 +264,15 @@ bool apply_tuned_conv(const tilekit::ConvShape& s, const tk_conv_params* p,
 }
 
 // GEMM: the N tile travels as an argument, the rest through tc_knobs.
-int tuned_gemm_tile(const tilekit::GemmShape& g, const tk_exec_options* o) {
+int tuned_gemm_tile(const tilekit::GemmShape& g, const tk_exec_options* o, bool* hit = nullptr) {
   const int prec = o ? o->precision : TK_PREC_FP32_EXACT;
+  if (hit) *hit = false;
   if (prec == TK_PREC_FP32_EXACT) return 0;
   if (!all_auto(o)) return o->tc_tile_n;
   TunedKnobs k;
   if (!tuning_db_lookup(g.key(), "gemm", prec, &k)) return 0;
+  if (!k.tile_n && !k.stages && !k.cluster && !k.split) return 0;  // the DB keeps the rules
+  if (hit) *hit = true;
   TcKnobs& t = tc_knobs();
   t.stages = k.stages;
   t.cluster = k.cluster;
@@ -839,6 +842,48 @@ int tk_gemm_naive(const tk_gemm_shape* shape, const float* a, const float* b, co
                  st);
     d2h(out, dd.p, 4 * nc, st);
     finish(st);
+  });
+}
+
+int tk_gemm_plan_info(const tk_gemm_shape* shape, const tk_gemm_config* cfg,
+                      const tk_exec_options* opts, tk_gemm_plan* out) {
+  return guarded([&] {
+    if (!out) fail(TK_ERR_CONTRACT, "gemm_plan_info: out must not be NULL");
+    KnobScope knobs(opts);
+    const tilekit::GemmShape g = gemm_shape(shape);
+    const int prec = precision_of(opts);
+    std::memset(out, 0, sizeof(*out));
+    out->requested_precision = prec;
+    out->splits = 1;
+    out->cta_group = 1;
+    if (prec == TK_PREC_FP32_EXACT) {
+      const ExactLaunch L = cfg ? exact_launch_of(gemm_config(cfg)) : exact_auto((long long)g.m, (long long)g.n);
+      out->kernel = TK_KERNEL_EXACT;
+      out->precision = TK_PREC_FP32_EXACT;
+      out->tile_m = L.h * L.r;
+      out->tile_n = L.w * L.c;
+      out->a_in_place = out->b_in_place = 1;
+      out->k_depth = (int)g.k;
+      return;
+    }
+    bool hit = false;
+    const int tile = tuned_gemm_tile(g, opts, &hit);
+    TcGemmPlan pl;
+    launch_tc_colmajor_gemm(g.m, g.n, g.k, g.alpha, g.beta, g.op_a == tilekit::Op::Transpose,
+                            g.op_b == tilekit::Op::Transpose, nullptr, nullptr,
+                            g.beta != 0.0f ? reinterpret_cast<const float*>(16) : nullptr, nullptr,
+                            prec, tile, nullptr, &pl);
+    out->kernel = TK_KERNEL_TC_PLAIN;
+    out->precision = prec;
+    out->cta_group = pl.cta_group;
+    out->tile_m = pl.tile_m;
+    out->tile_n = pl.tile_n;
+    out->splits = pl.splits;
+    out->tail_pieces = pl.tail_pieces;
+    out->a_in_place = pl.a_in_place;
+    out->b_in_place = pl.b_in_place;
+    out->k_depth = pl.k_depth;
+    out->tuned = hit ? 1 : 0;
   });
 }
 

@@ -2606,6 +2606,28 @@ void launch_tc_gemm(const TcGemm& g, cudaStream_t st) {
   const int step = 16 * cg;
   bn = (bn + step - 1) / step * step;
   if (bn < step) bn = step;
+  if (g.plan) {  // dry run (tk_gemm_plan_info): the tile choice and work split, no launch
+    const int num_kb = (g.K + ek - 1) / ek;
+    int sp = splits;
+    if (sp > 1) {
+      const int per = (num_kb + sp - 1) / sp;
+      sp = (num_kb + per - 1) / per;
+    }
+    const bool read_c = g.c != nullptr && g.beta != 0.0f;
+    const TailPlan tp = (read_c || sp > 1)
+                            ? TailPlan{}
+                            : plan_tail((long long)((g.M + kRows * cg - 1) / (kRows * cg)) *
+                                            ((g.N + bn - 1) / bn) * g.batch,
+                                        num_kb, cg, bn);
+    g.plan->precision = g.precision;
+    g.plan->cta_group = cg;
+    g.plan->tile_m = kRows * cg;
+    g.plan->tile_n = bn;
+    g.plan->splits = sp;
+    g.plan->tail_pieces = tp.q > 1 ? tp.q : 0;
+    g.plan->k_depth = g.K;
+    return;
+  }
   TcArgs p{};
   p.M = g.M;
   p.N = g.N;
@@ -2744,12 +2766,28 @@ void launch_tc_batched_colmajor(size_t m, size_t n, size_t k, size_t batch, cons
 
 void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float beta, bool ta,
                              bool tb, const float* a, const float* b, const float* c, float* d,
-                             int precision, int tile_n, cudaStream_t st) {
+                             int precision, int tile_n, cudaStream_t st, TcGemmPlan* plan) {
   require_tc(precision);
   if (precision == TK_PREC_3XTF32) {
     // Pack both operands K-major (fp32, unrounded), expand to the split
     // triple along K, run one TF32 GEMM of depth 3 kp.
     const long long kp = (long long)((k + 3) / 4 * 4);
+    if (plan) {
+      TcGemm g;
+      g.M = (int)m;
+      g.N = (int)n;
+      g.K = (int)(3 * kp);
+      g.c = c;
+      g.d_sm = 1;
+      g.d_sn = (long long)m;
+      g.beta = beta;
+      g.precision = TK_PREC_TF32;
+      g.tile_n = tile_n;
+      g.plan = plan;
+      launch_tc_gemm(g, st);
+      plan->a_in_place = plan->b_in_place = 0;
+      return;
+    }
     Scratch spa(st, kScratchPackA, (size_t)m * kp * 4), spb(st, kScratchPackB, (size_t)n * kp * 4);
     Scratch sa3(st, kScratchSplitA, (size_t)m * kp * 12), sb3(st, kScratchSplitB, (size_t)n * kp * 12);
     float *pa = spa.as<float>(), *pb = spb.as<float>(), *a3 = sa3.as<float>(), *b3 = sb3.as<float>();
@@ -2796,6 +2834,24 @@ void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float be
   const bool a_mn = mn_on && !ta && aligned(a) && m <= (1ull << 31) &&
                     ((tf32 && m % 32 == 0) || (in16 && m % 64 == 0));
   const size_t esz = tf32 ? 4 : 2;
+  if (plan) {
+    TcGemm g;
+    g.M = (int)m;
+    g.N = (int)n;
+    g.K = (int)kp;
+    g.a_mn = a_mn;
+    g.c = c;
+    g.d_sm = 1;
+    g.d_sn = (long long)m;
+    g.beta = beta;
+    g.precision = precision;
+    g.tile_n = tile_n;
+    g.plan = plan;
+    launch_tc_gemm(g, st);
+    plan->a_in_place = (a_ok || a_mn) ? 1 : 0;
+    plan->b_in_place = b_ok ? 1 : 0;
+    return;
+  }
   Scratch spa(st, kScratchPackA, (!a_ok && !a_mn) ? (size_t)m * kp * esz : 0);
   Scratch spb(st, kScratchPackB, !b_ok ? (size_t)n * kp * esz : 0);
   void* pa = spa.get();

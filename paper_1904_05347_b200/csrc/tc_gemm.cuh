@@ -8,6 +8,15 @@
 
 namespace tkb {
 
+// What a tensor-core GEMM call runs (tk_gemm_plan_info): filled instead of
+// launching when TcGemm::plan / the colmajor launcher's plan is non-null.
+struct TcGemmPlan {
+  int precision = 0;       // the MMA kind (TF32 for 3xTF32's tripled contraction)
+  int cta_group = 1, tile_m = 0, tile_n = 0, splits = 1, tail_pieces = 0;
+  int a_in_place = 0, b_in_place = 0;  // operands read where they lie (no pack)
+  int k_depth = 0;         // contraction depth the MMAs run (3 kp for 3xTF32)
+};
+
 // Row-major batched GEMM on tensor cores:
 //   D(m, n) = alpha * sum_k A[m][k] * B[n][k] (+ beta * C(m, n))
 // A is [M][K], B is [N][K] (both K contiguous, K % 4 == 0), D(m, n) lives at
@@ -32,6 +41,7 @@ struct TcGemm {
   // MN-major A: its true K extent (K may be padded for B); the TMA zero-fills
   // past it instead of reading beyond the end of A.  0 = K.
   long long a_k = 0;
+  TcGemmPlan* plan = nullptr;  // dry run: fill the plan, launch nothing
 };
 
 void launch_tc_gemm(const TcGemm& g, cudaStream_t st);
@@ -56,7 +66,8 @@ TcKnobs& tc_knobs();
 // where needed.
 void launch_tc_colmajor_gemm(size_t m, size_t n, size_t k, float alpha, float beta, bool ta,
                              bool tb, const float* a, const float* b, const float* c, float* d,
-                             int precision, int tile_n, cudaStream_t st);
+                             int precision, int tile_n, cudaStream_t st,
+                             TcGemmPlan* plan = nullptr);
 
 // Batched column-major C_g = A_g B_g (C zeroed: beta 0), g < batch, operand
 // strides in elements (the reference gemm_batched_strided, gemm.hpp:451-479)

@@ -171,3 +171,20 @@ def test_tuning_db_drives_the_plan(tk, tmp_path):
     assert tk.conv2d_plan_info(s, im, "tf32")["kernel"] == "tc_im2col"
     with pytest.raises(tk.IoError):
         tk.tuning_db_load(str(tmp_path / "missing.ndjson"))
+
+
+def test_gemm_plan_info_host_only(tk):
+    """tk_gemm_plan_info (what tk_gemm_dev would run) is host logic: it
+    answers without a GPU, follows the cost model, the knobs and the DB."""
+    d = tk.gemm_plan_info(tk.GemmShape(1024, 1024, 1024), precision="fp32")
+    assert d["kernel"] == "exact_simt" and d["precision"] == "fp32" and d["splits"] == 1
+    d = tk.gemm_plan_info(tk.GemmShape(1024, 1024, 1024), precision="tf32")
+    assert d["kernel"] == "tc_plain" and d["tile_m"] == 128 * d["cta_group"]
+    assert d["a_in_place"] and d["b_in_place"]  # nn: A MN-major, B K-major, read where they lie
+    d = tk.gemm_plan_info(tk.GemmShape(1024, 1024, 1024), precision="3xtf32")
+    assert d["k_depth"] == 3 * 1024 and not d["a_in_place"]
+    d = tk.gemm_plan_info(tk.GemmShape(512, 512, 512),
+                          options=tk.exec_options("tf32", tile_n=128, cluster=1, split=1))
+    assert (d["cta_group"], d["tile_n"], d["splits"]) == (1, 128, 1)
+    with pytest.raises(tk.ShapeError):
+        tk.gemm_plan_info(tk.GemmShape(0, 4, 4), precision="tf32")

@@ -421,6 +421,7 @@ def test_tc_gemm_tuned_db(tk, oracle, m, n, k, prec, config):
     tk.tuning_db_clear()
     tk.tuning_db_load(db)
     try:
+        assert tk.gemm_plan_info(tk.GemmShape(m, n, k), precision=prec)["tuned"] == 1, config
         a = oracle.fill_random(m * k, 21)
         b = oracle.fill_random(k * n, 22)
         want = oracle.gemm_naive(m, n, k, 1.0, 0.0, 0, 0, a, b, np.zeros(m * n, np.float32))
