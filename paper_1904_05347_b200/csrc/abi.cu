@@ -253,7 +253,8 @@ bool apply_tuned_conv(const tilekit::ConvShape& s, const tk_conv_params* p,
   const int prec = o ? o->precision : TK_PREC_FP32_EXACT;
   if (!p || p->algo != 2 || prec == TK_PREC_FP32_EXACT || !all_auto(o)) return false;
   TunedKnobs k;
-  if (!tuning_db_lookup(s.key(), "im2col", prec, &k)) return false;
+  // bf16 activations in HBM (io flags) are tuned separately ("im2col_io").
+  if (!tuning_db_lookup(s.key(), o->io ? "im2col_io" : "im2col", prec, &k)) return false;
   if (!k.stages && !k.cluster && !k.mode && !k.split) return false;  // the DB keeps the rules
   TcKnobs& t = tc_knobs();
   t.stages = k.stages;

@@ -215,7 +215,7 @@ def _oracle_bf16_in(oracle, idx, img, xb):
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("io", ["bf16", "in_bf16", "out_bf16"])
 @pytest.mark.parametrize("idx", range(len(LAYERS)), ids=[lay[0] for lay in LAYERS])
-def test_bench_layer_bf16_activations(tk, oracle, idx, io):
+def test_bench_layer_bf16_activations(tk, oracle, idx, io, knob_source):
     import torch
     name, r, s, h, c, k = LAYERS[idx]
     if io != "bf16" and idx % 3:
@@ -223,6 +223,11 @@ def test_bench_layer_bf16_activations(tk, oracle, idx, io):
     shape = tk.ConvShape(N, h, h, c, k, r, r, s, True)
     algo = tk.parse_conv_params("im2col")
     opts = tk.exec_options("bf16", io=io)
+    if knob_source == "tuned":
+        # the DB's bf16-activation records (family im2col_io, bench.py's
+        # vgg16_bf16_io / resnet50_bf16_io legs)
+        if io != "bf16" or not tk.conv2d_plan_info(shape, algo, options=opts)["tuned"]:
+            pytest.skip("the DB keeps the rules' plan for this shape / format")
     x, f = _device_inputs(idx)
     xb = x.to(torch.bfloat16)
     xin = xb if io in ("bf16", "in_bf16") else xb.float()  # same values either way

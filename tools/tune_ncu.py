@@ -51,6 +51,7 @@ LAYERS = [(name, 3, 1, h, c, k) for name, h, c, k, _ in VGG16] + \
 PRECISIONS = ("tf32", "bf16")
 EXTRA_SPLITS = ()  # --splits: forced K-split counts added to every mode (small batches)
 SPLITS_ONLY = False  # --splits-only: the rules against the split candidates only
+IO = "fp32"  # --io bf16: BF16 with bf16 activations in HBM (DB family "im2col_io")
 KNOBS = [  # (mode, cluster, split)
     ("auto", 0, 0), ("auto", 0, 1), ("halo", 0, 0), ("pixn", 0, 0), ("pixn", 1, 0),
     ("pixn", 2, 0), ("pixn", 0, 1), ("pixm", 0, 0), ("pointwise", 0, 0), ("pointwise", 0, 1),
@@ -65,7 +66,7 @@ SUFFIX_MODE = {"auto": "", "halo": "_halo", "pixn": "_pixn", "pixm": "_pixm",
 
 def config_name(prec, mode, cluster, split):
     """tilekit::b200::ExecOptions::suffix naming: im2col@<prec>[_c<C>][_mode][_nosplit]."""
-    s = f"im2col@{prec}"
+    s = f"im2col{'_io' if IO != 'fp32' else ''}@{prec}"
     if cluster:
         s += f"_c{cluster}"
     s += SUFFIX_MODE[mode]
@@ -88,7 +89,7 @@ def candidates(tk):
             knobs = ([("auto", 0, 0)] if SPLITS_ONLY else list(KNOBS)) + \
                 [(m, 0, sp) for m in ("auto", "halo", "pixn", "im2col") for sp in EXTRA_SPLITS]
             for mode, cl, sp in knobs:
-                opts = tk.exec_options(prec, cluster=cl, mode=mode, split=sp)
+                opts = tk.exec_options(prec, cluster=cl, mode=mode, split=sp, io=IO)
                 try:
                     plan = tk.conv2d_plan_info(shape, im, options=opts)
                 except tk.TilekitError:
@@ -107,7 +108,7 @@ def run_candidate(tk, torch, c, bufs):
     name, r, s, h, ch, k = LAYERS[c["li"]]
     shape = tk.ConvShape(N, h, h, ch, k, r, r, s, True)
     im = tk.parse_conv_params("im2col")
-    opts = tk.exec_options(c["prec"], cluster=c["cluster"], mode=c["mode"], split=c["split"])
+    opts = tk.exec_options(c["prec"], cluster=c["cluster"], mode=c["mode"], split=c["split"], io=IO)
     x, f, y = bufs[c["li"]]
     ws = torch.empty(max(tk.conv2d_workspace_size(shape, im, options=opts), 4) // 4 + 1,
                      device="cuda")
@@ -119,9 +120,10 @@ def make_bufs(torch):
     gen = torch.Generator(device="cuda").manual_seed(7)
     for li, (name, r, s, h, c, k) in enumerate(LAYERS):
         oh = (h + s - 1) // s
-        bufs[li] = (torch.rand((N, h, h, c), device="cuda", generator=gen) * 2 - 1,
+        dt = torch.bfloat16 if IO != "fp32" else torch.float32
+        bufs[li] = ((torch.rand((N, h, h, c), device="cuda", generator=gen) * 2 - 1).to(dt),
                     torch.rand((r, r, c, k), device="cuda", generator=gen) * 2 - 1,
-                    torch.empty((N, oh, oh, k), device="cuda"))
+                    torch.empty((N, oh, oh, k), device="cuda", dtype=dt))
     return bufs
 
 
@@ -271,7 +273,7 @@ def time_pass(short_path, db_path):
             best[k] = r
     for (layer, prec), r in sorted(best.items()):
         auto = [q for q in recs if q["layer"] == layer and q["precision"] == prec and
-                q["config"] == f"im2col@{prec}"]
+                q["config"] in (f"im2col@{prec}", f"im2col_io@{prec}")]
         a = auto[0]["median_ns"] if auto else float("nan")
         print(f"{layer:16s} {prec:5s} best {r['config']:28s} {r['median_ns'] / 1e3:8.1f} us "
               f"(rules {a / 1e3:8.1f} us) tc {r['tensor_pipe_pct']:5.1f}% dram {r['dram_pct']:5.1f}%")
@@ -289,7 +291,7 @@ def curate(all_path, db_path):
         groups.setdefault((r["problem"], r["precision"]), []).append(r)
     out = []
     for (prob, prec), rs in sorted(groups.items()):
-        rule = [r for r in rs if r["config"] == f"im2col@{prec}"]
+        rule = [r for r in rs if r["config"] in (f"im2col@{prec}", f"im2col_io@{prec}")]
         best = min(rs, key=lambda r: r["median_ns"])
         if rule:
             out.append(rule[0])
@@ -300,7 +302,7 @@ def curate(all_path, db_path):
     with open(db_path, "w") as fh:
         for r in out:
             fh.write(json.dumps(r) + "\n")
-    kept = sum(1 for r in out if not r["config"].endswith(("@tf32", "@bf16")))
+    kept = sum(1 for r in out if not r["config"].endswith(("@tf32", "@bf16")))  # (rules end in @prec)
     print(f"curated DB: {len(out)} records, {kept} non-default choices (>= {MIN_GAIN:.0%} over the rule)")
 
 
@@ -315,11 +317,16 @@ def main():
     ap.add_argument("--batch", type=int, default=32, help="images per layer (bench: 32; configs[1]: 1)")
     ap.add_argument("--which", default="all", choices=["all", "vgg16", "resnet50"])
     ap.add_argument("--splits", default="", help="extra forced K splits, e.g. 4,8,16")
+    ap.add_argument("--io", default="fp32", choices=["fp32", "bf16"],
+                    help="bf16: BF16 convolutions on bf16 activations (precision forced to bf16)")
     ap.add_argument("--splits-only", action="store_true",
                     help="candidates = the rules + the --splits variants only")
     args = ap.parse_args()
-    global N, LAYERS, EXTRA_SPLITS, SPLITS_ONLY
+    global N, LAYERS, EXTRA_SPLITS, SPLITS_ONLY, IO, PRECISIONS
     SPLITS_ONLY = args.splits_only
+    IO = args.io
+    if IO != "fp32":
+        PRECISIONS = ("bf16",)
     N = args.batch
     if args.which == "vgg16":
         LAYERS = LAYERS[:len(VGG16)]
