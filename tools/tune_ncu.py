@@ -291,7 +291,7 @@ def curate(all_path, db_path):
         groups.setdefault((r["problem"], r["precision"]), []).append(r)
     out = []
     for (prob, prec), rs in sorted(groups.items()):
-        rule = [r for r in rs if r["config"] in (f"im2col@{prec}", f"im2col_io@{prec}")]
+        rule = [r for r in rs if r["config"] in (f"im2col@{prec}", f"im2col_io@{prec}")]  # noqa
         best = min(rs, key=lambda r: r["median_ns"])
         if rule:
             out.append(rule[0])
@@ -302,7 +302,7 @@ def curate(all_path, db_path):
     with open(db_path, "w") as fh:
         for r in out:
             fh.write(json.dumps(r) + "\n")
-    kept = sum(1 for r in out if not r["config"].endswith(("@tf32", "@bf16")))  # (rules end in @prec)
+    kept = sum(1 for r in out if "@" in r["config"] and "_" in r["config"].split("@")[1])  # knob tokens
     print(f"curated DB: {len(out)} records, {kept} non-default choices (>= {MIN_GAIN:.0%} over the rule)")
 
 
@@ -317,6 +317,7 @@ def main():
     ap.add_argument("--batch", type=int, default=32, help="images per layer (bench: 32; configs[1]: 1)")
     ap.add_argument("--which", default="all", choices=["all", "vgg16", "resnet50"])
     ap.add_argument("--splits", default="", help="extra forced K splits, e.g. 4,8,16")
+    ap.add_argument("--precisions", default="", help="e.g. 3xtf32 (default tf32,bf16)")
     ap.add_argument("--io", default="fp32", choices=["fp32", "bf16"],
                     help="bf16: BF16 convolutions on bf16 activations (precision forced to bf16)")
     ap.add_argument("--splits-only", action="store_true",
@@ -327,6 +328,8 @@ def main():
     IO = args.io
     if IO != "fp32":
         PRECISIONS = ("bf16",)
+    elif args.precisions:
+        PRECISIONS = tuple(args.precisions.split(","))
     N = args.batch
     if args.which == "vgg16":
         LAYERS = LAYERS[:len(VGG16)]
