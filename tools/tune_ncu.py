@@ -51,6 +51,7 @@ LAYERS = [(name, 3, 1, h, c, k) for name, h, c, k, _ in VGG16] + \
 PRECISIONS = ("tf32", "bf16")
 EXTRA_SPLITS = ()  # --splits: forced K-split counts added to every mode (small batches)
 SPLITS_ONLY = False  # --splits-only: the rules against the split candidates only
+EXTRA_STAGES = ()  # --stages: forced operand-ring depths (rules' operand path)
 IO = "fp32"  # --io bf16: BF16 with bf16 activations in HBM (DB family "im2col_io")
 KNOBS = [  # (mode, cluster, split)
     ("auto", 0, 0), ("auto", 0, 1), ("halo", 0, 0), ("pixn", 0, 0), ("pixn", 1, 0),
@@ -64,7 +65,7 @@ SUFFIX_MODE = {"auto": "", "halo": "_halo", "pixn": "_pixn", "pixm": "_pixm",
                "gather": "_gather", "pointwise": "_pointwise", "im2col": "_im2col"}
 
 
-def config_name(prec, mode, cluster, split):
+def config_name(prec, mode, cluster, split, stages=0):
     """tilekit::b200::ExecOptions::suffix naming: im2col@<prec>[_c<C>][_mode][_nosplit]."""
     s = f"im2col{'_io' if IO != 'fp32' else ''}@{prec}"
     if cluster:
@@ -74,6 +75,8 @@ def config_name(prec, mode, cluster, split):
         s += "_nosplit"
     elif split > 1:
         s += f"_k{split}"
+    if stages:
+        s += f"_s{stages}"
     return s
 
 
@@ -86,21 +89,23 @@ def candidates(tk):
         shape = tk.ConvShape(N, h, h, c, k, r, r, s, True)
         for prec in PRECISIONS:
             seen = {}
-            knobs = ([("auto", 0, 0)] if SPLITS_ONLY else list(KNOBS)) + \
-                [(m, 0, sp) for m in ("auto", "halo", "pixn", "im2col") for sp in EXTRA_SPLITS]
-            for mode, cl, sp in knobs:
-                opts = tk.exec_options(prec, cluster=cl, mode=mode, split=sp, io=IO)
+            knobs = ([("auto", 0, 0, 0)] if SPLITS_ONLY or EXTRA_STAGES else
+                     [kn + (0,) for kn in KNOBS]) + \
+                [(m, 0, sp, 0) for m in ("auto", "halo", "pixn", "im2col") for sp in EXTRA_SPLITS] + \
+                [("auto", 0, 0, sg) for sg in EXTRA_STAGES]
+            for mode, cl, sp, sg in knobs:
+                opts = tk.exec_options(prec, cluster=cl, mode=mode, split=sp, io=IO, stages=sg)
                 try:
                     plan = tk.conv2d_plan_info(shape, im, options=opts)
                 except tk.TilekitError:
                     continue
                 key = json.dumps({k2: v for k2, v in plan.items() if k2 != "tuned"}, sort_keys=True)
-                if key in seen and not (mode == "auto" and sp == 0):
-                    continue
+                if sg == 0 and key in seen and not (mode == "auto" and sp == 0):
+                    continue  # (plan_info does not show the ring depth: keep stage variants)
                 seen[key] = True
                 out.append(dict(layer=name, li=li, problem=shape.key(), prec=prec, mode=mode,
-                                cluster=cl, split=sp, config=config_name(prec, mode, cl, sp),
-                                plan=plan))
+                                cluster=cl, split=sp, stages=sg,
+                                config=config_name(prec, mode, cl, sp, sg), plan=plan))
     return out
 
 
@@ -108,7 +113,8 @@ def run_candidate(tk, torch, c, bufs):
     name, r, s, h, ch, k = LAYERS[c["li"]]
     shape = tk.ConvShape(N, h, h, ch, k, r, r, s, True)
     im = tk.parse_conv_params("im2col")
-    opts = tk.exec_options(c["prec"], cluster=c["cluster"], mode=c["mode"], split=c["split"], io=IO)
+    opts = tk.exec_options(c["prec"], cluster=c["cluster"], mode=c["mode"], split=c["split"], io=IO,
+                           stages=c.get("stages", 0))
     x, f, y = bufs[c["li"]]
     ws = torch.empty(max(tk.conv2d_workspace_size(shape, im, options=opts), 4) // 4 + 1,
                      device="cuda")
@@ -201,7 +207,7 @@ def shortlist(csv_path, launches_path, out_path):
         best = cs[0]["ncu_us"]
         keep = [c for c in cs if c["ncu_us"] <= 1.15 * best][:4]
         for c in cs:
-            if c["mode"] == "auto" and c["split"] == 0 and c not in keep:
+            if c["mode"] == "auto" and c["split"] == 0 and not c.get("stages") and c not in keep:
                 keep.append(c)
         short += keep
         print(f"{key[0]:42s} {key[1]:5s} " + "  ".join(
@@ -320,10 +326,12 @@ def main():
     ap.add_argument("--precisions", default="", help="e.g. 3xtf32 (default tf32,bf16)")
     ap.add_argument("--io", default="fp32", choices=["fp32", "bf16"],
                     help="bf16: BF16 convolutions on bf16 activations (precision forced to bf16)")
+    ap.add_argument("--stages", default="", help="forced operand-ring depths, e.g. 3,4,6")
     ap.add_argument("--splits-only", action="store_true",
                     help="candidates = the rules + the --splits variants only")
     args = ap.parse_args()
-    global N, LAYERS, EXTRA_SPLITS, SPLITS_ONLY, IO, PRECISIONS
+    global N, LAYERS, EXTRA_SPLITS, SPLITS_ONLY, IO, PRECISIONS, EXTRA_STAGES
+    EXTRA_STAGES = tuple(int(v) for v in args.stages.split(",") if v)
     SPLITS_ONLY = args.splits_only
     IO = args.io
     if IO != "fp32":
