@@ -3016,6 +3016,16 @@ bool prefer_im2col(const ConvGeom& g, int precision) {
   return false;
 }
 
+// 3xTF32 runs one TF32 convolution over 3C channels; the operand-path rules
+// that depend on the channel count judge the caller's C (measured with the
+// tuner: halo tiles for VGG conv1_2 / conv2_x in 3xTF32, 1326 -> 939 us on
+// conv1_2, while the 3C view had sent them to pixel boxes).
+thread_local int t_split3_div = 1;
+struct Split3Scope {
+  Split3Scope() { t_split3_div = 3; }
+  ~Split3Scope() { t_split3_div = 1; }
+};
+
 ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
   ConvPlan c;
   const long long K = (long long)g.R * g.S * g.C;
@@ -3097,7 +3107,8 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
     // Halo mode: small-feature stride-1 layers whose tap re-reads of the
     // input would otherwise dominate the L2->SM traffic.
     const bool halo_ok = g.stride == 1 && g.R * g.S <= 9 && g.S <= 3 && g.K % 32 == 0 &&
-                         ((g.K <= 128 && g.C <= 128) || (force && std::string(force).rfind("halo", 0) == 0));
+                         ((g.K <= 128 && g.C / t_split3_div <= 128) ||
+                          (force && std::string(force).rfind("halo", 0) == 0));
     c.halo = halo_ok && !(force && std::string(force).rfind("halo", 0) != 0);
     const bool halo_geom = g.stride == 1 && g.R * g.S <= 9 && g.S <= 3 && g.K % 32 == 0;
     // Between halo and pixel boxes for >= 128 channels the deciding factor
@@ -3105,7 +3116,7 @@ ConvPlan plan_conv_impl(const ConvGeom& g, int precision) {
     // profiles/r01_tune_*_knobs.ndjson): full waves favour pixN (VGG
     // conv2_2, 3% faster), a mostly idle last wave favours halo's 4x more,
     // narrower tiles (ResNet res4a_branch2b: 30 vs 40 us).
-    if (halo_geom && g.C >= 128 && g.K <= 256 && !force && mode == TK_TC_AUTO) {
+    if (halo_geom && g.C / t_split3_div >= 128 && g.K <= 256 && !force && mode == TK_TC_AUTO) {
       const int pcg = g.K >= 2 * kRows ? 2 : 1;
       const BoxShape pb = pick_box(g, true, pcg);
       if (pb.wb != 0) {
@@ -3515,7 +3526,10 @@ void launch_narrow_halo(const ConvGeom& g, const ConvPlan& c, const float* in, c
 
 size_t tc_conv_workspace(const ConvGeom& g, int precision) {
   if (precision == TK_PREC_3XTF32)
+  {
+    Split3Scope s3;
     return split3_bytes_in(g) + split3_bytes_filt(g) + tc_conv_workspace(tripled(g), TK_PREC_TF32);
+  }
   const ConvPlan c = plan_conv(g, precision);
   return c.filt_bytes + c.in_bytes + c.part_bytes + align256(c.tail.bytes);
 }
@@ -3528,6 +3542,7 @@ void launch_tc_conv(const ConvGeom& g, const float* in, const float* filt, float
     // The same convolution over 3C channels: [x | x | x_lo] against
     // [f_hi | f_lo | f_hi], as one TF32 convolution (see split3_*).
     const ConvGeom g3 = tripled(g);
+    Split3Scope s3;
     char* w = static_cast<char*>(ws);
     float* x3 = reinterpret_cast<float*>(w);
     float* f3 = reinterpret_cast<float*>(w + split3_bytes_in(g));
@@ -3763,7 +3778,10 @@ TcConvInfo tc_conv_info(const ConvGeom& g, int precision) {
   TcConvInfo r;
   if (precision == TK_PREC_3XTF32) {
     // One TF32 convolution over 3C channels ([x | x | x_lo] . [f_hi | f_lo | f_hi]).
-    r = tc_conv_info(tripled(g), TK_PREC_TF32);
+    {
+      Split3Scope s3;
+      r = tc_conv_info(tripled(g), TK_PREC_TF32);
+    }
     r.precision = TK_PREC_3XTF32;
     return r;
   }
