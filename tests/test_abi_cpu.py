@@ -188,3 +188,35 @@ def test_gemm_plan_info_host_only(tk):
     assert (d["cta_group"], d["tile_n"], d["splits"]) == (1, 128, 1)
     with pytest.raises(tk.ShapeError):
         tk.gemm_plan_info(tk.GemmShape(0, 4, 4), precision="tf32")
+
+
+def test_committed_tuning_dbs_load_and_steer_plans(tk):
+    """The DBs bench.py loads parse (the reference's NDJSON schema + the B200
+    keys), and the plan queries report their choices -- host logic, no GPU."""
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    conv_db = os.path.join(root, "profiles", "r02_tune_ncu.ndjson")
+    gemm_db = os.path.join(root, "profiles", "r02_tune_gemm.ndjson")
+    tk.tuning_db_clear()
+    try:
+        assert tk.tuning_db_load(conv_db) > 0 and tk.tuning_db_load(gemm_db) > 0
+        # a tuned GEMM record steers the GEMM plan
+        rec = next(json.loads(ln) for ln in open(gemm_db)
+                   if "_" in json.loads(ln)["config"].split("@")[1])
+        m, n, k = (int(v) for v in re.match(r"gemm_nn_m(\d+)_n(\d+)_k(\d+)", rec["problem"]).groups())
+        assert tk.gemm_plan_info(tk.GemmShape(m, n, k), precision=rec["precision"])["tuned"] == 1
+        # a tuned conv record (fp32 activations) steers the conv plan
+        for ln in open(conv_db):
+            r = json.loads(ln)
+            fam, rest = r["config"].split("@")
+            if fam == "im2col" and "_" in rest and r["problem"].startswith("conv_n32_"):
+                g = re.match(r"conv_n(\d+)_(\d+)x(\d+)x(\d+)_k(\d+)_f(\d+)x(\d+)_s(\d+)_", r["problem"])
+                nb, h, w, c, kk, fr, fc, st = (int(v) for v in g.groups())
+                shape = tk.ConvShape(nb, h, w, c, kk, fr, fc, st, True)
+                assert tk.conv2d_plan_info(shape, tk.parse_conv_params("im2col"),
+                                           r["precision"])["tuned"] == 1, r["config"]
+                break
+        else:
+            pytest.fail("no tuned conv record")
+    finally:
+        tk.tuning_db_clear()
