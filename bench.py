@@ -755,6 +755,8 @@ def main():
             ts = []
             for _ in range(reps):
                 flush.zero_()
+                if prespin:
+                    torch.cuda._sleep(prespin)  # (see the timed steps)
                 a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a_.record(stream)
                 for L in layers:
@@ -784,6 +786,8 @@ def main():
             ts = []
             for _ in range(reps):
                 flush.zero_()
+                if prespin:
+                    torch.cuda._sleep(prespin)  # (see the timed steps)
                 a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a_.record(stream)
                 for L, xb, yb in zip(layers, xb_, yb_):
@@ -829,6 +833,8 @@ def main():
             torch.cuda.synchronize()
         ts = []
         for _ in range(5):
+            if prespin:
+                torch.cuda._sleep(prespin)  # (see the timed steps)
             a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a_.record(stream)
             if g_b1 is not None:
@@ -897,6 +903,8 @@ def main():
             ts = []
             for _ in range(3):
                 flush.zero_()
+                if prespin:
+                    torch.cuda._sleep(prespin)  # (see the timed steps)
                 a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a_.record(stream)
                 if g_rn is not None:
@@ -942,6 +950,8 @@ def main():
         torch.cuda.synchronize()
         a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         flush.zero_()
+        if prespin:
+            torch.cuda._sleep(prespin)
         a_.record(stream)
         rn_tiled(stream)
         b_.record(stream)
